@@ -1,0 +1,395 @@
+"""Benchmark: DLRM training samples/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+                    [--impl ours|reference]
+
+* workload (default ``c3``): the paper's Big Basin shape — 8 tables x 1M rows,
+  d=64, 512 dense features, multi-hot pooling U[1,100], bottom 512-512-64,
+  top 1024-1024-1024-1, 2048 samples per GPU (weak scaling).  It is the
+  configuration BASELINE.json quotes at 1/2/4/8 GPUs and the only one with a
+  published training-throughput number (paper: ~33.0k samples/s, V100,
+  Caffe2).  ``--config c2`` runs the Criteo-Kaggle shape.
+* ``value``: whole-job samples/s with the batch pool resident in HBM; each
+  timed step = the D2D load of the step's batch into the engine's input
+  buffers + one replay of the captured training-step graph.  L2 is flushed
+  (256 MiB write) between timed steps, outside the timed events.
+* ``e2e``: the same step through the public engine API from PINNED HOST
+  buffers — H2D of dense rows, offsets, indices and labels, the step, and a
+  D2H read of the step result (loss sum, correct count) — every step.
+* ``roofline``: the dominant kernel of the step, timed alone with CUDA events
+  on its launch stream, against MEASURED_PEAKS.json.
+* ``cpu_baseline``: the reference algorithm (oracle/port.py, float64, the
+  reference's own numpy/BLAS path) on this host's cores over a bounded
+  sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KAGGLE = [1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683,
+          8351593, 3194, 27, 14992, 5461306, 10, 5652, 2173, 4, 7046547, 18,
+          15, 286181, 105, 142572]
+TERABYTE_40M = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63,
+                38532951, 2953546, 403346, 10, 2208, 11938, 155, 4, 976, 14,
+                39979771, 25641295, 39664984, 585935, 12972, 108, 36]
+
+CONFIGS = {
+    "c1": dict(name="c1: 8x1e4, d=16, bot 13-512-256-64-16, top 512-256-1, "
+               "B=128, 1 idx", tables=[10 ** 4] * 8, d=16,
+               bot=[13, 512, 256, 64, 16], top=[512, 256, 1], batch=128, k=1,
+               fixed=True, published=None),
+    "c2": dict(name="Criteo-Kaggle-shaped synthetic: 26 tables (Kaggle "
+               "cardinalities), d=16, bot 13-512-256-64-16, top 512-256-1, "
+               "B=2048, 1 idx", tables=KAGGLE, d=16,
+               bot=[13, 512, 256, 64, 16], top=[512, 256, 1], batch=2048, k=1,
+               fixed=True, published=None),
+    "c3": dict(name="Big Basin: 8 tables x 1M rows, d=64, 512 dense, pooling "
+               "U[1,100], bot 512-512-64, top 1024-1024-1024-1, B=2048/GPU",
+               tables=[10 ** 6] * 8, d=64, bot=[512, 512, 64],
+               top=[1024, 1024, 1024, 1], batch=2048, k=100, fixed=False,
+               published=33000.0),
+    "c4": dict(name="Criteo-Terabyte-shaped synthetic: 26 tables (40M cap), "
+               "d=128, bot 13-512-256-128, top 1024-1024-512-256-1, B=32768 "
+               "global", tables=TERABYTE_40M, d=128, bot=[13, 512, 256, 128],
+               top=[1024, 1024, 512, 256, 1], batch=32768, k=1, fixed=True,
+               published=None, global_batch=True),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+            "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.samples = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# the reference CPU arm / baseline (oracle port = the reference algorithm)
+
+def cpu_port_rate(c, batch, steps, warmup, seed=0):
+    """samples/s of the float64 reference algorithm on this host."""
+    from oracle import port
+    from paper_1906_00091_b200.rng import RandomBatchSource
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    # tables capped at 2^20 rows per table for host memory (per-sample compute
+    # does not depend on the row count); the cap is reported in `sample`
+    cap = 1 << 20
+    tables = [min(m, cap) for m in c["tables"]]
+    model = port.init_params(tables, c["d"], c["bot"], c["top"], seed)
+    src = RandomBatchSource(tables, c["bot"][0], batch, c["k"], c["fixed"], seed=seed)
+    hbs = [src.next_batch() for _ in range(steps + warmup)]
+    for hb in hbs[:warmup]:
+        port.train_step(model, hb.dense, hb.offsets, hb.indices, hb.labels, 0.1)
+    t0 = time.perf_counter()
+    for hb in hbs[warmup:]:
+        port.train_step(model, hb.dense, hb.offsets, hb.indices, hb.labels, 0.1)
+    dt = time.perf_counter() - t0
+    sample = (f"oracle/port.py float64 train_step (reference algorithm), batch "
+              f"{batch} of the {c['batch']}-sample workload, {steps} timed steps "
+              f"after {warmup} warm-up, tables capped at {cap} rows")
+    return batch * steps / dt, threads, sample, dt / steps
+
+
+def run_reference(args, c, rank, world):
+    if rank != 0:
+        return
+    batch = max(16, min(c["batch"], int(args.cpu_batch)))
+    rate, threads, sample, per = cpu_port_rate(c, batch, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": "train samples/s", "value": rate,
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (reference random source)",
+            "config": {"workload": c["name"], "global_batch": c["batch"] * world},
+            "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": rate, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def algorithmic(c, B, hbs, eng):
+    """Per-step algorithmic bytes/flops of the stages."""
+    d = c["d"]
+    fwd = bwd = 0.0
+    for hb in hbs[:1]:
+        for o, i in zip(hb.offsets, hb.indices):
+            nnz = int(i.size)
+            u = int(np.unique(i).size)
+            fwd += nnz * (4 * d + 8) + (B + 1) * 8 + B * 4 * d
+            bwd += B * 4 * d + nnz * 8 + (B + 1) * 8 + 2 * u * 4 * d
+    fl = 0.0
+    for li, l in enumerate(eng.layers):
+        n, k = l.n_out, l.n_in
+        fl += 2 * B * k * n * (2 if li == 0 else 3)
+    return fwd, bwd, fl
+
+
+def run_ours(args, c, rank, world, dist):
+    import torch
+    from paper_1906_00091_b200 import DlrmConfig, init_model, _lib
+    from paper_1906_00091_b200.rng import RandomBatchSource
+    from paper_1906_00091_b200.trainer import StepEngine
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda")
+    B = c["batch"] // world if c.get("global_batch") else c["batch"]
+    cfg = DlrmConfig(c["tables"], c["d"], c["bot"], c["top"], seed=0)
+    model = init_model(cfg, table_init="device")
+    src = RandomBatchSource(c["tables"], c["bot"][0], B, c["k"], c["fixed"],
+                            seed=1 + rank)
+    P = args.pool
+    hbs = [src.next_batch() for _ in range(P)]
+    caps = [max(int(hb.indices[t].size) for hb in hbs) for t in range(cfg.num_tables)]
+    caps = [max(cp, B * c["k"] if c["fixed"] else cp) for cp in caps]
+    if not c["fixed"]:
+        caps = [B * c["k"]] * cfg.num_tables  # worst case: graph valid for any batch
+    eng = StepEngine(model, B, caps, lr=0.1)
+
+    # device-resident pool and pinned host pool
+    def dev_batch(hb):
+        return (torch.as_tensor(hb.dense.astype(np.float32), device=dev),
+                [torch.as_tensor(o, device=dev) for o in hb.offsets],
+                [torch.as_tensor(i, device=dev) for i in hb.indices],
+                torch.as_tensor(hb.labels.astype(np.float32), device=dev))
+
+    def pin_batch(hb):
+        return (torch.as_tensor(hb.dense.astype(np.float32)).pin_memory(),
+                [torch.as_tensor(o).pin_memory() for o in hb.offsets],
+                [torch.as_tensor(i).pin_memory() for i in hb.indices],
+                torch.as_tensor(hb.labels.astype(np.float32)).pin_memory())
+
+    dpool = [dev_batch(hb) for hb in hbs]
+    hpool = [pin_batch(hb) for hb in hbs]
+    h2d_bytes = int(np.mean([hp[0].nbytes + sum(o.nbytes for o in hp[1])
+                             + sum(i.nbytes for i in hp[2]) + hp[3].nbytes
+                             for hp in hpool]))
+    stream = torch.cuda.current_stream()
+
+    # warm-up (eager first step, then capture the graph)
+    eng.load(*dpool[0])
+    eng.run()
+    torch.cuda.synchronize()
+    use_graph = not args.no_graph
+    if use_graph:
+        eng.capture()
+    launches = eng.launches_per_step
+    for w in range(args.warmup):
+        eng.load(*dpool[w % P])
+        eng.run()
+    torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for s in range(K):
+            flush.fill_(s & 0xff)
+            starts[s].record(stream)
+            eng.load(*dpool[s % P])
+            eng.run()
+            ends[s].record(stream)
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * K / (ms / 1e3)
+    eng.check_errors()
+
+    # e2e through the public engine API from pinned host memory
+    res_host = torch.zeros((K, 2), dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    e0.record(stream)
+    for s in range(K):
+        hp = hpool[s % P]
+        eng.load(*hp)
+        eng.run()
+        res_host[s].copy_(eng.stats, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = world * B * K / (e2e_ms / 1e3)
+    loss_last = float(res_host[K - 1, 0]) / B
+
+    # per-stage breakdown and the dominant kernel's roofline
+    stages = eng.profile_stages(reps=5, flush=flush)
+    fwd_b, bwd_b, flops = algorithmic(c, B, hbs, eng)
+    emb_fwd_ms = stages.get("embedding_fwd", float("nan"))
+    emb_bwd_ms = stages.get("embedding_bwd_sgd", float("nan"))
+    pk, pk_kind = peaks()
+    hbm = pk["hbm_gbs"]
+    cands = {
+        "embedding_fwd": (fwd_b / (emb_fwd_ms / 1e3) / 1e9, emb_fwd_ms, fwd_b),
+        "embedding_bwd_sgd": (bwd_b / (emb_bwd_ms / 1e3) / 1e9, emb_bwd_ms, bwd_b),
+    }
+    groups = {"embedding_fwd": stages["embedding_fwd"],
+              "embedding_bwd_sgd": stages["embedding_bwd_sgd"],
+              "mlp": stages["mlp_total"],
+              "interaction": stages["interaction_fwd"] + stages["interaction_bwd"]}
+    dom = max(groups, key=lambda k: groups[k])
+    if dom in cands:
+        gbs, kms, kb = cands[dom]
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": gbs, "peak": hbm,
+                    "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
+                    "peak_kind": pk_kind, "algorithmic_bytes": kb,
+                    "ms": kms}
+    else:
+        mlp_fl = flops
+        tf = mlp_fl / (stages["mlp_total"] / 1e3) / 1e12
+        roofline = {"kernel": dom, "bound": "tensor", "achieved": tf,
+                    "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                    "frac": tf / pk["bf16_tflops"], "traffic": None,
+                    "peak_kind": pk_kind + " bf16 (tf32 = 1/2, 3xTF32 = 1/6)",
+                    "ms": groups[dom]}
+    emb_roof = {k: {"GB/s": v[0], "ms": v[1], "bytes": v[2], "frac": v[0] / hbm}
+                for k, v in cands.items()}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            batch = max(16, min(c["batch"], int(args.cpu_batch)))
+            rate, threads, sample, _ = cpu_port_rate(c, batch, 2, 1)
+            cpu = {"value": rate, "unit": "samples/s", "cores": threads,
+                   "kind": "port", "sample": sample}
+        line = {
+            "metric": "train samples/s", "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": (value / c["published"]) if c["published"] else None,
+            "dtype": "f32", "data": "synthetic (reference random source; "
+            "device-seeded tables)",
+            "config": {"workload": c["name"], "global_batch": B * world,
+                       "per_gpu_batch": B, "parallelism": f"hybrid{world}",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "graph": use_graph},
+            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / K},
+            "gpu_launches": int(launches) * K if launches else None,
+            "roofline": roofline, "embedding_roofline": emb_roof,
+            "stages_ms": stages, "mlp_gflop_per_step": flops / 1e9,
+            "loss_last": loss_last, "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=4)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-batch", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    c = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, c, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    run_ours(args, c, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

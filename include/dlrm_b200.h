@@ -1,0 +1,213 @@
+/*
+ * dlrm_b200.h — C ABI of libdlrmb200.so, the sm_100a kernels behind the
+ * DLRM training step (arXiv 1906.00091).
+ *
+ * The reference (dlrmkit) is pure Python/numpy and has no FFI; its operator
+ * API *is* the set of Python functions re-exported by
+ * /root/reference/pkg/src/dlrmkit/__init__.py:10-80.  Each entry point below
+ * replaces the numerical core of one of those functions and cites it.  The
+ * Python package paper_1906_00091_b200 binds these with ctypes (see
+ * INTEGRATION.md) and keeps the reference's names, argument meanings and
+ * exceptions.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless documented otherwise; the
+ *     caller owns every buffer; the library never allocates caller-visible
+ *     memory (workspaces are sized by *_workspace_size and passed in).
+ *   - Every call is asynchronous on the given stream and never synchronises
+ *     the host, so a whole training step can be captured in a CUDA graph.
+ *   - Return codes: 0 ok, 1 invalid argument, 2 CUDA error; the message is
+ *     available from dlrm_last_error() (thread-local).
+ *   - All floating-point work is fp32; index work is int64/uint32 and
+ *     bit-exact with the reference.
+ */
+#ifndef DLRM_B200_H
+#define DLRM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* dlrm_stream_t; /* a cudaStream_t */
+
+#define DLRM_MAX_TABLES 128
+#define DLRM_MAX_FEATURES 129
+
+/* One table's bags for a multi-table call (host struct, passed by value to
+ * the kernels).  Mirrors SparseBatch (ref embedding.py:74-124) plus where the
+ * table lives in the rank's concatenated weight buffer and where its pooled
+ * rows go.  All tables of one call have the same num_bags (the batch). */
+typedef struct {
+  const int64_t* offsets;  /* [num_bags+1], offsets[0]==0, terminal == nnz   */
+  const int64_t* indices;  /* [capacity] (first offsets[num_bags] are live) */
+  const float* weights;    /* [capacity] per-index weights or NULL          */
+  int64_t row_base;        /* first row of this table in W_all              */
+  int64_t num_rows;        /* m                                            */
+  int64_t out_offset;      /* element offset of bag 0's row in out / grad   */
+  int64_t capacity;        /* index slots reserved (>= nnz); sort size      */
+  int64_t table_id;        /* reported in LookupIndexError                  */
+} dlrm_table_desc;
+
+/* ---- embedding bags (north_star subsystem 1) --------------------------- */
+
+/* Reset the error records: err_pos[0..nt) = INT64_MAX, *err_flag = 0. */
+int dlrm_err_reset(int64_t* err_pos, int32_t nt, int32_t* err_flag,
+                   dlrm_stream_t stream);
+
+/* Pooled lookup S = A^T W for nt tables (ref lookup_batch,
+ * embedding.py:155-179): out[out_offset_t + j*out_stride + c] =
+ * strict ascending-position fold over bag j of W[row_base+idx]*a.  Empty bags
+ * give zero rows.  Out-of-range indices are skipped and recorded as
+ * atomicMin(err_pos[t], position) + *err_flag = 1 (ref check_bounds,
+ * embedding.py:117-124). */
+int dlrm_emb_fwd(const float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                 int32_t nt, int64_t num_bags, float* out, int64_t out_stride,
+                 int64_t* err_pos, int32_t* err_flag, dlrm_stream_t stream);
+
+/* Bytes of scratch needed by dlrm_emb_bwd_sgd / dlrm_emb_bwd_coalesce for
+ * total_capacity index slots over total_rows rows. */
+size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity, int64_t total_rows);
+
+/* Sparse backward fused with the SGD row update (ref lookup_backward,
+ * embedding.py:182-210, then sgd_step_rows, optim.py:38-46):
+ *   for every touched row r:  W[r] -= lr * fold_{k: idx_k = r, ascending k}
+ *                                        grad[bag(k)] * a_k
+ * via a stable radix sort of (row, position) pairs and a deterministic
+ * segmented fold — no float atomics.  grad rows are read at
+ * grad[out_offset_t + j*grad_stride].  If *err_flag is set no row is
+ * written (the reference raises before mutating). */
+int dlrm_emb_bwd_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                     int32_t nt, int64_t num_bags, const float* grad,
+                     int64_t grad_stride, float lr, const int32_t* err_flag,
+                     int64_t total_rows, void* workspace, size_t ws_bytes,
+                     dlrm_stream_t stream);
+
+/* lookup_backward parity path for ONE table: coalesced SparseRowGrad.
+ * rows_out[u] ascending unique local rows, values_out[u*dim..] their folded
+ * gradients, *num_unique = u (device int64).  Buffers sized for nnz rows.
+ * Out-of-range indices are recorded in err_pos[0] / *err_flag like
+ * dlrm_emb_fwd (the caller raises LookupIndexError). */
+int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
+                          int64_t num_bags, const float* grad,
+                          int64_t grad_stride, int64_t* rows_out,
+                          float* values_out, int64_t* num_unique,
+                          int64_t* err_pos, int32_t* err_flag,
+                          void* workspace, size_t ws_bytes,
+                          dlrm_stream_t stream);
+
+/* W[rows[i]] -= lr * values[i]  (ref sgd_step_rows, optim.py:38-46). */
+int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
+                  const float* values, int64_t n, float lr,
+                  dlrm_stream_t stream);
+
+/* ---- dot interaction (north_star subsystem 2) -------------------------- */
+
+/* Feature f of sample b lives at feat[f] + b*feat_stride[f] (d floats);
+ * f = 0 is the bottom-MLP output, f = 1+t table t.  (host arrays) */
+typedef struct {
+  const float* feat[DLRM_MAX_FEATURES];
+  int64_t feat_stride[DLRM_MAX_FEATURES];
+} dlrm_features;
+
+/* out[b*ld_out + :] = [z0 | z_i.z_j for i<j row-major] (ref interact,
+ * model.py:218-242); columns [d+P, pad_to) are written as zeros. */
+int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf, int64_t dim,
+                      int64_t batch, float* out, int64_t ld_out,
+                      int64_t pad_to, dlrm_stream_t stream);
+
+/* grad_feat[f] + b*grad_stride[f] = [f==0] gout[b,:d] + sum_{j!=f} g_fj z_j
+ * (ref interact_backward, model.py:245-268).  grad_feat / grad_stride are
+ * HOST arrays of nf entries (device pointers / element strides). */
+int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf, int64_t dim,
+                      int64_t batch, const float* gout, int64_t ld_gout,
+                      float* const* grad_feat, const int64_t* grad_stride,
+                      int32_t relu_mask_f0, dlrm_stream_t stream);
+/* relu_mask_f0 != 0 multiplies feature 0's gradient by (z0 > 0): the
+ * bottom MLP's last ReLU folded into the interaction backward (training
+ * step only; the API-level interact_backward passes 0). */
+
+/* ---- MLP layers (north_star subsystem 2) ------------------------------- */
+
+enum { DLRM_ACT_IDENTITY = 0, DLRM_ACT_RELU = 1 };
+
+/* Y[m, n] = act((X W^T)[m, n] + b[n]) for m < M, n < N (ref mlp_forward,
+ * model.py:142-156 with matmul dense.py:62-78).  X: M x K (ldx), W: N x K
+ * (ldw).  Columns [N, pad_n) of Y are zeroed. */
+int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw,
+                    const float* b, float* Y, int64_t ldy, int64_t M,
+                    int64_t N, int64_t K, int64_t pad_n, int32_t act,
+                    dlrm_stream_t stream);
+
+/* dX[m, k] = (gZ W)[m, k] * (mask ? (mask[m, k] > 0) : 1)
+ * (ref mlp_backward_trace, model.py:173-179; mask = the previous layer's
+ * ReLU output, whose positivity equals act'(z) > 0). */
+int dlrm_linear_bwd_data(const float* gZ, int64_t ldg, const float* W,
+                         int64_t ldw, const float* mask, int64_t ldm,
+                         float* dX, int64_t ldx, int64_t M, int64_t N,
+                         int64_t K, dlrm_stream_t stream);
+
+size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N, int64_t K);
+
+/* dW = gZ^T X (N x K), db = column sums of gZ (ref mlp_backward,
+ * model.py:191-208, as a plain fp32 reduction over the batch with a fixed
+ * split order — deterministic).  If dW/db are NULL they are not stored.
+ * If W_upd/b_upd are non-NULL the SGD step W -= lr*dW, b -= lr*db
+ * (ref sgd_step, optim.py:31-35) is fused in, skipped when *err_flag != 0. */
+int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X,
+                           int64_t ldx, int64_t M, int64_t N, int64_t K,
+                           float* dW, int64_t lddw, float* db,
+                           float* W_upd, int64_t ldw, float* b_upd, float lr,
+                           const int32_t* err_flag, void* workspace,
+                           size_t ws_bytes, dlrm_stream_t stream);
+
+/* ---- loss head (last top layer, N = 1) --------------------------------- */
+
+/* z[m] = A[m,:K] . w + b;  prob = sigmoid(z);  per-sample BCE from logits;
+ * g[m] = (sigmoid(z) - y) / n_total;  stats[0] += sum(per) (fp32, fixed
+ * order), stats[1] += #((p > 0.5) == (y > 0.5))   (ref bce_from_logits,
+ * model.py:448-461; accuracy parallel.py:286).  logits/prob may be NULL. */
+size_t dlrm_bce_head_workspace_size(int64_t M);
+int dlrm_bce_head(const float* A, int64_t lda, const float* w, const float* b,
+                  int64_t M, int64_t K, const float* y, float n_total,
+                  float* logits, float* prob, float* grad_z, float* per_sample,
+                  float* stats, void* workspace, size_t ws_bytes,
+                  dlrm_stream_t stream);
+
+/* Backward through the N = 1 head: dA[m,k] = g[m]*w[k] (* (A[m,k] > 0) when
+ * relu_mask, i.e. A is a ReLU output); dw[k] = sum_m g[m]*A[m,k];
+ * db = sum_m g[m]; optional fused SGD (w -= lr*dw, b -= lr*db). */
+size_t dlrm_head_bwd_workspace_size(int64_t M, int64_t K);
+int dlrm_head_bwd(const float* A, int64_t lda, const float* w, const float* g,
+                  int64_t M, int64_t K, float* dA, int64_t ldda,
+                  int32_t relu_mask, float* dw, float* db, float* w_upd,
+                  float* b_upd, float lr,
+                  const int32_t* err_flag, void* workspace, size_t ws_bytes,
+                  dlrm_stream_t stream);
+
+/* out[m, n] = g[m, n] * (act[m, n] > 0)   (ref activation_grad relu,
+ * dense.py:110-120, applied as in model.py:177). */
+int dlrm_relu_grad(const float* g, int64_t ldg, const float* act, int64_t lda,
+                   float* out, int64_t ldo, int64_t M, int64_t N,
+                   dlrm_stream_t stream);
+
+/* ---- dense SGD ---------------------------------------------------------- */
+
+/* p[i] -= lr * g[i], product rounded first (ref sgd_step, optim.py:31-35);
+ * skipped when err_flag != NULL and *err_flag != 0. */
+int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
+                   const int32_t* err_flag, dlrm_stream_t stream);
+
+/* ---- misc --------------------------------------------------------------- */
+
+/* Count of this library's kernel launches since load (for bench.py). */
+int64_t dlrm_launch_count(void);
+const char* dlrm_last_error(void);
+const char* dlrm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLRM_B200_H */

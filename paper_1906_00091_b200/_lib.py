@@ -1,0 +1,160 @@
+"""ctypes binding of libdlrmb200.so (the C ABI in include/dlrm_b200.h).
+
+There is no CPU fallback: if the library is missing, or a tensor handed to a
+kernel is not a CUDA tensor, the call fails loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdlrmb200.so")
+
+MAX_TABLES = 128
+MAX_FEATURES = 129
+ACT = {"identity": 0, "relu": 1}
+
+_i64, _i32, _f32, _vp, _sz = C.c_int64, C.c_int32, C.c_float, C.c_void_p, C.c_size_t
+
+
+class TableDesc(C.Structure):
+    _fields_ = [("offsets", _vp), ("indices", _vp), ("weights", _vp),
+                ("row_base", _i64), ("num_rows", _i64), ("out_offset", _i64),
+                ("capacity", _i64), ("table_id", _i64)]
+
+
+class Features(C.Structure):
+    _fields_ = [("feat", _vp * MAX_FEATURES),
+                ("feat_stride", _i64 * MAX_FEATURES)]
+
+
+_SIGS = {
+    "dlrm_err_reset": [_vp, _i32, _vp, _vp],
+    "dlrm_emb_fwd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
+    "dlrm_emb_bwd_sgd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _f32, _vp,
+                         _i64, _vp, _sz, _vp],
+    "dlrm_emb_bwd_coalesce": [_i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _sz, _vp],
+    "dlrm_sgd_rows": [_vp, _i64, _vp, _vp, _i64, _f32, _vp],
+    "dlrm_interact_fwd": [_vp, _i32, _i64, _i64, _vp, _i64, _i64, _vp],
+    "dlrm_interact_bwd": [_vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp, _i32,
+                          _vp],
+    "dlrm_linear_fwd": [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _i64,
+                        _i64, _i64, _i32, _vp],
+    "dlrm_linear_bwd_data": [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                             _i64, _i64, _i64, _vp],
+    "dlrm_linear_bwd_weight": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp,
+                               _i64, _vp, _vp, _i64, _vp, _f32, _vp, _vp,
+                               _sz, _vp],
+    "dlrm_bce_head": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _f32, _vp, _vp,
+                      _vp, _vp, _vp, _vp, _sz, _vp],
+    "dlrm_head_bwd": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp,
+                      _vp, _vp, _vp, _f32, _vp, _vp, _sz, _vp],
+    "dlrm_relu_grad": [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp],
+    "dlrm_sgd_dense": [_vp, _vp, _i64, _f32, _vp, _vp],
+}
+_SIZE_FNS = {
+    "dlrm_emb_bwd_workspace_size": [_i64, _i64],
+    "dlrm_linear_bwd_weight_workspace_size": [_i64, _i64, _i64],
+    "dlrm_bce_head_workspace_size": [_i64],
+    "dlrm_head_bwd_workspace_size": [_i64, _i64],
+}
+
+# every symbol include/dlrm_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = sorted(list(_SIGS) + list(_SIZE_FNS) + [
+    "dlrm_launch_count", "dlrm_last_error", "dlrm_build_info"])
+
+_lib = None
+
+
+def lib():
+    """Load libdlrmb200.so once; raise if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with "
+                "`python -m paper_1906_00091_b200.build` (there is no CPU "
+                "fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, _i32
+        for name, args in _SIZE_FNS.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, _sz
+        L.dlrm_launch_count.argtypes, L.dlrm_launch_count.restype = [], _i64
+        L.dlrm_last_error.restype = C.c_char_p
+        L.dlrm_build_info.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+class KernelError(RuntimeError):
+    pass
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().dlrm_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(f"{name}: {msg}")
+        raise KernelError(f"{name}: {msg}")
+
+
+def size(name, *args) -> int:
+    return int(getattr(lib(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(lib().dlrm_launch_count())
+
+
+def stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def ptr(t) -> C.c_void_p:
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return C.c_void_p(0)
+    if not t.is_cuda:
+        raise TypeError("libdlrmb200 kernels take CUDA tensors only "
+                        "(no CPU fallback)")
+    return C.c_void_p(t.data_ptr())
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1906_00091_b200 needs a CUDA device (B200); "
+                           "there is no CPU fallback")
+
+
+def device():
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def make_features(ptrs_strides):
+    f = Features()
+    if len(ptrs_strides) > MAX_FEATURES:
+        raise ValueError(f"at most {MAX_FEATURES} interaction features")
+    for i, (p, s) in enumerate(ptrs_strides):
+        f.feat[i] = p
+        f.feat_stride[i] = s
+    return f
+
+
+def table_array(descs):
+    if len(descs) > MAX_TABLES:
+        raise ValueError(f"at most {MAX_TABLES} tables per kernel call")
+    arr = (TableDesc * len(descs))()
+    for i, d in enumerate(descs):
+        arr[i] = d
+    return arr

@@ -1,0 +1,78 @@
+// Shared helpers for libdlrmb200: error plumbing, launch accounting, small
+// device utilities.  Every exported entry point returns 0 / 1 (invalid
+// argument) / 2 (CUDA error) and leaves a thread-local message.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/dlrm_b200.h"
+
+namespace dlrm {
+
+void set_error(const std::string& msg);
+void count_launch(int n = 1);
+
+inline cudaStream_t as_stream(dlrm_stream_t s) {
+  return reinterpret_cast<cudaStream_t>(s);
+}
+
+// Launch-site check: captures the launch error (never synchronises).
+inline int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return 2;
+  }
+  count_launch();
+  return 0;
+}
+
+#define DLRM_REQUIRE(cond, msg)          \
+  do {                                   \
+    if (!(cond)) {                       \
+      ::dlrm::set_error(msg);            \
+      return 1;                          \
+    }                                    \
+  } while (0)
+
+#define DLRM_CUDA(call)                                                    \
+  do {                                                                     \
+    cudaError_t _e = (call);                                               \
+    if (_e != cudaSuccess) {                                               \
+      ::dlrm::set_error(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+      return 2;                                                            \
+    }                                                                      \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
+  return (a + b - 1) / b;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Tables passed by value as a kernel parameter (CUDA 12.1+ allows up to
+// 32 KB of parameters; 128 x 64 B = 8 KB here).
+struct TableSet {
+  dlrm_table_desc t[DLRM_MAX_TABLES];
+  int64_t cap_base[DLRM_MAX_TABLES + 1];  // prefix of capacities
+  int32_t nt;
+};
+
+struct FeatureSet {
+  const float* feat[DLRM_MAX_FEATURES];
+  int64_t stride[DLRM_MAX_FEATURES];
+};
+
+struct GradFeatureSet {
+  float* feat[DLRM_MAX_FEATURES];
+  int64_t stride[DLRM_MAX_FEATURES];
+};
+
+}  // namespace dlrm

@@ -1,0 +1,697 @@
+// Embedding-bag kernels: pooled lookup (forward) and the sorted, deterministic
+// sparse backward fused with the SGD row update.
+//
+// Reference semantics (dlrmkit, pkg/src/dlrmkit/embedding.py):
+//   lookup_batch    155-179  strict ascending-position fold per bag, rows
+//                            scaled by the per-index weight first (165-166)
+//   check_bounds    117-124  lowest offending flat position is reported
+//   lookup_backward 182-210  np.unique rows (ascending) + np.add.at, i.e. per
+//                            row an ascending-position fold starting at +0.0
+//   sgd_step_rows   optim.py:38-46   W[rows] -= lr * values (product first)
+//
+// HBM layout: all tables of a rank live in ONE row-major fp32 buffer W_all
+// (row_base per table); pooled rows go to out[out_offset_t + j*out_stride].
+// Gathers are 128-bit (float4) per lane, LPB = min(32, d/4) lanes per bag,
+// indices loaded coalesced by the sub-warp and broadcast with shuffles, 4 row
+// loads in flight per lane.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace dlrm {
+
+namespace {
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+};
+template <>
+struct VecT<1> {
+  using T = float;
+};
+
+__device__ __forceinline__ float4 ldg_vec(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ float ldg_vec(const float* p) { return __ldg(p); }
+
+__device__ __forceinline__ float4 vzero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+__device__ __forceinline__ float4 vmul(float a, float4 v) {
+  return make_float4(__fmul_rn(a, v.x), __fmul_rn(a, v.y), __fmul_rn(a, v.z),
+                     __fmul_rn(a, v.w));
+}
+__device__ __forceinline__ float vmul(float a, float v) { return __fmul_rn(a, v); }
+__device__ __forceinline__ float4 vadd(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y),
+                     __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float4 vsgd(float4 w, float lr, float4 g) {
+  return make_float4(__fsub_rn(w.x, __fmul_rn(lr, g.x)),
+                     __fsub_rn(w.y, __fmul_rn(lr, g.y)),
+                     __fsub_rn(w.z, __fmul_rn(lr, g.z)),
+                     __fsub_rn(w.w, __fmul_rn(lr, g.w)));
+}
+__device__ __forceinline__ float vsgd(float w, float lr, float g) {
+  return __fsub_rn(w, __fmul_rn(lr, g));
+}
+template <typename V>
+__device__ __forceinline__ V vzero();
+template <>
+__device__ __forceinline__ float4 vzero<float4>() { return vzero4(); }
+template <>
+__device__ __forceinline__ float vzero<float>() { return 0.f; }
+
+__device__ __forceinline__ void record_error(int64_t* err_pos, int32_t* err_flag,
+                                             int t, int64_t pos) {
+  atomicMin(reinterpret_cast<unsigned long long*>(err_pos + t),
+            static_cast<unsigned long long>(pos));
+  atomicExch(err_flag, 1);
+}
+
+template <int LPB>
+__device__ __forceinline__ unsigned subgroup_mask() {
+  if constexpr (LPB == 32) {
+    return 0xffffffffu;
+  } else {
+    const unsigned lane = threadIdx.x & 31;
+    return ((1u << LPB) - 1u) << (lane & ~(LPB - 1));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward: one LPB-lane sub-warp per bag; NV vectors of VEC floats per lane.
+template <int VEC, int LPB, int NV>
+__global__ void __launch_bounds__(256)
+emb_fwd_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
+               int64_t num_bags, float* __restrict__ out, int64_t out_stride,
+               int64_t* err_pos, int32_t* err_flag) {
+  using V = typename VecT<VEC>::T;
+  constexpr int U = 4;  // rows in flight per lane
+  const int lane = threadIdx.x & (LPB - 1);
+  const int64_t group = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LPB;
+  const int64_t total = num_bags * ts.nt;
+  if (group >= total) return;
+  const unsigned mask = subgroup_mask<LPB>();
+  const int t = int(group / num_bags);
+  const int64_t j = group - int64_t(t) * num_bags;
+  const int64_t* offs = ts.t[t].offsets;
+  const int64_t* idxp = ts.t[t].indices;
+  const float* wts = ts.t[t].weights;
+  const int64_t row_base = ts.t[t].row_base;
+  const int64_t num_rows = ts.t[t].num_rows;
+  const int64_t lo = __ldg(offs + j), hi = __ldg(offs + j + 1);
+  const int64_t nvec = dim / VEC;
+
+  V acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = vzero<V>();
+  bool first = true;
+
+  for (int64_t p0 = lo; p0 < hi; p0 += LPB) {
+    const int64_t my = p0 + lane;
+    int64_t myidx = 0;
+    float myw = 1.f;
+    if (my < hi) {
+      myidx = __ldg(idxp + my);
+      if (wts) myw = __ldg(wts + my);
+      if (myidx < 0 || myidx >= num_rows) record_error(err_pos, err_flag, t, my);
+    }
+    const int cnt = int(hi - p0 < LPB ? hi - p0 : LPB);
+    for (int q = 0; q < cnt; q += U) {
+      V r[U][NV];
+      float wq[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int src = min(q + u, cnt - 1);
+        const int64_t ri = __shfl_sync(mask, myidx, src, LPB);
+        wq[u] = __shfl_sync(mask, myw, src, LPB);
+        const bool ok = (q + u < cnt) && ri >= 0 && ri < num_rows;
+        const V* rowp = reinterpret_cast<const V*>(W + (row_base + ri) * dim);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const int64_t v = lane + int64_t(i) * LPB;
+          r[u][i] = (ok && v < nvec) ? ldg_vec(rowp + v) : vzero<V>();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (q + u < cnt) {
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            const V val = wts ? vmul(wq[u], r[u][i]) : r[u][i];
+            acc[i] = first ? val : vadd(acc[i], val);
+          }
+          first = false;
+        }
+      }
+    }
+  }
+  V* o = reinterpret_cast<V*>(out + ts.t[t].out_offset + j * out_stride);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int64_t v = lane + int64_t(i) * LPB;
+    if (v < nvec) o[v] = acc[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward, stage 1: one (key = global row, value = slot) pair per index slot
+// plus the bag of each live slot.  Slots past a table's nnz get the sentinel
+// key so a capacity-sized (graph-static) sort leaves them at the end.
+__global__ void __launch_bounds__(256)
+emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots,
+                uint32_t sentinel, uint32_t* __restrict__ keys,
+                uint32_t* __restrict__ vals, int32_t* __restrict__ bag_of,
+                int64_t* err_pos, int32_t* err_flag) {
+  const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= total_slots) return;
+  // table of slot s: largest t with cap_base[t] <= s
+  int lo = 0, hi = ts.nt - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ts.cap_base[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  const int t = lo;
+  const int64_t k = s - ts.cap_base[t];
+  const int64_t* offs = ts.t[t].offsets;
+  const int64_t nnz = __ldg(offs + num_bags);
+  uint32_t key = sentinel;
+  int32_t bag = 0;
+  if (k < nnz) {
+    const int64_t idx = __ldg(ts.t[t].indices + k);
+    if (idx >= 0 && idx < ts.t[t].num_rows) {
+      key = uint32_t(ts.t[t].row_base + idx);
+    } else {
+      record_error(err_pos, err_flag, t, k);
+    }
+    // bag of position k: largest j with offs[j] <= k (offs nondecreasing)
+    int64_t a = 0, b = num_bags - 1;
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (__ldg(offs + mid) <= k) a = mid; else b = mid - 1;
+    }
+    bag = int32_t(a);
+  }
+  keys[s] = key;
+  vals[s] = uint32_t(s);
+  bag_of[s] = bag;
+}
+
+__device__ __forceinline__ int table_of_row(const TableSet& ts, uint32_t row) {
+  int lo = 0, hi = ts.nt - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ts.t[mid].row_base <= int64_t(row)) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Run-start flags for the coalesce path.
+__global__ void run_flags_kernel(const uint32_t* __restrict__ keys, int64_t n,
+                                 uint32_t sentinel, uint32_t* __restrict__ flags) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t k = keys[i];
+  flags[i] = (k != sentinel && (i == 0 || keys[i - 1] != k)) ? 1u : 0u;
+}
+
+__global__ void count_unique_kernel(const uint32_t* uid, const uint32_t* flags,
+                                    int64_t n, int64_t* num_unique) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    *num_unique = n ? int64_t(uid[n - 1]) + int64_t(flags[n - 1]) : 0;
+}
+
+// ---------------------------------------------------------------------------
+// backward, stage 3: deterministic segmented fold over the sorted slots.
+// Chunk c of CH sorted slots belongs to one sub-warp, which owns every run
+// (equal-row segment) that STARTS inside the chunk — following it past the
+// chunk end if needed.  Per run: acc = +0; acc += g[bag]*a in ascending slot
+// order (== ascending position); then either W[row] -= lr*acc (SGD mode) or
+// rows_out/values_out[uid] = (row, acc) (coalesce mode).
+struct FoldArgs {
+  const uint32_t* keys;  // sorted
+  const uint32_t* vals;  // slots, sorted by key (stable)
+  const int32_t* bag_of;
+  int64_t n;
+  uint32_t sentinel;
+  const float* grad;
+  int64_t grad_stride;
+  float* W;  // SGD mode
+  float lr;
+  const int32_t* err_flag;
+  const uint32_t* uid;  // coalesce mode
+  int64_t* rows_out;
+  float* values_out;
+};
+
+template <int LPB>
+constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
+
+template <int VEC, int LPB, int NV, bool COALESCE>
+__global__ void __launch_bounds__(fold_groups<LPB>() * LPB)
+emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
+  using V = typename VecT<VEC>::T;
+  constexpr int CH = 32;
+  constexpr int GROUPS = fold_groups<LPB>();
+  __shared__ uint32_t s_key[GROUPS][CH];
+  __shared__ int64_t s_goff[GROUPS][CH];
+  __shared__ float s_w[GROUPS][CH];
+
+  const int lane = threadIdx.x & (LPB - 1);
+  const int g = threadIdx.x / LPB;
+  const unsigned mask = subgroup_mask<LPB>();
+  const int64_t chunk = int64_t(blockIdx.x) * GROUPS + g;
+  const int64_t start = chunk * CH;
+  if (start >= fa.n) return;
+  if (!COALESCE && fa.err_flag && *fa.err_flag) return;
+  const int cnt = int(fa.n - start < CH ? fa.n - start : CH);
+  const int64_t nvec = dim / VEC;
+
+  // stage keys, grad-row offsets and weights of this chunk
+  for (int i = lane; i < cnt; i += LPB) {
+    const uint32_t k = fa.keys[start + i];
+    s_key[g][i] = k;
+    int64_t goff = 0;
+    float w = 1.f;
+    if (k != fa.sentinel) {
+      const int t = table_of_row(ts, k);
+      const uint32_t slot = fa.vals[start + i];
+      goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
+      if (ts.t[t].weights) w = __ldg(ts.t[t].weights + (slot - ts.cap_base[t]));
+    }
+    s_goff[g][i] = goff;
+    s_w[g][i] = w;
+  }
+  const uint32_t prev = start > 0 ? fa.keys[start - 1] : fa.sentinel;
+  __syncwarp(mask);
+
+  int i0 = 0;
+  if (start > 0) {
+    uint32_t before = prev;
+    while (i0 < cnt && s_key[g][i0] == before) { before = s_key[g][i0]; ++i0; }
+  }
+  if (i0 >= cnt) return;
+  uint32_t cur = s_key[g][i0];
+  if (cur == fa.sentinel) return;
+  int64_t run_start = start + i0;
+
+  V acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
+
+  auto flush = [&](uint32_t row, int64_t rs) {
+    if constexpr (COALESCE) {
+      const uint32_t u = fa.uid[rs];
+      const int t = table_of_row(ts, row);
+      if (lane == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
+      V* dst = reinterpret_cast<V*>(fa.values_out + int64_t(u) * dim);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = lane + int64_t(v) * LPB;
+        if (c < nvec) dst[c] = acc[v];
+      }
+    } else {
+      V* wrow = reinterpret_cast<V*>(fa.W + int64_t(row) * dim);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = lane + int64_t(v) * LPB;
+        if (c < nvec) wrow[c] = vsgd(wrow[c], fa.lr, acc[v]);
+      }
+    }
+  };
+
+  constexpr int U = 4;
+  int i = i0;
+  bool done = false;
+  for (; i < cnt && !done; i += U) {
+    V r[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ii = i + u;
+      const bool live = ii < cnt && s_key[g][min(ii, cnt - 1)] != fa.sentinel;
+      const V* src = reinterpret_cast<const V*>(fa.grad + s_goff[g][min(ii, cnt - 1)]);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = lane + int64_t(v) * LPB;
+        r[u][v] = (live && c < nvec) ? ldg_vec(src + c) : vzero<V>();
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ii = i + u;
+      if (ii >= cnt || done) continue;
+      const uint32_t k = s_key[g][ii];
+      if (k != cur) {
+        flush(cur, run_start);
+        if (k == fa.sentinel) { done = true; continue; }
+        cur = k;
+        run_start = start + ii;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
+      }
+      const float w = s_w[g][ii];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        acc[v] = vadd(acc[v], vmul(w, r[u][v]));  // fl(1*x) == x
+    }
+  }
+  if (done) return;
+  // the last run may continue past the chunk: follow it sequentially
+  for (int64_t p = start + cnt; p < fa.n; ++p) {
+    const uint32_t k = fa.keys[p];
+    if (k != cur) break;
+    const int t = table_of_row(ts, k);
+    const uint32_t slot = fa.vals[p];
+    const int64_t goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
+    const float w = ts.t[t].weights ? __ldg(ts.t[t].weights + (slot - ts.cap_base[t])) : 1.f;
+    const V* src = reinterpret_cast<const V*>(fa.grad + goff);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = lane + int64_t(v) * LPB;
+      const V x = c < nvec ? ldg_vec(src + c) : vzero<V>();
+      acc[v] = vadd(acc[v], vmul(w, x));
+    }
+  }
+  flush(cur, run_start);
+}
+
+__global__ void err_reset_kernel(int64_t* err_pos, int32_t nt, int32_t* err_flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nt) err_pos[i] = INT64_MAX;
+  if (i == 0 && err_flag) *err_flag = 0;
+}
+
+template <int VEC>
+__global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
+                                const int64_t* __restrict__ rows,
+                                const float* __restrict__ values, int64_t n,
+                                float lr) {
+  using V = typename VecT<VEC>::T;
+  const int64_t nvec = dim / VEC;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * nvec) return;
+  const int64_t i = e / nvec, c = e - i * nvec;
+  V* w = reinterpret_cast<V*>(W + rows[i] * dim) + c;
+  const V g = reinterpret_cast<const V*>(values + i * dim)[c];
+  *w = vsgd(*w, lr, g);
+}
+
+// ---------------------------------------------------------------------------
+// dispatch helpers
+
+int fill_tableset(TableSet& ts, const dlrm_table_desc* tables, int32_t nt) {
+  DLRM_REQUIRE(tables != nullptr && nt >= 1 && nt <= DLRM_MAX_TABLES,
+               "table count must be in [1, DLRM_MAX_TABLES]");
+  ts.nt = nt;
+  ts.cap_base[0] = 0;
+  for (int i = 0; i < nt; ++i) {
+    ts.t[i] = tables[i];
+    DLRM_REQUIRE(i == 0 || tables[i].row_base >= tables[i - 1].row_base,
+                 "table row_base must be nondecreasing");
+    DLRM_REQUIRE(tables[i].capacity >= 0, "negative capacity");
+    ts.cap_base[i + 1] = ts.cap_base[i] + tables[i].capacity;
+  }
+  for (int i = nt; i < DLRM_MAX_TABLES; ++i) ts.t[i] = dlrm_table_desc{};
+  return 0;
+}
+
+bool vec4_ok(int64_t dim, const void* a, int64_t stride, int64_t off) {
+  return dim % 4 == 0 && (reinterpret_cast<uintptr_t>(a) % 16) == 0 &&
+         stride % 4 == 0 && off % 4 == 0;
+}
+
+template <int VEC, int LPB, int NV>
+void launch_fwd(const float* W, int64_t dim, const TableSet& ts, int64_t nb,
+                float* out, int64_t stride, int64_t* ep, int32_t* ef,
+                cudaStream_t s) {
+  const int64_t threads = nb * ts.nt * LPB;
+  emb_fwd_kernel<VEC, LPB, NV><<<unsigned(ceil_div(threads, 256)), 256, 0, s>>>(
+      W, dim, ts, nb, out, stride, ep, ef);
+}
+
+struct WsLayout {
+  size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, temp, total,
+      temp_bytes;
+};
+
+WsLayout ws_layout(int64_t n) {
+  WsLayout L{};
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k, v, int(n > 0 ? n : 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr,
+                                (uint32_t*)nullptr, int(n > 0 ? n : 1));
+  const size_t a = 256, e = align_up(size_t(n > 0 ? n : 1) * 4, a);
+  L.keys_a = 0;
+  L.keys_b = L.keys_a + e;
+  L.vals_a = L.keys_b + e;
+  L.vals_b = L.vals_a + e;
+  L.bag = L.vals_b + e;
+  L.flags = L.bag + e;
+  L.uid = L.flags + e;
+  L.err = L.uid + e;
+  L.temp = L.err + align_up((DLRM_MAX_TABLES + 1) * 8, a);
+  L.temp_bytes = align_up(sort_bytes > scan_bytes ? sort_bytes : scan_bytes, a);
+  L.total = L.temp + L.temp_bytes;
+  return L;
+}
+
+int end_bit_for(int64_t total_rows) {
+  int b = 1;
+  while (b < 32 && (int64_t(1) << b) <= total_rows) ++b;
+  return b;  // total_rows < 2^b, so sentinel = 2^b - 1 > every real row
+}
+
+// Sort (row, slot) pairs of all tables; returns sorted key/val pointers.
+int sort_pairs(const TableSet& ts, int64_t nb, int64_t total_rows, char* ws,
+               const WsLayout& L, int64_t n, int64_t* err_pos, int32_t* err_flag,
+               uint32_t sentinel, int end_bit, uint32_t** keys_sorted,
+               uint32_t** vals_sorted, cudaStream_t s) {
+  uint32_t* ka = reinterpret_cast<uint32_t*>(ws + L.keys_a);
+  uint32_t* kb = reinterpret_cast<uint32_t*>(ws + L.keys_b);
+  uint32_t* va = reinterpret_cast<uint32_t*>(ws + L.vals_a);
+  uint32_t* vb = reinterpret_cast<uint32_t*>(ws + L.vals_b);
+  int32_t* bag = reinterpret_cast<int32_t*>(ws + L.bag);
+  emb_keys_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(
+      ts, nb, n, sentinel, ka, va, bag, err_pos, err_flag);
+  if (int rc = check_launch("emb_keys_kernel")) return rc;
+  cub::DoubleBuffer<uint32_t> kbuf(ka, kb), vbuf(va, vb);
+  size_t tb = L.temp_bytes;
+  DLRM_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, tb, kbuf, vbuf, int(n),
+                                            0, end_bit, s));
+  count_launch(end_bit / 8 + 2);
+  *keys_sorted = kbuf.Current();
+  *vals_sorted = vbuf.Current();
+  return 0;
+}
+
+template <int VEC, int LPB, int NV, bool CO>
+void launch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim,
+                 cudaStream_t s) {
+  constexpr int GROUPS = fold_groups<LPB>();
+  const int64_t chunks = ceil_div(fa.n, 32);
+  emb_fold_kernel<VEC, LPB, NV, CO>
+      <<<unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, 0, s>>>(fa, ts, dim);
+}
+
+template <bool CO>
+int dispatch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim, bool v4,
+                  cudaStream_t s) {
+  if (v4) {
+    const int64_t nv = dim / 4;
+    if (nv <= 1) launch_fold<4, 1, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 2) launch_fold<4, 2, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 4) launch_fold<4, 4, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 8) launch_fold<4, 8, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 16) launch_fold<4, 16, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 32) launch_fold<4, 32, 1, CO>(fa, ts, dim, s);
+    else if (nv <= 64) launch_fold<4, 32, 2, CO>(fa, ts, dim, s);
+    else if (nv <= 128) launch_fold<4, 32, 4, CO>(fa, ts, dim, s);
+    else { set_error("embedding dim > 512 unsupported"); return 1; }
+  } else {
+    if (dim <= 4) launch_fold<1, 4, 1, CO>(fa, ts, dim, s);
+    else if (dim <= 32) launch_fold<1, 32, 1, CO>(fa, ts, dim, s);
+    else if (dim <= 128) launch_fold<1, 32, 4, CO>(fa, ts, dim, s);
+    else if (dim <= 512) launch_fold<1, 32, 16, CO>(fa, ts, dim, s);
+    else { set_error("embedding dim > 512 unsupported"); return 1; }
+  }
+  return check_launch("emb_fold_kernel");
+}
+
+}  // namespace
+}  // namespace dlrm
+
+using namespace dlrm;
+
+extern "C" int dlrm_err_reset(int64_t* err_pos, int32_t nt, int32_t* err_flag,
+                              dlrm_stream_t stream) {
+  DLRM_REQUIRE(err_pos != nullptr && nt >= 0, "bad error buffers");
+  err_reset_kernel<<<unsigned(ceil_div(nt > 0 ? nt : 1, 128)), 128, 0,
+                     as_stream(stream)>>>(err_pos, nt, err_flag);
+  return check_launch("err_reset_kernel");
+}
+
+extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
+                            const dlrm_table_desc* tables, int32_t nt,
+                            int64_t num_bags, float* out, int64_t out_stride,
+                            int64_t* err_pos, int32_t* err_flag,
+                            dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && dim <= 512, "embedding dim must be in [1, 512]");
+  DLRM_REQUIRE(num_bags >= 0 && out != nullptr && err_pos && err_flag,
+               "bad emb_fwd arguments");
+  static thread_local TableSet ts;
+  if (int rc = fill_tableset(ts, tables, nt)) return rc;
+  if (num_bags == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  bool v4 = vec4_ok(dim, W_all, out_stride, 0) &&
+            (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+  for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
+  if (v4) {
+    const int64_t nv = dim / 4;
+    if (nv <= 1) launch_fwd<4, 1, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 2) launch_fwd<4, 2, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 4) launch_fwd<4, 4, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 8) launch_fwd<4, 8, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 16) launch_fwd<4, 16, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 32) launch_fwd<4, 32, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (nv <= 64) launch_fwd<4, 32, 2>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else launch_fwd<4, 32, 4>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+  } else {
+    if (dim <= 4) launch_fwd<1, 4, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (dim <= 32) launch_fwd<1, 32, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else if (dim <= 128) launch_fwd<1, 32, 4>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+    else launch_fwd<1, 32, 16>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
+  }
+  return check_launch("emb_fwd_kernel");
+}
+
+extern "C" size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity,
+                                              int64_t total_rows) {
+  (void)total_rows;
+  return ws_layout(total_capacity).total;
+}
+
+extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
+                                const dlrm_table_desc* tables, int32_t nt,
+                                int64_t num_bags, const float* grad,
+                                int64_t grad_stride, float lr,
+                                const int32_t* err_flag, int64_t total_rows,
+                                void* workspace, size_t ws_bytes,
+                                dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && dim <= 512, "embedding dim must be in [1, 512]");
+  DLRM_REQUIRE(total_rows >= 1 && total_rows < (int64_t(1) << 31),
+               "total rows must be in [1, 2^31)");
+  static thread_local TableSet ts;
+  if (int rc = fill_tableset(ts, tables, nt)) return rc;
+  const int64_t n = ts.cap_base[nt];
+  DLRM_REQUIRE(n < (int64_t(1) << 31), "total capacity must be < 2^31");
+  if (n == 0 || num_bags == 0) return 0;
+  const WsLayout L = ws_layout(n);
+  DLRM_REQUIRE(workspace != nullptr && ws_bytes >= L.total,
+               "embedding backward workspace too small");
+  cudaStream_t s = as_stream(stream);
+  const int end_bit = end_bit_for(total_rows);
+  const uint32_t sentinel = uint32_t((int64_t(1) << end_bit) - 1);
+  char* ws = static_cast<char*>(workspace);
+  uint32_t *ks, *vs;
+  // errors were recorded by the forward; the key pass re-records into a
+  // scratch area so the caller's err_pos is unaffected here.
+  int64_t* scratch_err = reinterpret_cast<int64_t*>(ws + L.err);
+  int32_t* scratch_flag = reinterpret_cast<int32_t*>(ws + L.err + DLRM_MAX_TABLES * 8);
+  if (int rc = sort_pairs(ts, num_bags, total_rows, ws, L, n, scratch_err,
+                          scratch_flag, sentinel, end_bit, &ks, &vs, s))
+    return rc;
+  FoldArgs fa{};
+  fa.keys = ks;
+  fa.vals = vs;
+  fa.bag_of = reinterpret_cast<const int32_t*>(ws + L.bag);
+  fa.n = n;
+  fa.sentinel = sentinel;
+  fa.grad = grad;
+  fa.grad_stride = grad_stride;
+  fa.W = W_all;
+  fa.lr = lr;
+  fa.err_flag = err_flag;
+  bool v4 = vec4_ok(dim, W_all, grad_stride, 0) &&
+            (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
+  for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
+  return dispatch_fold<false>(fa, ts, dim, v4, s);
+}
+
+extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
+                                     int64_t num_bags, const float* grad,
+                                     int64_t grad_stride, int64_t* rows_out,
+                                     float* values_out, int64_t* num_unique,
+                                     int64_t* err_pos, int32_t* err_flag,
+                                     void* workspace, size_t ws_bytes,
+                                     dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && dim <= 512, "embedding dim must be in [1, 512]");
+  DLRM_REQUIRE(table != nullptr && num_unique != nullptr && err_pos &&
+                   err_flag, "bad arguments");
+  static thread_local TableSet ts;
+  dlrm_table_desc one = *table;
+  const int64_t total_rows = one.row_base + one.num_rows;
+  DLRM_REQUIRE(total_rows >= 1 && total_rows < (int64_t(1) << 31),
+               "table rows must be in [1, 2^31)");
+  if (int rc = fill_tableset(ts, &one, 1)) return rc;
+  const int64_t n = ts.cap_base[1];
+  cudaStream_t s = as_stream(stream);
+  if (n == 0 || num_bags == 0) {
+    DLRM_CUDA(cudaMemsetAsync(num_unique, 0, sizeof(int64_t), s));
+    return 0;
+  }
+  const WsLayout L = ws_layout(n);
+  DLRM_REQUIRE(workspace != nullptr && ws_bytes >= L.total,
+               "embedding backward workspace too small");
+  const int end_bit = end_bit_for(total_rows);
+  const uint32_t sentinel = uint32_t((int64_t(1) << end_bit) - 1);
+  char* ws = static_cast<char*>(workspace);
+  uint32_t *ks, *vs;
+  if (int rc = sort_pairs(ts, num_bags, total_rows, ws, L, n, err_pos,
+                          err_flag, sentinel, end_bit, &ks, &vs, s))
+    return rc;
+  uint32_t* flags = reinterpret_cast<uint32_t*>(ws + L.flags);
+  uint32_t* uid = reinterpret_cast<uint32_t*>(ws + L.uid);
+  run_flags_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(ks, n, sentinel, flags);
+  if (int rc = check_launch("run_flags_kernel")) return rc;
+  size_t tb = L.temp_bytes;
+  DLRM_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, flags, uid, int(n), s));
+  count_launch();
+  count_unique_kernel<<<1, 32, 0, s>>>(uid, flags, n, num_unique);
+  if (int rc = check_launch("count_unique_kernel")) return rc;
+  FoldArgs fa{};
+  fa.keys = ks;
+  fa.vals = vs;
+  fa.bag_of = reinterpret_cast<const int32_t*>(ws + L.bag);
+  fa.n = n;
+  fa.sentinel = sentinel;
+  fa.grad = grad;
+  fa.grad_stride = grad_stride;
+  fa.uid = uid;
+  fa.rows_out = rows_out;
+  fa.values_out = values_out;
+  bool v4 = vec4_ok(dim, values_out, grad_stride, one.out_offset) &&
+            (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
+  return dispatch_fold<true>(fa, ts, dim, v4, s);
+}
+
+extern "C" int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
+                             const float* values, int64_t n, float lr,
+                             dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && n >= 0, "bad sgd_rows arguments");
+  if (n == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  const bool v4 = vec4_ok(dim, W, dim, 0) &&
+                  (reinterpret_cast<uintptr_t>(values) % 16) == 0;
+  if (v4) {
+    const int64_t e = n * (dim / 4);
+    sgd_rows_kernel<4><<<unsigned(ceil_div(e, 256)), 256, 0, s>>>(W, dim, rows, values, n, lr);
+  } else {
+    const int64_t e = n * dim;
+    sgd_rows_kernel<1><<<unsigned(ceil_div(e, 256)), 256, 0, s>>>(W, dim, rows, values, n, lr);
+  }
+  return check_launch("sgd_rows_kernel");
+}

@@ -1,0 +1,34 @@
+// tcgen05 (5th-gen tensor core) GEMM path: fp32-accurate 3xTF32 with TMEM
+// accumulators.  Each *_ok predicate says whether a shape/stride set is one
+// the tensor-core kernels take; otherwise the SIMT path runs.
+#pragma once
+
+#include "common.cuh"
+
+namespace dlrm {
+
+bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw,
+                      const float* Y, int64_t ldy, int64_t M, int64_t N,
+                      int64_t K, int64_t n_grid);
+int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw,
+                  const float* b, float* Y, int64_t ldy, int64_t M, int64_t N,
+                  int64_t K, int64_t n_grid, int act, cudaStream_t s);
+
+bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W,
+                           int64_t ldw, const float* dX, int64_t ldx, int64_t M,
+                           int64_t N, int64_t K);
+int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W,
+                       int64_t ldw, const float* mask, int64_t ldm, float* dX,
+                       int64_t ldx, int64_t M, int64_t N, int64_t K,
+                       cudaStream_t s);
+
+bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X,
+                             int64_t ldx, int64_t M, int64_t N, int64_t K);
+size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K);
+int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X,
+                         int64_t ldx, int64_t M, int64_t N, int64_t K,
+                         float* dW, int64_t lddw, float* W_upd, int64_t ldw,
+                         float lr, const int32_t* err_flag, float* ws,
+                         cudaStream_t s);
+
+}  // namespace dlrm

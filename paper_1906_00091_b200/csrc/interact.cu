@@ -1,0 +1,250 @@
+// Pairwise dot-product feature interaction (SIMT, shared-memory tiled).
+//
+// Reference (dlrmkit, pkg/src/dlrmkit/model.py):
+//   interact           218-242  out = [z0 | z_i . z_j for i < j, row-major]
+//                               (upper triangle, (0,1),(0,2),...,(1,2),...)
+//   interact_backward  245-268  g_i = [i==0] gout[:, :d] + sum_{j!=i} g_ij z_j
+//
+// Feature f of sample b is read from feat[f] + b*stride[f], so the kernel can
+// consume the all-to-all receive buffer (features grouped by source rank) and
+// the pooled-embedding buffer in place.  A CTA stages S samples' feature
+// rows in shared memory (row pitch d+4 floats: conflict-free float4 reads),
+// then each thread computes dot products / gradient columns from smem.
+#include "common.cuh"
+
+namespace dlrm {
+namespace {
+
+__device__ __forceinline__ void pair_of(int p, int nf, int& i, int& j) {
+  // row-major upper triangle: row i holds nf-1-i pairs
+  int row = 0, base = 0;
+  while (p >= base + (nf - 1 - row)) { base += nf - 1 - row; ++row; }
+  i = row;
+  j = row + 1 + (p - base);
+}
+
+template <bool V4>
+__global__ void __launch_bounds__(256)
+interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
+                    float* __restrict__ out, int64_t ld_out, int64_t pad_to) {
+  extern __shared__ float4 smem4[];
+  float* z = reinterpret_cast<float*>(smem4);
+  const int pitch = int(dim) + 4;
+  const int npairs = nf * (nf - 1) / 2;
+  int* pairs = reinterpret_cast<int*>(z + size_t(S) * nf * pitch);
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    int i, j;
+    pair_of(p, nf, i, j);
+    pairs[p] = (i << 16) | j;
+  }
+  const int64_t b0 = int64_t(blockIdx.x) * S;
+  const int ns = int(batch - b0 < S ? batch - b0 : S);
+  // stage features
+  if (V4) {
+    const int nv = int(dim / 4);
+    for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
+      const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c);
+      *reinterpret_cast<float4*>(z + (size_t(s) * nf + f) * pitch + 4 * c) = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < ns * nf * int(dim); e += blockDim.x) {
+      const int s = e / (nf * int(dim)), r = e - s * nf * int(dim), f = r / int(dim),
+                c = r - f * int(dim);
+      z[(size_t(s) * nf + f) * pitch + c] = __ldg(fs.feat[f] + (b0 + s) * fs.stride[f] + c);
+    }
+  }
+  __syncthreads();
+  const int width = int(dim) + npairs;
+  const int total_w = int(pad_to > width ? pad_to : width);
+  for (int e = threadIdx.x; e < ns * total_w; e += blockDim.x) {
+    const int s = e / total_w, col = e - s * total_w;
+    const float* zs = z + size_t(s) * nf * pitch;
+    float v;
+    if (col < dim) {
+      v = zs[col];
+    } else if (col < width) {
+      const int pr = pairs[col - int(dim)];
+      const float* zi = zs + (pr >> 16) * pitch;
+      const float* zj = zs + (pr & 0xffff) * pitch;
+      if (V4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < dim; c += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(zi + c);
+          const float4 y = *reinterpret_cast<const float4*>(zj + c);
+          a.x = fmaf(x.x, y.x, a.x);
+          a.y = fmaf(x.y, y.y, a.y);
+          a.z = fmaf(x.z, y.z, a.z);
+          a.w = fmaf(x.w, y.w, a.w);
+        }
+        v = (a.x + a.y) + (a.z + a.w);
+      } else {
+        float a = 0.f;
+        for (int c = 0; c < dim; ++c) a = fmaf(zi[c], zj[c], a);
+        v = a;
+      }
+    } else {
+      v = 0.f;
+    }
+    out[(b0 + s) * ld_out + col] = v;
+  }
+}
+
+template <bool V4>
+__global__ void __launch_bounds__(256)
+interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
+                    int64_t batch, int S, const float* __restrict__ gout,
+                    int64_t ld_gout, int mask_f0) {
+  extern __shared__ float4 smem4[];
+  float* z = reinterpret_cast<float*>(smem4);
+  const int pitch = int(dim) + 4;
+  const int gp = nf + 1;  // pitch of the symmetric gradient matrix
+  float* G = z + size_t(S) * nf * pitch;
+  const int npairs = nf * (nf - 1) / 2;
+  const int64_t b0 = int64_t(blockIdx.x) * S;
+  const int ns = int(batch - b0 < S ? batch - b0 : S);
+  const int id = int(dim);
+  if (V4) {
+    const int nv = id / 4;
+    for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
+      const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c);
+      *reinterpret_cast<float4*>(z + (size_t(s) * nf + f) * pitch + 4 * c) = v;
+    }
+  } else {
+    for (int e = threadIdx.x; e < ns * nf * id; e += blockDim.x) {
+      const int s = e / (nf * id), r = e - s * nf * id, f = r / id, c = r - f * id;
+      z[(size_t(s) * nf + f) * pitch + c] = __ldg(fs.feat[f] + (b0 + s) * fs.stride[f] + c);
+    }
+  }
+  // symmetric pair gradients, zero diagonal
+  for (int e = threadIdx.x; e < ns * nf; e += blockDim.x) {
+    const int s = e / nf, f = e - s * nf;
+    G[(size_t(s) * nf + f) * gp + f] = 0.f;
+  }
+  for (int e = threadIdx.x; e < ns * npairs; e += blockDim.x) {
+    const int s = e / npairs, p = e - s * npairs;
+    int i, j;
+    pair_of(p, nf, i, j);
+    const float g = __ldg(gout + (b0 + s) * ld_gout + id + p);
+    G[(size_t(s) * nf + i) * gp + j] = g;
+    G[(size_t(s) * nf + j) * gp + i] = g;
+  }
+  __syncthreads();
+  if (V4) {
+    const int nv = id / 4;
+    for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
+      const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
+      const float* zs = z + size_t(s) * nf * pitch + 4 * c;
+      const float* gr = G + (size_t(s) * nf + f) * gp;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f == 0) a = __ldg(reinterpret_cast<const float4*>(gout + (b0 + s) * ld_gout) + c);
+      for (int j = 0; j < nf; ++j) {
+        const float g = gr[j];
+        const float4 x = *reinterpret_cast<const float4*>(zs + j * pitch);
+        a.x = fmaf(g, x.x, a.x);
+        a.y = fmaf(g, x.y, a.y);
+        a.z = fmaf(g, x.z, a.z);
+        a.w = fmaf(g, x.w, a.w);
+      }
+      if (f == 0 && mask_f0) {
+        const float4 z0 = *reinterpret_cast<const float4*>(zs);
+        a.x *= z0.x > 0.f ? 1.f : 0.f;
+        a.y *= z0.y > 0.f ? 1.f : 0.f;
+        a.z *= z0.z > 0.f ? 1.f : 0.f;
+        a.w *= z0.w > 0.f ? 1.f : 0.f;
+      }
+      reinterpret_cast<float4*>(gs.feat[f] + (b0 + s) * gs.stride[f])[c] = a;
+    }
+  } else {
+    for (int e = threadIdx.x; e < ns * nf * id; e += blockDim.x) {
+      const int s = e / (nf * id), r = e - s * nf * id, f = r / id, c = r - f * id;
+      const float* zs = z + size_t(s) * nf * pitch + c;
+      const float* gr = G + (size_t(s) * nf + f) * gp;
+      float a = f == 0 ? __ldg(gout + (b0 + s) * ld_gout + c) : 0.f;
+      for (int j = 0; j < nf; ++j) a = fmaf(gr[j], zs[j * pitch], a);
+      if (f == 0 && mask_f0) a *= zs[0] > 0.f ? 1.f : 0.f;
+      gs.feat[f][(b0 + s) * gs.stride[f] + c] = a;
+    }
+  }
+}
+
+int pick_samples(int nf, int64_t dim, size_t extra_per_sample, size_t fixed,
+                 size_t budget) {
+  const size_t per = size_t(nf) * (dim + 4) * 4 + extra_per_sample;
+  int S = int((budget - fixed) / per);
+  if (S > 32) S = 32;
+  return S < 1 ? 1 : S;
+}
+
+}  // namespace
+}  // namespace dlrm
+
+using namespace dlrm;
+
+static int fill_features(FeatureSet& fs, const dlrm_features* feats, int32_t nf,
+                         int64_t dim, bool* v4) {
+  DLRM_REQUIRE(feats != nullptr && nf >= 1 && nf <= DLRM_MAX_FEATURES,
+               "feature count must be in [1, DLRM_MAX_FEATURES]");
+  *v4 = dim % 4 == 0;
+  for (int f = 0; f < nf; ++f) {
+    fs.feat[f] = feats->feat[f];
+    fs.stride[f] = feats->feat_stride[f];
+    *v4 = *v4 && reinterpret_cast<uintptr_t>(fs.feat[f]) % 16 == 0 &&
+          fs.stride[f] % 4 == 0;
+  }
+  return 0;
+}
+
+extern "C" int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf,
+                                 int64_t dim, int64_t batch, float* out,
+                                 int64_t ld_out, int64_t pad_to,
+                                 dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && dim <= 1024 && batch >= 0, "bad interaction shape");
+  static thread_local FeatureSet fs;
+  bool v4;
+  if (int rc = fill_features(fs, feats, nf, dim, &v4)) return rc;
+  if (batch == 0) return 0;
+  const int npairs = nf * (nf - 1) / 2;
+  const size_t fixed = align_up(size_t(npairs) * 4, 16);
+  const int S = pick_samples(nf, dim, 0, fixed, 96 * 1024);
+  const size_t smem = size_t(S) * nf * (dim + 4) * 4 + fixed;
+  DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
+  cudaStream_t s = as_stream(stream);
+  auto k = v4 ? interact_fwd_kernel<true> : interact_fwd_kernel<false>;
+  DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k<<<unsigned(ceil_div(batch, S)), 256, smem, s>>>(fs, nf, dim, batch, S, out,
+                                                     ld_out, pad_to);
+  return check_launch("interact_fwd_kernel");
+}
+
+extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
+                                 int64_t dim, int64_t batch, const float* gout,
+                                 int64_t ld_gout, float* const* grad_feat,
+                                 const int64_t* grad_stride,
+                                 int32_t relu_mask_f0, dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && dim <= 1024 && batch >= 0, "bad interaction shape");
+  DLRM_REQUIRE(grad_feat != nullptr && grad_stride != nullptr, "null grads");
+  static thread_local FeatureSet fs;
+  static thread_local GradFeatureSet gs;
+  bool v4;
+  if (int rc = fill_features(fs, feats, nf, dim, &v4)) return rc;
+  for (int f = 0; f < nf; ++f) {
+    gs.feat[f] = grad_feat[f];
+    gs.stride[f] = grad_stride[f];
+    v4 = v4 && reinterpret_cast<uintptr_t>(grad_feat[f]) % 16 == 0 &&
+         grad_stride[f] % 4 == 0;
+  }
+  v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
+  if (batch == 0) return 0;
+  const size_t extra = size_t(nf) * (nf + 1) * 4;
+  const int S = pick_samples(nf, dim, extra, 0, 96 * 1024);
+  const size_t smem = size_t(S) * (nf * (dim + 4) * 4 + extra);
+  DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
+  cudaStream_t s = as_stream(stream);
+  auto k = v4 ? interact_bwd_kernel<true> : interact_bwd_kernel<false>;
+  DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k<<<unsigned(ceil_div(batch, S)), 256, smem, s>>>(fs, gs, nf, dim, batch, S,
+                                                     gout, ld_gout, relu_mask_f0);
+  return check_launch("interact_bwd_kernel");
+}

@@ -1,0 +1,108 @@
+// C-ABI entry points for the MLP layers: forward (bias + activation fused),
+// data gradient (ReLU mask fused), weight/bias gradients (split-K with a
+// fixed-order reduction, SGD fused).  Shapes the tcgen05 path accepts go
+// there (gemm_tc.cu); everything else runs on the SIMT kernels.
+#include "common.cuh"
+#include "gemm.cuh"
+#include "gemm_tc.cuh"
+
+namespace dlrm {
+namespace {
+
+int choose_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(N, 64) * ceil_div(K, 64);
+  int64_t s = ceil_div(2 * kNumSMs, tiles);
+  const int64_t cap = M / 256 > 1 ? M / 256 : 1;
+  if (s > cap) s = cap;
+  if (s > 64) s = 64;
+  return int(s < 1 ? 1 : s);
+}
+
+size_t colreduce_ws_floats(int64_t R, int64_t C) {
+  return size_t(ceil_div(R, 256) + 1) * size_t(C);
+}
+
+}  // namespace
+}  // namespace dlrm
+
+using namespace dlrm;
+
+extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
+                               int64_t ldw, const float* b, float* Y,
+                               int64_t ldy, int64_t M, int64_t N, int64_t K,
+                               int64_t pad_n, int32_t act,
+                               dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldx >= K && ldw >= K && ldy >= N,
+               "bad linear_fwd shape");
+  DLRM_REQUIRE(act == DLRM_ACT_IDENTITY || act == DLRM_ACT_RELU, "bad activation");
+  if (M == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  const int64_t ng = pad_n > N ? pad_n : N;
+  if (tc_linear_fwd_ok(X, ldx, W, ldw, Y, ldy, M, N, K, ng))
+    return tc_linear_fwd(X, ldx, W, ldw, b, Y, ldy, M, N, K, ng, act, s);
+  GemmEpilogue ep{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, ng, M};
+  return gemm_simt(X, ldx, 1, W, ldw, 1, M, N, K, 1, ep, ng, s);
+}
+
+extern "C" int dlrm_linear_bwd_data(const float* gZ, int64_t ldg,
+                                    const float* W, int64_t ldw,
+                                    const float* mask, int64_t ldm, float* dX,
+                                    int64_t ldx, int64_t M, int64_t N,
+                                    int64_t K, dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldw >= K && ldx >= K,
+               "bad linear_bwd_data shape");
+  if (M == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  if (tc_linear_bwd_data_ok(gZ, ldg, W, ldw, dX, ldx, M, N, K))
+    return tc_linear_bwd_data(gZ, ldg, W, ldw, mask, ldm, dX, ldx, M, N, K, s);
+  GemmEpilogue ep{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M};
+  // dX(M x K) = gZ(M x N) W(N x K): A(m,k') = gZ[m*ldg+k'], B(k',n') = W[k'*ldw+n']
+  return gemm_simt(gZ, ldg, 1, W, 1, ldw, M, K, N, 1, ep, K, s);
+}
+
+extern "C" size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N,
+                                                        int64_t K) {
+  const int sp = choose_splits(M, N, K);
+  size_t f = size_t(sp) * N * K + colreduce_ws_floats(M, N);
+  const size_t tc = tc_linear_bwd_weight_ws_floats(M, N, K);
+  if (tc > f) f = tc;
+  return f * sizeof(float) + 256;
+}
+
+extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
+                                      const float* X, int64_t ldx, int64_t M,
+                                      int64_t N, int64_t K, float* dW,
+                                      int64_t lddw, float* db, float* W_upd,
+                                      int64_t ldw, float* b_upd, float lr,
+                                      const int32_t* err_flag, void* workspace,
+                                      size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldx >= K,
+               "bad linear_bwd_weight shape");
+  DLRM_REQUIRE(ws_bytes >= dlrm_linear_bwd_weight_workspace_size(M, N, K) &&
+                   workspace != nullptr,
+               "linear_bwd_weight workspace too small");
+  cudaStream_t s = as_stream(stream);
+  float* ws = static_cast<float*>(workspace);
+  if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K)) {
+    if (int rc = tc_linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, W_upd,
+                                      ldw, lr, err_flag, ws, s))
+      return rc;
+  } else {
+    const int sp = choose_splits(M, N, K);
+    GemmEpilogue ep{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N};
+    // dW(N x K) = gZ^T X: A(m',k') = gZ[k'*ldg + m'], B(k',n') = X[k'*ldx + n']
+    int used = 1;
+    if (int rc = gemm_simt(gZ, 1, ldg, X, 1, ldx, N, K, M, sp, ep, K, s, &used))
+      return rc;
+    if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s))
+      return rc;
+  }
+  if (db || b_upd) {
+    float* cws = ws + size_t(choose_splits(M, N, K)) * N * K;
+    if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K))
+      cws = ws + tc_linear_bwd_weight_ws_floats(M, N, K) - colreduce_ws_floats(M, N);
+    return colreduce(gZ, ldg, nullptr, M, N, db, b_upd, lr, err_flag, cws,
+                     colreduce_ws_floats(M, N), s);
+  }
+  return 0;
+}

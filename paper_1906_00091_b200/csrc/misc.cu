@@ -1,0 +1,61 @@
+// Library bookkeeping: thread-local error message, launch counter, build
+// info, and the dense SGD kernel (ref optim.py:31-35).
+#include "common.cuh"
+
+namespace dlrm {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+// p -= fl(lr * g): __fmul_rn/__fsub_rn keep nvcc from contracting to an FMA,
+// matching numpy's `param -= lr * grad` rounding.
+__global__ void sgd_dense_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                 int64_t n, float lr, const int32_t* err_flag) {
+  if (err_flag && *err_flag) return;
+  const int64_t n4 = n / 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 w = reinterpret_cast<float4*>(p)[i];
+    const float4 d = reinterpret_cast<const float4*>(g)[i];
+    w.x = __fsub_rn(w.x, __fmul_rn(lr, d.x));
+    w.y = __fsub_rn(w.y, __fmul_rn(lr, d.y));
+    w.z = __fsub_rn(w.z, __fmul_rn(lr, d.z));
+    w.w = __fsub_rn(w.w, __fmul_rn(lr, d.w));
+    reinterpret_cast<float4*>(p)[i] = w;
+  }
+  for (int64_t i = n4 * 4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    p[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+}
+
+}  // namespace
+}  // namespace dlrm
+
+using namespace dlrm;
+
+extern "C" const char* dlrm_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int64_t dlrm_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char* dlrm_build_info(void) {
+  return "libdlrmb200 sm_100a";
+}
+
+extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
+                              const int32_t* err_flag, dlrm_stream_t stream) {
+  DLRM_REQUIRE(n >= 0, "negative length");
+  if (n == 0) return 0;
+  DLRM_REQUIRE(reinterpret_cast<uintptr_t>(p) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(g) % 16 == 0,
+               "sgd_dense needs 16-byte aligned buffers");
+  const int64_t blocks = ceil_div(ceil_div(n, 4), 256);
+  sgd_dense_kernel<<<unsigned(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256,
+                     0, as_stream(stream)>>>(p, g, n, lr, err_flag);
+  return check_launch("sgd_dense_kernel");
+}

@@ -1,0 +1,249 @@
+"""Device plan, collectives and the training-step drivers — the reference's
+``dlrmkit.parallel`` API (ref ``pkg/src/dlrmkit/parallel.py``).
+
+* ``partition_tables`` / ``shard_bounds`` / ``make_plan`` / ``DevicePlan``
+  are integer bookkeeping and bit-identical to the reference.
+* ``butterfly_shuffle`` / ``inverse_shuffle`` / ``allreduce`` keep the
+  reference's in-process semantics (used by ``ParallelTrainer`` and tests);
+  the real multi-GPU exchange over NCCL lives in ``distributed.py``.
+* ``train_step`` is the single-device hot path: it runs the fused
+  ``StepEngine`` (CUDA-graph replay after the first call).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .model import DlrmConfig, DlrmModel
+from .optim import Sgd
+from .trainer import StepEngine, StepResult
+
+__all__ = [
+    "DevicePlan", "ShuffleSlice", "CommLog", "StepResult", "partition_tables",
+    "shard_bounds", "make_plan", "butterfly_shuffle", "inverse_shuffle",
+    "allreduce", "allreduce_max", "train_step", "format_comm_report",
+]
+
+
+# --------------------------------------------------------------------------
+# device plan  (ref parallel.py:62-122)
+
+@dataclass
+class DevicePlan:
+    num_devices: int
+    table_assignment: list      # table id -> owning device
+    shard_bounds: list          # len num_devices + 1, contiguous sample ranges
+
+    def validate(self):
+        if self.num_devices < 1:
+            raise ValueError("need at least one device")
+        if any(not 0 <= d < self.num_devices for d in self.table_assignment):
+            raise ValueError("table assigned to a device outside the plan")
+        b = self.shard_bounds
+        if b[0] != 0 or any(x > y for x, y in zip(b, b[1:])):
+            raise ValueError("shard bounds must start at 0 and be nondecreasing")
+        sizes = [y - x for x, y in zip(b, b[1:])]
+        if sizes and max(sizes) - min(sizes) > 1:
+            raise ValueError("shard sizes must differ by at most 1")
+
+    def shard(self, device: int):
+        return self.shard_bounds[device], self.shard_bounds[device + 1]
+
+    @property
+    def batch_size(self) -> int:
+        return self.shard_bounds[-1]
+
+    def owned(self, device: int) -> list:
+        return [t for t, d in enumerate(self.table_assignment) if d == device]
+
+
+def partition_tables(table_sizes, num_devices: int) -> list:
+    """Greedy largest-first, each table to the least-loaded device (lowest id
+    on ties) — bit-identical to ref parallel.py:88-104."""
+    if num_devices < 1:
+        raise ValueError("need at least one device")
+    loads = [0] * num_devices
+    owner = [0] * len(table_sizes)
+    for t in sorted(range(len(table_sizes)), key=lambda t: (-table_sizes[t], t)):
+        dev = min(range(num_devices), key=lambda d: (loads[d], d))
+        owner[t] = dev
+        loads[dev] += table_sizes[t]
+    return owner
+
+
+def shard_bounds(batch_size: int, num_devices: int) -> list:
+    """Contiguous shards, sizes differing by <= 1, earlier devices larger."""
+    base, extra = divmod(batch_size, num_devices)
+    out = [0]
+    for d in range(num_devices):
+        out.append(out[-1] + base + (1 if d < extra else 0))
+    return out
+
+
+def make_plan(config: DlrmConfig, batch_size: int, num_devices: int) -> DevicePlan:
+    sizes = [m * config.sparse_dim for m in config.embedding_sizes]
+    plan = DevicePlan(num_devices, partition_tables(sizes, num_devices),
+                      shard_bounds(batch_size, num_devices))
+    plan.validate()
+    return plan
+
+
+# --------------------------------------------------------------------------
+# collectives, in-process semantics  (ref parallel.py:128-232)
+
+@dataclass
+class ShuffleSlice:
+    source_device: int
+    table_id: int
+    sample_range: tuple
+    values: torch.Tensor
+
+
+@dataclass
+class CommLog:
+    """Per-step record of collective traffic: (step, name, bytes, parties)."""
+
+    entries: list = field(default_factory=list)
+
+    def add(self, step: int, collective: str, nbytes: int, participants: int):
+        self.entries.append((step, collective, int(nbytes), participants))
+
+
+def _nbytes(t) -> int:
+    return int(t.numel() * t.element_size())
+
+
+def butterfly_shuffle(per_table_outputs: dict, plan: DevicePlan,
+                      comm: CommLog | None = None, step: int = 0) -> list:
+    """Per-table full-batch pooled rows (on their owners) -> per-device
+    all-table shards, ascending table id, tagged with the source device."""
+    for t, m in per_table_outputs.items():
+        if m.shape[0] != plan.batch_size:
+            raise ValueError(f"table {t} output has {m.shape[0]} rows, plan "
+                             f"expects {plan.batch_size}")
+    if set(per_table_outputs) != set(range(len(plan.table_assignment))):
+        raise ValueError("per-table outputs do not match the plan's tables")
+    out = [[] for _ in range(plan.num_devices)]
+    moved = 0
+    for dst in range(plan.num_devices):
+        lo, hi = plan.shard(dst)
+        for t in sorted(per_table_outputs):
+            src = plan.table_assignment[t]
+            v = per_table_outputs[t][lo:hi]
+            out[dst].append(ShuffleSlice(src, t, (lo, hi), v))
+            if src != dst:
+                moved += _nbytes(v)
+    if comm is not None:
+        comm.add(step, "butterfly_shuffle", moved, plan.num_devices)
+    return out
+
+
+def inverse_shuffle(per_device_grads: list, plan: DevicePlan,
+                    comm: CommLog | None = None, step: int = 0) -> dict:
+    """Per-device shard gradients -> full-batch gradient per table on its
+    owner, shards concatenated in ascending device (= sample) order."""
+    moved = 0
+    full = {}
+    for t in range(len(plan.table_assignment)):
+        owner = plan.table_assignment[t]
+        parts = []
+        for dev in range(plan.num_devices):
+            g = per_device_grads[dev][t]
+            lo, hi = plan.shard(dev)
+            if g.shape[0] != hi - lo:
+                raise ValueError(f"device {dev} grad for table {t} has "
+                                 f"{g.shape[0]} rows, shard is {hi - lo}")
+            parts.append(g)
+            if dev != owner:
+                moved += _nbytes(g)
+        full[t] = torch.cat(parts, dim=0)
+    if comm is not None:
+        comm.add(step, "grad_reverse_shuffle", moved, plan.num_devices)
+    return full
+
+
+def allreduce(per_replica: list):
+    """Elementwise sum in ascending replica order."""
+    if not per_replica:
+        raise ValueError("allreduce needs at least one replica")
+    shape = tuple(per_replica[0].shape)
+    for i, m in enumerate(per_replica[1:], start=1):
+        if tuple(m.shape) != shape:
+            raise ValueError(f"replica {i} shape {tuple(m.shape)} != replica "
+                             f"0 shape {shape}")
+    out = per_replica[0].clone()
+    for m in per_replica[1:]:
+        out = out + m
+    return out
+
+
+def allreduce_max(per_replica: list):
+    out = per_replica[0].clone()
+    for m in per_replica[1:]:
+        out = torch.maximum(out, m)
+    return out
+
+
+def format_comm_report(comm: CommLog) -> str:
+    lines = ["step, collective, bytes, participants"]
+    for step, name, nbytes, parts in comm.entries:
+        lines.append(f"{step}, {name}, {nbytes}, {parts}")
+    return "\n".join(lines) + "\n"
+
+
+# --------------------------------------------------------------------------
+# single-device training step  (ref parallel.py:250-287)
+
+def _engine_for(model: DlrmModel, batch: int, batches, lr: float,
+                weighted: bool) -> StepEngine:
+    eng = getattr(model, "_engine", None)
+    nnz = [sb.nnz for sb in batches]
+    if (eng is not None and eng.B == batch and eng.lr == float(lr)
+            and eng.weighted == weighted
+            and all(n <= c for n, c in zip(nnz, eng.caps))):
+        return eng
+    caps = [max(n, batch) for n in nnz]
+    if eng is not None:  # grow geometrically so graphs are rarely rebuilt
+        caps = [max(c, int(1.25 * old)) for c, old in zip(caps, eng.caps)]
+    eng = StepEngine(model, batch, caps, lr=lr, weighted=weighted)
+    eng.eager_runs = 0
+    model._engine = eng
+    return eng
+
+
+def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
+               timer=None, use_graph: bool = True) -> StepResult:
+    """One forward/backward/SGD step over a mini-batch on the current GPU.
+
+    Same contract as the reference: updates ``model`` in place and returns
+    (loss, accuracy, probs); an out-of-range index raises LookupIndexError
+    and leaves every parameter untouched."""
+    if not isinstance(optimizer, Sgd):
+        raise NotImplementedError("the fused step implements SGD only")
+    cfg = model.config
+    if len(batches) != cfg.num_tables:
+        raise ValueError(
+            f"got {len(batches)} sparse batches for {cfg.num_tables} tables")
+    b = int(dense_x.shape[0])
+    for t, sb in enumerate(batches):
+        if sb.num_segments != b:
+            raise ValueError(
+                f"sparse batch {t} has {sb.num_segments} segments, batch is {b}")
+    weighted = any(sb.weights is not None for sb in batches)
+    eng = _engine_for(model, b, batches, optimizer.lr, weighted)
+    eng.load(dense_x, [sb.offsets for sb in batches],
+             [sb.indices for sb in batches], labels,
+             [sb.weights for sb in batches] if weighted else None)
+    if eng.graph is None and use_graph and eng.eager_runs >= 1:
+        eng.capture()
+    if eng.graph is not None:
+        eng.graph.replay()
+    else:
+        eng.run()
+        eng.eager_runs += 1
+    if timer is not None and hasattr(timer, "seconds"):
+        timer.seconds.setdefault("train_step", 0.0)
+    return eng.result()

@@ -1,0 +1,387 @@
+"""The fused single-device DLRM training step (the hot path).
+
+``StepEngine`` owns every buffer of one training step for a fixed batch
+size and per-table index capacity, re-homes the model's parameters into two
+flat allocations (all MLP weights+biases; all embedding tables), and issues
+the whole forward/backward/SGD sequence as ~50 kernel launches on one stream
+— optionally captured once into a CUDA graph and replayed.
+
+Reference: ``dlrmkit.parallel.train_step`` (ref parallel.py:250-287) —
+same stage order, same semantics:
+
+    bottom MLP fwd -> pooled lookups -> interaction -> top MLP fwd -> BCE
+    -> top MLP bwd -> interaction bwd -> bottom MLP bwd -> sparse bwd -> SGD
+
+Fusions relative to the reference (all result-preserving):
+  * SGD is fused into each layer's weight-gradient reduction (a layer's
+    data gradient is always computed before its weights change), and into
+    the sparse backward (sort -> segmented fold -> row update);
+  * the last top layer (N = 1) + sigmoid + BCE + logit gradient + accuracy
+    run in one loss-head kernel;
+  * ReLU' masks are applied in the producing GEMM's epilogue;
+  * the bottom MLP writes feature 0 and the lookups write features 1..T of
+    one [B, nf, d] buffer that the interaction reads in place.
+Out-of-range indices set a device error flag; every parameter update checks
+it, so a failing step mutates nothing (the reference raises before any
+update), and the host raises LookupIndexError when it reads the step result.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .embedding import LookupIndexError, SparseBatch
+from .model import DlrmModel, ceil4
+
+__all__ = ["StepEngine", "StepResult"]
+
+INT64_MAX = np.iinfo(np.int64).max
+
+
+class StepResult:
+    """loss, accuracy, probs — the reference's StepResult (parallel.py:243-247)
+    with probs as a CUDA tensor."""
+
+    def __init__(self, loss: float, accuracy: float, probs: torch.Tensor):
+        self.loss, self.accuracy, self.probs = loss, accuracy, probs
+
+    def __repr__(self):
+        return f"StepResult(loss={self.loss:.6f}, accuracy={self.accuracy:.4f})"
+
+
+class StepEngine:
+    """One device's fused training step over a fixed batch geometry.
+
+    ``n_total`` is the global batch the logit gradient is divided by (the
+    reference's ``n_total``; = batch_size on one device).
+    """
+
+    def __init__(self, model: DlrmModel, batch_size: int, capacities=None,
+                 lr: float = 0.1, weighted: bool = False,
+                 n_total: int | None = None):
+        _lib.require_cuda()
+        cfg = model.config
+        self.model, self.cfg = model, cfg
+        self.B = B = int(batch_size)
+        self.T = T = cfg.num_tables
+        self.d = d = cfg.sparse_dim
+        self.nf = nf = T + 1
+        self.lr = float(lr)
+        self.n_total = float(n_total if n_total is not None else B)
+        self.weighted = weighted
+        dev = self.dev = _lib.device()
+        caps = capacities if capacities is not None else [B] * T
+        self.caps = [max(1, int(c)) for c in caps]
+        f32 = dict(dtype=torch.float32, device=dev)
+
+        # ---- parameters: one flat MLP buffer, one table buffer
+        self.layers = model.bottom.layers + model.top.layers
+        self.Lb, self.Lt = len(model.bottom.layers), len(model.top.layers)
+        sizes = []
+        for l in self.layers:
+            sizes += [l.n_out * ceil4(l.n_in), ceil4(l.n_out)]
+        self.param_numel = int(sum(sizes))
+        self.params = torch.zeros(self.param_numel, **f32)
+        off = 0
+        for l in self.layers:
+            nw = l.n_out * ceil4(l.n_in)
+            w = self.params[off:off + nw].view(l.n_out, ceil4(l.n_in))
+            off += nw
+            b = self.params[off:off + l.n_out]
+            off += ceil4(l.n_out)
+            l.rebind(w, b)
+        self.rows = [t.num_rows for t in model.tables]
+        self.row_base = np.concatenate([[0], np.cumsum(self.rows)]).astype(np.int64)
+        self.total_rows = int(self.row_base[-1])
+        self.W_all = torch.empty(self.total_rows * d, **f32)
+        for t, tab in enumerate(model.tables):
+            v = self.W_all[self.row_base[t] * d:self.row_base[t + 1] * d].view(
+                self.rows[t], d)
+            v.copy_(tab.weights)
+            tab.weights = v
+
+        # ---- inputs
+        self.k0 = cfg.dense_dim
+        self.x = torch.zeros((B, ceil4(self.k0)), **f32)
+        self.offsets = torch.zeros((T, B + 1), dtype=torch.int64, device=dev)
+        self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
+        self.indices = torch.zeros(int(self.cap_base[-1]), dtype=torch.int64,
+                                   device=dev)
+        self.iweights = (torch.ones(int(self.cap_base[-1]), **f32)
+                         if weighted else None)
+        self.labels = torch.zeros(B, **f32)
+
+        # ---- activations
+        self.Z = torch.zeros((B, nf * d), **f32)
+        bl = model.bottom.layers
+        self.bact = [torch.zeros((B, ceil4(l.n_out)), **f32) for l in bl[:-1]]
+        self.width = cfg.top_in_dim
+        self.R = torch.zeros((B, ceil4(self.width)), **f32)
+        tl = model.top.layers
+        self.tact = [torch.zeros((B, ceil4(l.n_out)), **f32) for l in tl[:-1]]
+        self.logits = torch.zeros(B, **f32)
+        self.prob = torch.zeros(B, **f32)
+        self.glogit = torch.zeros(B, **f32)
+
+        # ---- gradients
+        self.gtop = [torch.zeros((B, ceil4(l.n_out)), **f32) for l in tl[:-1]]
+        self.gR = torch.zeros((B, ceil4(self.width)), **f32)
+        self.gZ = torch.zeros((B, nf * d), **f32)
+        self.gbot = [torch.zeros((B, ceil4(l.n_out)), **f32) for l in bl[:-1]]
+
+        # ---- workspaces and step result
+        self.emb_ws_bytes = _lib.size("dlrm_emb_bwd_workspace_size",
+                                      int(self.cap_base[-1]), self.total_rows)
+        self.emb_ws = torch.empty(self.emb_ws_bytes, dtype=torch.uint8, device=dev)
+        lin = max(_lib.size("dlrm_linear_bwd_weight_workspace_size", B,
+                            l.n_out, l.n_in) for l in self.layers)
+        lin = max(lin, _lib.size("dlrm_head_bwd_workspace_size", B,
+                                 tl[-1].n_in),
+                  _lib.size("dlrm_bce_head_workspace_size", B))
+        self.lin_ws_bytes = lin
+        self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(2, **f32)
+        self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
+        self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        self._build_descs()
+        self.graph = None
+        self.launches_per_step = None
+
+    # ------------------------------------------------------------------
+    def _build_descs(self):
+        d, nf, B = self.d, self.nf, self.B
+        descs = []
+        for t in range(self.T):
+            cb = int(self.cap_base[t])
+            descs.append(_lib.TableDesc(
+                self.offsets[t].data_ptr(),
+                self.indices.data_ptr() + 8 * cb,
+                (self.iweights.data_ptr() + 4 * cb) if self.weighted else None,
+                int(self.row_base[t]), self.rows[t], (1 + t) * d,
+                self.caps[t], self.model.tables[t].table_id))
+        self._descs = _lib.table_array(descs)
+        self._descs_p = C.cast(self._descs, C.c_void_p)
+        self._feats = _lib.make_features(
+            [(self.Z.data_ptr() + 4 * f * d, nf * d) for f in range(nf)])
+        self._feats_p = C.c_void_p(C.addressof(self._feats))
+        self._gfeat = (C.c_void_p * nf)(
+            *[self.gZ.data_ptr() + 4 * f * d for f in range(nf)])
+        self._gstride = (C.c_int64 * nf)(*([nf * d] * nf))
+
+    # ------------------------------------------------------------------
+    # inputs
+    def load(self, dense, offsets, indices, labels, weights=None, stream=None):
+        """Copy one batch into the engine's input buffers (host numpy arrays
+        or device tensors; per-table lists for offsets/indices/weights)."""
+        B, T = self.B, self.T
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            dx = _to_dev_f32(dense, self.dev)
+            if tuple(dx.shape) != (B, self.k0):
+                raise ValueError(f"dense input {tuple(dx.shape)} != {(B, self.k0)}")
+            self.x[:, :self.k0].copy_(dx, non_blocking=True)
+            for t in range(T):
+                o = offsets[t]
+                i = indices[t]
+                n = int(i.shape[0])
+                if n > self.caps[t]:
+                    raise OverflowError(f"table {t}: {n} indices exceed "
+                                        f"capacity {self.caps[t]}")
+                self.offsets[t].copy_(_to_dev(o, torch.int64, self.dev),
+                                      non_blocking=True)
+                cb = int(self.cap_base[t])
+                self.indices[cb:cb + n].copy_(_to_dev(i, torch.int64, self.dev),
+                                              non_blocking=True)
+                if self.weighted:
+                    w = weights[t] if weights is not None else None
+                    if w is None:
+                        self.iweights[cb:cb + n].fill_(1.0)
+                    else:
+                        self.iweights[cb:cb + n].copy_(
+                            _to_dev_f32(w, self.dev), non_blocking=True)
+            self.labels.copy_(_to_dev_f32(labels, self.dev), non_blocking=True)
+        self._host_indices = indices
+
+    # ------------------------------------------------------------------
+    STAGES = ("bottom_mlp_fwd", "embedding_fwd", "interaction_fwd",
+              "top_mlp_fwd", "loss_head", "top_mlp_bwd", "interaction_bwd",
+              "bottom_mlp_bwd", "embedding_bwd_sgd")
+
+    def launch(self, stream=None, mark=None):
+        """Issue the whole step on ``stream`` (default: current stream).
+        ``mark(stage)`` (profiling only) is called before each stage."""
+        mark = mark or (lambda name: None)
+        s = _lib.stream_handle(stream)
+        L, call, P = self.layers, _lib.call, _lib.ptr
+        B, d, nf, lr = self.B, self.d, self.nf, self.lr
+        relu = _lib.ACT["relu"]
+        ef = P(self.err_flag)
+        call("dlrm_err_reset", P(self.err_pos), self.T, ef, s)
+
+        # bottom MLP forward; the last layer writes feature 0 of Z
+        mark("bottom_mlp_fwd")
+        a, lda = self.x, self.x.stride(0)
+        for i in range(self.Lb):
+            l = L[i]
+            last = i == self.Lb - 1
+            out, ldo = (self.Z, nf * d) if last else (self.bact[i], self.bact[i].stride(0))
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), ldo, B, l.n_out, l.n_in, l.n_out if last else out.shape[1],
+                 relu, s)
+            a, lda = out, ldo
+        # pooled lookups -> features 1..T of Z
+        mark("embedding_fwd")
+        call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
+             P(self.Z), nf * d, P(self.err_pos), ef, s)
+        # interaction -> R
+        mark("interaction_fwd")
+        call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
+             self.R.stride(0), self.R.shape[1], s)
+        # top MLP (all but the N=1 head)
+        mark("top_mlp_fwd")
+        a, lda = self.R, self.R.stride(0)
+        for i in range(self.Lt - 1):
+            l = L[self.Lb + i]
+            out = self.tact[i]
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), out.stride(0), B, l.n_out, l.n_in, out.shape[1],
+                 relu, s)
+            a, lda = out, out.stride(0)
+        mark("loss_head")
+        head = L[-1]
+        ws, wsb = P(self.lin_ws), self.lin_ws_bytes
+        call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), B,
+             head.n_in, P(self.labels), self.n_total, P(self.logits),
+             P(self.prob), P(self.glogit), None, P(self.stats), ws, wsb, s)
+        # head backward (dA masked by the ReLU below it) + fused SGD
+        ga = self.gtop[-1] if self.Lt > 1 else self.gR
+        call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), B,
+             head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None,
+             None, P(head.storage), P(head.bias), lr, ef, ws, wsb, s)
+        # top MLP backward
+        mark("top_mlp_bwd")
+        for i in range(self.Lt - 2, -1, -1):
+            l = L[self.Lb + i]
+            gz = self.gtop[i]
+            xin = self.R if i == 0 else self.tact[i - 1]
+            dx = self.gR if i == 0 else self.gtop[i - 1]
+            mask = None if i == 0 else self.tact[i - 1]
+            call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
+                 l.ldw, P(mask), mask.stride(0) if mask is not None else 0,
+                 P(dx), dx.stride(0), B, l.n_out, l.n_in, s)
+            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin),
+                 xin.stride(0), B, l.n_out, l.n_in, None, 0, None,
+                 P(l.storage), l.ldw, P(l.bias), lr, ef, ws, wsb, s)
+        # interaction backward (bottom's last ReLU folded in for feature 0)
+        mark("interaction_bwd")
+        call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
+             self.gR.stride(0), C.cast(self._gfeat, C.c_void_p),
+             C.cast(self._gstride, C.c_void_p), 1, s)
+        # bottom MLP backward
+        mark("bottom_mlp_bwd")
+        for i in range(self.Lb - 1, -1, -1):
+            l = L[i]
+            if i == self.Lb - 1:
+                gz, ldg = self.gZ, nf * d
+            else:
+                gz, ldg = self.gbot[i], self.gbot[i].stride(0)
+            xin = self.x if i == 0 else self.bact[i - 1]
+            if i > 0:
+                dx = self.gbot[i - 1]
+                call("dlrm_linear_bwd_data", P(gz), ldg, P(l.storage), l.ldw,
+                     P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
+                     dx.stride(0), B, l.n_out, l.n_in, s)
+            call("dlrm_linear_bwd_weight", P(gz), ldg, P(xin), xin.stride(0),
+                 B, l.n_out, l.n_in, None, 0, None, P(l.storage), l.ldw,
+                 P(l.bias), lr, ef, ws, wsb, s)
+        # sparse backward fused with the row-wise SGD update
+        mark("embedding_bwd_sgd")
+        call("dlrm_emb_bwd_sgd", P(self.W_all), d, self._descs_p, self.T, B,
+             P(self.gZ), nf * d, lr, ef, self.total_rows, P(self.emb_ws),
+             self.emb_ws_bytes, s)
+
+    # ------------------------------------------------------------------
+    def capture(self):
+        """Record launch() into a CUDA graph.  Capturing executes nothing, so
+        run one eager step first (kernel attributes, CUB initialisation)."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n0 = _lib.launch_count()
+        with torch.cuda.graph(g):
+            self.launch()
+        self.launches_per_step = _lib.launch_count() - n0
+        self.graph = g
+        return g
+
+    def profile_stages(self, reps: int = 5, flush=None) -> dict:
+        """Mean milliseconds per stage over ``reps`` eager steps, CUDA events
+        recorded on the launch stream at the stage boundaries (L2 flushed
+        before each rep when ``flush`` is a buffer).  Performs real SGD
+        steps on the current input batch."""
+        stream = torch.cuda.current_stream()
+        acc = {k: 0.0 for k in self.STAGES}
+        for r in range(reps):
+            if flush is not None:
+                flush.fill_(r & 0xff)
+            evs = []
+
+            def mark(name):
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                evs.append((name, e))
+            self.launch(stream, mark)
+            end = torch.cuda.Event(enable_timing=True)
+            end.record(stream)
+            torch.cuda.synchronize()
+            for (name, e), (_, nxt) in zip(evs, evs[1:] + [(None, end)]):
+                acc[name] += e.elapsed_time(nxt)
+        out = {k: v / reps for k, v in acc.items()}
+        out["mlp_total"] = sum(out[k] for k in ("bottom_mlp_fwd", "top_mlp_fwd",
+                                                "loss_head", "top_mlp_bwd",
+                                                "bottom_mlp_bwd"))
+        out["step_total"] = sum(out[k] for k in self.STAGES)
+        return out
+
+    def run(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            n0 = _lib.launch_count()
+            self.launch()
+            self.launches_per_step = _lib.launch_count() - n0
+
+    # ------------------------------------------------------------------
+    def check_errors(self):
+        if int(self.err_flag.item()):
+            pos = self.err_pos.cpu().numpy()
+            for t in range(self.T):
+                if pos[t] != INT64_MAX:
+                    k = int(pos[t])
+                    idx = self._host_indices[t]
+                    val = int(idx[k].item() if isinstance(idx, torch.Tensor)
+                              else idx[k])
+                    tab = self.model.tables[t]
+                    raise LookupIndexError(tab.table_id, k, val, tab.num_rows)
+
+    def result(self) -> StepResult:
+        self.check_errors()
+        st = self.stats.cpu()
+        return StepResult(float(st[0]) / self.B, float(st[1]) / self.B,
+                          self.prob.clone())
+
+
+def _to_dev(a, dtype, dev):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype)
+    return torch.as_tensor(np.asarray(a), device=dev).to(dtype)
+
+
+def _to_dev_f32(a, dev):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=torch.float32)
+    return torch.as_tensor(np.asarray(a, dtype=np.float32), device=dev)

@@ -1,0 +1,46 @@
+"""Shared test helpers (no reference import: runs on the GPU box too)."""
+
+import hashlib
+import json
+
+import numpy as np
+
+from paper_1906_00091_b200.rng import RandomBatchSource
+
+
+def digest(arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def batch_arrays(hb):
+    return [hb.dense, *hb.offsets, *hb.indices, hb.labels]
+
+
+def port_arrays(m):
+    out = []
+    for w, b, _ in m["bottom"] + m["top"]:
+        out += [w, b]
+    return out + list(m["tables"])
+
+
+def traj_inputs(fx):
+    """Config dict and the host batches of a trajectory fixture."""
+    c = json.loads(str(fx["config"]))
+    src = RandomBatchSource(c["tables"], c["bot"][0], c["batch"], c["k"],
+                            c["fixed"], seed=c["seed"], key=0)
+    return c, [src.next_batch() for _ in range(c["steps"])]
+
+
+def rel_err(got, ref, floor=1e-3):
+    """max |got - ref| / (|ref| + floor * max|ref|)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if ref.size == 0:
+        return 0.0
+    scale = np.abs(ref) + floor * max(np.abs(ref).max(), 1e-30)
+    return float((np.abs(got - ref) / scale).max())

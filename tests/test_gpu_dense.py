@@ -1,0 +1,110 @@
+"""MLP layers, interaction and loss head on the GPU vs the float64 oracle.
+
+Tolerances (fp32 kernels vs float64 reference on fp32-rounded inputs):
+max |gpu - ref| / (|ref| + 1e-3 max|ref|) <= 1e-5 for single ops.
+The interaction's output LAYOUT ([z0 | (i,j) i<j row-major]) is bit-exact
+(checked on exactly representable values).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import port
+from paper_1906_00091_b200 import (MlpLayer, MlpParams, bce_from_logits,
+                                   interact, interact_backward, mlp_backward,
+                                   mlp_forward, sgd_step)
+from paper_1906_00091_b200.rng import RngStream
+from tests._util import rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def np64(t):
+    return t.detach().cpu().double().numpy()
+
+
+def f32r(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("dims,acts,batch", [
+    ([13, 512, 256, 64, 16], ["relu"] * 4, 128),
+    ([367, 512, 256, 1], ["relu", "relu", "identity"], 100),
+    ([4, 3], ["relu"], 9), ([100, 1024, 1024, 1], ["relu", "relu", "identity"], 64),
+    ([479, 64, 30], ["relu", "identity"], 33)])
+def test_mlp_forward_backward(dims, acts, batch):
+    rs = RngStream(len(dims) + batch)
+    layers = []
+    for l in range(len(dims) - 1):
+        w = f32r(rs.normal(dims[l + 1], dims[l]) * 0.1)
+        b = f32r(rs.normal(1, dims[l + 1])[0] * 0.1)
+        layers.append((w, b, acts[l]))
+    x = f32r(rs.uniform(batch, dims[0]))
+    gy = f32r(rs.normal(batch, dims[-1]))
+    params = MlpParams([MlpLayer(w, b, a) for w, b, a in layers])
+    out, cache = mlp_forward(params, x)
+    ref, ins, pres = port.mlp_forward([(w.copy(), b.copy(), a) for w, b, a in layers], x)
+    assert rel_err(np64(out), ref) < TOL
+    grads, gx = mlp_backward(params, cache, gy)
+    dws, dbs, gx_ref = port.mlp_backward(layers, ins, pres, gy, batch)
+    assert rel_err(np64(gx), gx_ref) < TOL
+    for l in range(len(layers)):
+        assert rel_err(np64(grads.weights[l]), dws[l]) < TOL, l
+        assert rel_err(np64(grads.biases[l]), dbs[l]) < TOL, l
+
+
+def test_interaction_layout_bit_exact():
+    # ref test_model.py:139-144 hand example
+    out = interact(torch.tensor([[1.0, 0.0]]), [torch.tensor([[0.0, 1.0]]),
+                                                torch.tensor([[1.0, 1.0]])])
+    assert out.cpu().tolist() == [[1.0, 0.0, 0.0, 1.0, 1.0]]
+    # integer-valued features: every dot is exact, so the whole [z0 | pairs]
+    # layout must equal the reference's upper-triangle row-major order
+    rng = np.random.default_rng(5)
+    for nf, d in [(27, 16), (9, 64), (4, 3), (27, 128)]:
+        feats = [rng.integers(-3, 4, (7, d)).astype(np.float64) for _ in range(nf)]
+        got = np64(interact(torch.tensor(feats[0]), [torch.tensor(f) for f in feats[1:]]))
+        assert np.array_equal(got, port.interact(feats[0], feats[1:]))
+
+
+@pytest.mark.parametrize("nf,d,b", [(27, 16, 64), (9, 64, 33), (27, 128, 10), (3, 3, 5)])
+def test_interaction_values_and_backward(nf, d, b):
+    rs = RngStream(nf * d)
+    feats = [f32r(rs.normal(b, d)) for _ in range(nf)]
+    tf = [torch.tensor(f, dtype=torch.float32) for f in feats]
+    out = interact(tf[0], tf[1:])
+    ref = port.interact(feats[0], feats[1:])
+    assert out.shape == ref.shape
+    assert rel_err(np64(out), ref) < TOL
+    g = f32r(rs.normal(b, ref.shape[1]))
+    g0, gs = interact_backward(tf[0], tf[1:], torch.tensor(g, dtype=torch.float32))
+    r0, rs_ = port.interact_backward(feats[0], feats[1:], g)
+    assert rel_err(np64(g0), r0) < TOL
+    for a, r in zip(gs, rs_):
+        assert rel_err(np64(a), r) < TOL
+
+
+def test_bce_from_logits():
+    rs = RngStream(21)
+    z = f32r(rs.normal(1, 1000)[0] * 4)
+    y = (rs.uniform(1, 1000)[0] < 0.5).astype(np.float64)
+    m, g, per = bce_from_logits(torch.tensor(z), torch.tensor(y))
+    rm, rg, rper = port.bce_from_logits(z, y)
+    assert abs(m - rm) <= 1e-5 * abs(rm)
+    assert rel_err(np64(g), rg) < TOL and rel_err(np64(per), rper) < TOL
+
+
+def test_sgd_dense_rounding():
+    # ref test_optim.py:24-27, and w - fl(lr*g) exactly (no FMA)
+    p = torch.tensor([1.0], device="cuda")
+    sgd_step(p, torch.tensor([2.0], device="cuda"), 0.5)
+    assert p.item() == 0.0
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal(1001).astype(np.float32)
+    g = rng.standard_normal(1001).astype(np.float32)
+    t = torch.tensor(w, device="cuda")
+    sgd_step(t, torch.tensor(g, device="cuda"), 0.1)
+    exp = w - np.float32(0.1) * g
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), exp.view(np.uint32))

