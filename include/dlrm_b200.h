@@ -202,6 +202,10 @@ int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
 
 /* ---- misc --------------------------------------------------------------- */
 
+/* GEMM kernel selection (tests / A-B measurements): 0 = tcgen05 3xTF32
+ * wherever the shape and strides allow (default), 1 = SIMT fp32 only. */
+int dlrm_gemm_mode(int32_t mode);
+
 /* Count of this library's kernel launches since load (for bench.py). */
 int64_t dlrm_launch_count(void);
 const char* dlrm_last_error(void);

@@ -56,6 +56,7 @@ _SIGS = {
                       _vp, _vp, _vp, _f32, _vp, _vp, _sz, _vp],
     "dlrm_relu_grad": [_vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp],
     "dlrm_sgd_dense": [_vp, _vp, _i64, _f32, _vp, _vp],
+    "dlrm_gemm_mode": [_i32],
 }
 _SIZE_FNS = {
     "dlrm_emb_bwd_workspace_size": [_i64, _i64],

@@ -21,9 +21,13 @@ inline cudaStream_t as_stream(dlrm_stream_t s) {
   return reinterpret_cast<cudaStream_t>(s);
 }
 
-// Launch-site check: captures the launch error (never synchronises).
+bool debug_sync();
+
+// Launch-site check: captures the launch error (never synchronises, except
+// with DLRM_DEBUG_SYNC=1 set in the environment, for debugging).
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync()) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return 2;

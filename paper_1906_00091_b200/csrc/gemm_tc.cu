@@ -1,40 +1,518 @@
-// tcgen05 3xTF32 GEMMs — placeholder until the tensor-core kernels land;
-// every predicate declines so the SIMT path runs.
+// fp32-accurate MLP GEMMs on the 5th-generation tensor cores (tcgen05).
+//
+//   D[M x N] = sum_k A(m, k) * B(n, k)        (fp32 in, fp32 out)
+//
+// computed as 3xTF32: x = hi + lo with hi = x rounded to the nearest TF32
+// (cvt.rna.tf32.f32) and lo = x - hi (exact in fp32),
+// then D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.  Single
+// TF32 fails the reference tolerance on updated weights (SURVEY Appendix A:
+// 6e-2); 3xTF32 matches fp32 (1.6e-7 loss, 9e-7 weights).
+//
+// Operands are fetched by TMA (cp.async.bulk.tensor, 128B swizzle) straight
+// from the row-major activations/weights, K-major or MN-major as each GEMM
+// needs (tcgen05 kind::tf32 accepts MN-major descriptors), so no transposed
+// copies exist anywhere:
+//   forward      Y  = X W^T      A = X  (K-major)   B = W (K-major)
+//   data grad    dX = gZ W       A = gZ (K-major)   B = W (MN-major)
+//   weight grad  dW = gZ^T X     A = gZ (MN-major)  B = X (MN-major)
+//
+// CTA = 6 warps, one 128 x BN output tile, 3-stage smem ring:
+//   warp 0     TMA producer (one thread)
+//   warp 1     TMEM allocator + MMA issuer (one thread)
+//   warps 2-5  hi/lo splitter for each landed stage, then the epilogue
+//              (tcgen05.ld 32x32b -> bias/ReLU/mask -> global)
+// Barriers: full[s] (TMA tx), conv[s] (4 splitter warps), empty[s]
+// (tcgen05.commit), acc_full (tcgen05.commit after the last k-block).
+#include <cuda.h>
+
+#include "gemm.cuh"
 #include "gemm_tc.cuh"
 
 namespace dlrm {
+namespace {
 
-bool tc_linear_fwd_ok(const float*, int64_t, const float*, int64_t,
-                      const float*, int64_t, int64_t, int64_t, int64_t,
-                      int64_t) {
-  return false;
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 per 128-byte swizzle row
+constexpr int STAGES = 3;
+constexpr int THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-int tc_linear_fwd(const float*, int64_t, const float*, int64_t, const float*,
-                  float*, int64_t, int64_t, int64_t, int64_t, int64_t, int,
-                  cudaStream_t) {
-  set_error("tcgen05 linear_fwd not built");
-  return 1;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-bool tc_linear_bwd_data_ok(const float*, int64_t, const float*, int64_t,
-                           const float*, int64_t, int64_t, int64_t, int64_t) {
-  return false;
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
 }
-int tc_linear_bwd_data(const float*, int64_t, const float*, int64_t,
-                       const float*, int64_t, float*, int64_t, int64_t,
-                       int64_t, int64_t, cudaStream_t) {
-  set_error("tcgen05 linear_bwd_data not built");
-  return 1;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-bool tc_linear_bwd_weight_ok(const float*, int64_t, const float*, int64_t,
-                             int64_t, int64_t, int64_t) {
-  return false;
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
-size_t tc_linear_bwd_weight_ws_floats(int64_t, int64_t, int64_t) { return 0; }
-int tc_linear_bwd_weight(const float*, int64_t, const float*, int64_t, int64_t,
-                         int64_t, int64_t, float*, int64_t, float*, int64_t,
-                         float, const int32_t*, float*, cudaStream_t) {
-  set_error("tcgen05 linear_bwd_weight not built");
-  return 1;
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1").  K-major tiles use
+// SWIZZLE_128B (layout 2: 16-byte chunks XOR row%8, 1024-byte atoms);
+// MN-major tf32 tiles must use SWIZZLE_128B_BASE32B (layout 1: 32-byte chunks
+// XOR row%4, 512-byte atoms) — the only MN-major layout tf32 accepts; TMA
+// writes it with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) |
+         (uint64_t(layout) << 61);
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128.
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) |
+         (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// x = hi + lo: hi = x rounded to nearest TF32 (|lo| <= 2^-12 |x|), lo exact.
+__device__ __forceinline__ float4 split_hi(float4 v, float4& lo) {
+  float4 h;
+  h.x = tf32_rna(v.x);
+  h.y = tf32_rna(v.y);
+  h.z = tf32_rna(v.z);
+  h.w = tf32_rna(v.w);
+  lo.x = v.x - h.x;
+  lo.y = v.y - h.y;
+  lo.z = v.z - h.z;
+  lo.w = v.w - h.w;
+  return h;
+}
+
+struct TcArgs {
+  int64_t M, N, K;
+  int k_tiles_per_split;
+  int k_tiles;
+  GemmEpilogue ep;
+};
+
+template <bool A_MN, bool B_MN, int BN>
+__global__ void __launch_bounds__(THREADS, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               TcArgs args) {
+  constexpr uint32_t A_BYTES = BM * BK * 4;  // 16 KB
+  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  // NBIG interleaved accumulators for hi*hi (k-block it -> it % NBIG) plus
+  // one for the small cross terms; summed in fp32 in the epilogue.  The
+  // tensor core's fp32 accumulation truncates, so its error grows with the
+  // number of accumulate steps per chain: splitting cuts it ~3*NBIG-fold
+  // (measured: 8.5e-6 -> fp32-FFMA level at K = 1024).
+  constexpr int NBIG = 3;
+  constexpr uint32_t COLS_NEEDED = (NBIG + 1) * BN;
+  constexpr uint32_t TMEM_COLS = COLS_NEEDED <= 32 ? 32 : COLS_NEEDED <= 64 ? 64
+                               : COLS_NEEDED <= 128 ? 128 : COLS_NEEDED <= 256 ? 256 : 512;
+  static_assert(COLS_NEEDED <= 512, "TMEM overflow");
+  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* conv = bars + STAGES;
+  uint64_t* empty = bars + 2 * STAGES;
+  uint64_t* acc_full = bars + 3 * STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int kt0 = blockIdx.z * args.k_tiles_per_split;
+  const int kt1 = min(args.k_tiles, kt0 + args.k_tiles_per_split);
+  const int nk = kt1 - kt0;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        const int k0 = (kt0 + it) * BK;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c)
+            tma_load_2d(st + c * 32 * BK * 4, &tmA, &full[s], int(m0 + 32 * c), k0);
+        } else {
+          tma_load_2d(st, &tmA, &full[s], k0, int(m0));
+        }
+        uint8_t* sb = st + 2 * A_BYTES;
+        if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c)
+            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
+          if (BN % 32)  // BN == 16: a single 16-wide box
+            tma_load_2d(sb, &tmB, &full[s], int(n0), k0);
+        } else {
+          tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&conv[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_hi = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t a_lo = a_hi + A_BYTES;
+        const uint32_t b_hi = a_hi + 2 * A_BYTES;
+        const uint32_t b_lo = b_hi + B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
+          const uint32_t ao = A_MN ? kk * 1024 : kk * 32;
+          const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
+          const uint32_t a_lbo = A_MN ? 32 * BK * 4 : 16, a_sbo = A_MN ? 512 : 1024;
+          const uint32_t b_lbo = B_MN ? 32 * BK * 4 : 16, b_sbo = B_MN ? 512 : 1024;
+          const uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
+          const uint64_t dah = smem_desc(a_hi + ao, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = smem_desc(a_lo + ao, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = smem_desc(b_hi + bo, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = smem_desc(b_lo + bo, b_lbo, b_sbo, b_lay);
+          const uint32_t big = tmem + uint32_t((it % NBIG) * BN);
+          const uint32_t small = tmem + uint32_t(NBIG * BN);
+          const uint32_t acc_small = (it > 0 || kk > 0) ? 1u : 0u;
+          const uint32_t acc_big = (it >= NBIG || kk > 0) ? 1u : 0u;
+          mma_tf32(small, dal, dbh, IDESC, acc_small);
+          mma_tf32(small, dah, dbl, IDESC, 1u);
+          mma_tf32(big, dah, dbh, IDESC, acc_big);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(acc_full);
+    }
+  } else {
+    // ---- splitter warps (2..5): hi/lo split of every landed stage
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      float4* ahi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
+      float4* alo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + A_BYTES);
+      float4* bhi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * A_BYTES);
+      float4* blo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * A_BYTES + B_BYTES);
+#pragma unroll 4
+      for (int i = ct; i < int(A_BYTES / 16); i += 128) {
+        float4 lo;
+        const float4 h = split_hi(ahi[i], lo);
+        ahi[i] = h;
+        alo[i] = lo;
+      }
+#pragma unroll 4
+      for (int i = ct; i < int(B_BYTES / 16); i += 128) {
+        float4 lo;
+        const float4 h = split_hi(bhi[i], lo);
+        bhi[i] = h;
+        blo[i] = lo;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
+    }
+    // ---- epilogue: TMEM lanes [32q, 32q+32) belong to warp with warp%4 == q
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int64_t row = m0 + 32 * q + lane;
+    const GemmEpilogue& ep = args.ep;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16], t[16];
+      const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(c0);
+      tmem_ld16(lane_base + uint32_t(NBIG * BN), v);  // cross terms
+      const int used = nk < NBIG ? nk : NBIG;
+      for (int j = 0; j < used; ++j) {
+        tmem_ld16(lane_base + uint32_t(j * BN), t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += t[i];
+      }
+      if (row < args.M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          apply_epilogue(ep, row, n0 + c0 + j, args.N, v[j], blockIdx.z);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+int g_tc_mode = 0;  // 0: use tcgen05 where the shape allows; 1: never
+
+bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
+            int64_t ld_elems, int box_inner, int box_outer, CUtensorMapSwizzle swz) {
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld_elems) * 4};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      const_cast<float*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+constexpr size_t smem_bytes(int bn) {
+  return size_t(STAGES) * (2 * BM * BK * 4 + 2 * bn * BK * 4) + 1024 + 256;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
+              int splits, cudaStream_t s) {
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
+  const size_t sm = smem_bytes(BN);
+  static bool configured = false;
+  if (!configured) {
+    DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    configured = true;
+  }
+  dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)), unsigned(splits));
+  k<<<grid, THREADS, sm, s>>>(a, b, args);
+  return check_launch("tc_gemm_kernel");
+}
+
+// Pick the N tile: the largest of {128, 64, 32, 16} that still gives >= ~100
+// CTAs (148 SMs, one CTA each), else 16.
+int pick_bn(int64_t M, int64_t n_grid) {
+  const int64_t mt = ceil_div(M, BM);
+  for (int bn : {128, 64, 32}) {
+    if (n_grid >= bn && mt * ceil_div(n_grid, bn) >= 100) return bn;
+  }
+  if (n_grid > 64) return 32;
+  if (n_grid > 32) return 64 <= n_grid ? 64 : 32;
+  return n_grid > 16 ? 32 : 16;
+}
+
+template <bool A_MN, bool B_MN>
+int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
+           int bn, int splits, cudaStream_t s) {
+  switch (bn) {
+    case 16: return launch_bn<A_MN, B_MN, 16>(a, b, args, n_grid, splits, s);
+    case 32: return launch_bn<A_MN, B_MN, 32>(a, b, args, n_grid, splits, s);
+    case 64: return launch_bn<A_MN, B_MN, 64>(a, b, args, n_grid, splits, s);
+    default: return launch_bn<A_MN, B_MN, 128>(a, b, args, n_grid, splits, s);
+  }
+}
+
+// TMA boxes: K-major operand -> box {BK, rows}; MN-major -> box {32 (or 16), BK}
+bool map_operand(CUtensorMap* m, const float* p, bool mn_major, int64_t mn, int64_t k,
+                 int64_t ld, int rows) {
+  if (!aligned16(p) || (ld % 4) != 0) return false;
+  if (mn_major)
+    return encode(m, p, mn, k, ld, rows < 32 ? rows : 32, BK,
+                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  return encode(m, p, k, mn, ld, BK, rows, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+}  // namespace
+
+bool tc_enabled() { return g_tc_mode == 0; }
+
+bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* Y,
+                      int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid) {
+  (void)Y;
+  (void)ldy;
+  return tc_enabled() && M >= 1 && N >= 16 && K >= 1 && aligned16(X) && aligned16(W) &&
+         ldx % 4 == 0 && ldw % 4 == 0 && n_grid >= N;
+}
+
+int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* b,
+                  float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
+                  int act, cudaStream_t s) {
+  const int bn = pick_bn(M, n_grid);
+  CUtensorMap ma, mb;
+  DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
+                   map_operand(&mb, W, false, N, K, ldw, bn),
+               "tensor map encoding failed (linear_fwd)");
+  TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M}};
+  a.k_tiles = int(ceil_div(K, BK));
+  a.k_tiles_per_split = a.k_tiles;
+  return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
+}
+
+bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
+                           const float* dX, int64_t ldx, int64_t M, int64_t N, int64_t K) {
+  (void)dX;
+  (void)ldx;
+  return tc_enabled() && M >= 1 && K >= 32 && N >= 1 && aligned16(gZ) && aligned16(W) &&
+         ldg % 4 == 0 && ldw % 4 == 0;
+}
+
+int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
+                       const float* mask, int64_t ldm, float* dX, int64_t ldx, int64_t M,
+                       int64_t N, int64_t K, cudaStream_t s) {
+  // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
+  int bn = pick_bn(M, K);
+  if (bn < 32) bn = 32;
+  CUtensorMap ma, mb;
+  DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
+                   map_operand(&mb, W, true, K, N, ldw, bn),
+               "tensor map encoding failed (linear_bwd_data)");
+  TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M}};
+  a.k_tiles = int(ceil_div(N, BK));
+  a.k_tiles_per_split = a.k_tiles;
+  return launch<false, true>(ma, mb, a, K, bn, 1, s);
+}
+
+bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
+                             int64_t M, int64_t N, int64_t K) {
+  return tc_enabled() && M >= 32 && N >= 32 && K >= 32 && aligned16(gZ) && aligned16(X) &&
+         ldg % 4 == 0 && ldx % 4 == 0;
+}
+
+namespace {
+int weight_splits(int64_t M, int64_t N, int64_t K, int bn) {
+  const int64_t tiles = ceil_div(N, BM) * ceil_div(K, bn);
+  const int64_t kt = ceil_div(M, BK);
+  int64_t s = ceil_div(2 * kNumSMs, tiles);
+  if (s > kt / 4) s = kt / 4;
+  if (s > 16) s = 16;
+  return int(s < 1 ? 1 : s);
+}
+}  // namespace
+
+size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K) {
+  const int bn = pick_bn(N, K);
+  const int sp = weight_splits(M, N, K, bn);
+  return size_t(sp) * N * K + size_t(ceil_div(M, 256) + 1) * N;
+}
+
+int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
+                         int64_t N, int64_t K, float* dW, int64_t lddw, float* W_upd,
+                         int64_t ldw, float lr, const int32_t* err_flag, float* ws,
+                         cudaStream_t s) {
+  // dW (N x K) = gZ^T X: GEMM m = N (MN-major in gZ), n = K (MN-major in X), k = M
+  const int bn = pick_bn(N, K) < 32 ? 32 : pick_bn(N, K);
+  const int sp = weight_splits(M, N, K, bn);
+  CUtensorMap ma, mb;
+  DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
+                   map_operand(&mb, X, true, K, M, ldx, bn),
+               "tensor map encoding failed (linear_bwd_weight)");
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N}};
+  a.k_tiles = int(ceil_div(M, BK));
+  a.k_tiles_per_split = int(ceil_div(a.k_tiles, sp));
+  const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
+  if (int rc = launch<true, true>(ma, mb, a, K, bn, used, s)) return rc;
+  return splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s);
 }
 
 }  // namespace dlrm
+
+extern "C" int dlrm_gemm_mode(int32_t mode) {
+  dlrm::g_tc_mode = mode;
+  return 0;
+}

@@ -1,5 +1,7 @@
 // Library bookkeeping: thread-local error message, launch counter, build
 // info, and the dense SGD kernel (ref optim.py:31-35).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace dlrm {
@@ -10,6 +12,13 @@ std::atomic<int64_t> g_launches{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool debug_sync() {
+  static const bool on = [] {
+    const char* v = getenv("DLRM_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {

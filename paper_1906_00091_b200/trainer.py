@@ -319,10 +319,61 @@ class StepEngine:
         return g
 
     def profile_stages(self, reps: int = 5, flush=None) -> dict:
-        """Mean milliseconds per stage over ``reps`` eager steps, CUDA events
-        recorded on the launch stream at the stage boundaries (L2 flushed
-        before each rep when ``flush`` is a buffer).  Performs real SGD
-        steps on the current input batch."""
+        """Mean milliseconds per stage over ``reps`` steps.  The step is
+        captured into a separate CUDA graph with event-record nodes at the
+        stage boundaries, so host launch overhead does not pollute the
+        numbers (eager fallback if event capture is unavailable).  Performs
+        real SGD steps on the current input batch."""
+        stream = torch.cuda.current_stream()
+        evs = []
+
+        def mark(name):
+            try:  # external=True: a real event-record node inside the graph
+                e = torch.cuda.Event(enable_timing=True, external=True)
+            except TypeError:
+                e = torch.cuda.Event(enable_timing=True)
+            e.record(torch.cuda.current_stream())
+            evs.append((name, e))
+
+        graph = None
+        try:
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self.launch(mark=mark)
+                mark("end")
+        except Exception:
+            graph, evs = None, []
+        acc = {k: 0.0 for k in self.STAGES}
+        for r in range(reps):
+            if flush is not None:
+                flush.fill_(r & 0xff)
+            if graph is not None:
+                graph.replay()
+            else:
+                evs.clear()
+                self.launch(stream, mark)
+                mark("end")
+            torch.cuda.synchronize()
+            try:
+                for (name, e), (_, nxt) in zip(evs[:-1], evs[1:]):
+                    acc[name] += e.elapsed_time(nxt)
+            except Exception:
+                if graph is None:
+                    raise
+                graph, evs = None, []  # fall back to eager marks
+                acc = {k: 0.0 for k in self.STAGES}
+                return self.profile_stages(reps, flush) if False else \
+                    self._profile_eager(reps, flush)
+        out = {k: v / reps for k, v in acc.items()}
+        out["mlp_total"] = sum(out[k] for k in ("bottom_mlp_fwd", "top_mlp_fwd",
+                                                "loss_head", "top_mlp_bwd",
+                                                "bottom_mlp_bwd"))
+        out["step_total"] = sum(out[k] for k in self.STAGES)
+        out["captured"] = graph is not None
+        return out
+
+    def _profile_eager(self, reps, flush):
         stream = torch.cuda.current_stream()
         acc = {k: 0.0 for k in self.STAGES}
         for r in range(reps):
@@ -335,16 +386,16 @@ class StepEngine:
                 e.record(stream)
                 evs.append((name, e))
             self.launch(stream, mark)
-            end = torch.cuda.Event(enable_timing=True)
-            end.record(stream)
+            mark("end")
             torch.cuda.synchronize()
-            for (name, e), (_, nxt) in zip(evs, evs[1:] + [(None, end)]):
+            for (name, e), (_, nxt) in zip(evs[:-1], evs[1:]):
                 acc[name] += e.elapsed_time(nxt)
         out = {k: v / reps for k, v in acc.items()}
         out["mlp_total"] = sum(out[k] for k in ("bottom_mlp_fwd", "top_mlp_fwd",
                                                 "loss_head", "top_mlp_bwd",
                                                 "bottom_mlp_bwd"))
         out["step_total"] = sum(out[k] for k in self.STAGES)
+        out["captured"] = False
         return out
 
     def run(self):

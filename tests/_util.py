@@ -44,3 +44,12 @@ def rel_err(got, ref, floor=1e-3):
         return 0.0
     scale = np.abs(ref) + floor * max(np.abs(ref).max(), 1e-30)
     return float((np.abs(got - ref) / scale).max())
+
+
+def maxnorm_err(got, ref):
+    """max |got - ref| / max |ref| (normwise, per tensor)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if ref.size == 0:
+        return 0.0
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))

@@ -1,0 +1,122 @@
+"""tcgen05 3xTF32 GEMMs (forward, data gradient, weight gradient) vs a
+float64 reference, and vs the SIMT fp32 kernels.
+
+Tolerance: normwise max|err| / max|ref| <= 1e-5 (fp32-level; single-pass
+TF32 would be ~1e-3)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1906_00091_b200 import _lib
+from tests._util import maxnorm_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+SHAPES = [(2048, 1024, 1024), (2048, 512, 512), (2048, 64, 512), (2048, 1024, 100),
+          (2048, 512, 13), (128, 512, 52), (64, 256, 367), (33, 30, 64), (300, 16, 64),
+          (4096, 128, 479), (2048, 16, 64)]
+
+
+def ceil4(n):
+    return (n + 3) // 4 * 4
+
+
+def rand(shape, seed, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(shape, generator=g, device="cuda") * scale
+
+
+def linear_fwd(X, W, b, N, K, act):
+    M = X.shape[0]
+    Y = torch.full((M, ceil4(N)), float("nan"), device="cuda")
+    _lib.call("dlrm_linear_fwd", _lib.ptr(X), X.stride(0), _lib.ptr(W), W.stride(0),
+              _lib.ptr(b), _lib.ptr(Y), Y.stride(0), M, N, K, Y.shape[1], act,
+              _lib.stream_handle())
+    return Y
+
+
+@pytest.fixture(params=[0, 1], ids=["tcgen05", "simt"])
+def mode(request):
+    _lib.call("dlrm_gemm_mode", request.param)
+    yield request.param
+    _lib.call("dlrm_gemm_mode", 0)
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_linear_fwd(mode, M, N, K):
+    X = torch.zeros((M, ceil4(K)), device="cuda")
+    X[:, :K] = rand((M, K), 1)
+    W = torch.zeros((N, ceil4(K)), device="cuda")
+    W[:, :K] = rand((N, K), 2, K ** -0.5)
+    b = rand((N,), 3)
+    Y = linear_fwd(X, W, b, N, K, 1)
+    ref = torch.relu(X[:, :K].double() @ W[:, :K].double().T + b.double())
+    assert maxnorm_err(Y[:, :N].cpu(), ref.cpu()) < TOL
+    assert bool((Y[:, N:] == 0).all())
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_linear_bwd_data(mode, M, N, K):
+    gZ = torch.zeros((M, ceil4(N)), device="cuda")
+    gZ[:, :N] = rand((M, N), 4)
+    W = torch.zeros((N, ceil4(K)), device="cuda")
+    W[:, :K] = rand((N, K), 5, N ** -0.5)
+    mask = torch.relu(rand((M, ceil4(K)), 6))
+    dX = torch.full((M, ceil4(K)), float("nan"), device="cuda")
+    _lib.call("dlrm_linear_bwd_data", _lib.ptr(gZ), gZ.stride(0), _lib.ptr(W), W.stride(0),
+              _lib.ptr(mask), mask.stride(0), _lib.ptr(dX), dX.stride(0), M, N, K,
+              _lib.stream_handle())
+    ref = (gZ[:, :N].double() @ W[:, :K].double()) * (mask[:, :K] > 0).double()
+    assert maxnorm_err(dX[:, :K].cpu(), ref.cpu()) < TOL
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_linear_bwd_weight_and_sgd(mode, M, N, K):
+    gZ = torch.zeros((M, ceil4(N)), device="cuda")
+    gZ[:, :N] = rand((M, N), 7, M ** -0.5)
+    X = torch.zeros((M, ceil4(K)), device="cuda")
+    X[:, :K] = rand((M, K), 8)
+    dW = torch.full((N, K), float("nan"), device="cuda")
+    db = torch.full((N,), float("nan"), device="cuda")
+    W = torch.zeros((N, ceil4(K)), device="cuda")
+    W[:, :K] = rand((N, K), 9)
+    bias = rand((N,), 10)
+    W0, b0 = W.clone(), bias.clone()
+    wsb = _lib.size("dlrm_linear_bwd_weight_workspace_size", M, N, K)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("dlrm_linear_bwd_weight", _lib.ptr(gZ), gZ.stride(0), _lib.ptr(X), X.stride(0),
+              M, N, K, _lib.ptr(dW), dW.stride(0), _lib.ptr(db), _lib.ptr(W), W.stride(0),
+              _lib.ptr(bias), 0.5, _lib.ptr(flag), _lib.ptr(ws), wsb, _lib.stream_handle())
+    refw = gZ[:, :N].double().T @ X[:, :K].double()
+    refb = gZ[:, :N].double().sum(0)
+    assert maxnorm_err(dW.cpu(), refw.cpu()) < TOL
+    assert maxnorm_err(db.cpu(), refb.cpu()) < TOL
+    # fused SGD used exactly the stored gradient: W = W0 - fl(0.5*dW)
+    exp = (W0[:, :K] - 0.5 * dW)
+    assert torch.equal(W[:, :K], exp)
+    assert torch.equal(bias, b0 - 0.5 * db)
+    assert bool((W[:, K:] == 0).all())
+
+
+def test_tensor_core_path_differs_from_simt():
+    """Guard against a silent fallback: the two kernels round differently."""
+    M, N, K = 2048, 1024, 1024
+    X = rand((M, K), 11)
+    W = rand((N, K), 12, K ** -0.5)
+    b = torch.zeros(N, device="cuda")
+    _lib.call("dlrm_gemm_mode", 0)
+    n0 = _lib.launch_count()
+    y_tc = linear_fwd(X, W, b, N, K, 0)
+    _lib.call("dlrm_gemm_mode", 1)
+    y_simt = linear_fwd(X, W, b, N, K, 0)
+    _lib.call("dlrm_gemm_mode", 0)
+    assert _lib.launch_count() - n0 == 2
+    assert not torch.equal(y_tc, y_simt)
+    ref = X.double() @ W.double().T
+    e_tc = maxnorm_err(y_tc.cpu(), ref.cpu())
+    e_simt = maxnorm_err(y_simt.cpu(), ref.cpu())
+    print(f"K=1024 normwise error: tcgen05 3xTF32 {e_tc:.2e}, SIMT fp32 {e_simt:.2e}")
+    assert e_tc < 2e-5  # TC fp32 accumulation is ~6x looser than FFMA chains
