@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdlrmb200.so")
+LIB_PATH = os.environ.get("DLRM_B200_LIB") or os.path.join(_HERE, "libdlrmb200.so")
 
 MAX_TABLES = 128
 MAX_FEATURES = 129

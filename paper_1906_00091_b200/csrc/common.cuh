@@ -10,7 +10,7 @@
 #include <atomic>
 #include <string>
 
-#include "../../include/dlrm_b200.h"
+#include "dlrm_b200.h"
 
 namespace dlrm {
 

@@ -254,7 +254,8 @@ template <int VEC, int LPB, int NV, bool COALESCE>
 __global__ void __launch_bounds__(fold_groups<LPB>() * LPB)
 emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   using V = typename VecT<VEC>::T;
-  constexpr int CH = 32;
+  constexpr int CH = 32;  // sorted slots staged per batch
+  constexpr int U = 8;    // gradient rows in flight per lane
   constexpr int GROUPS = fold_groups<LPB>();
   __shared__ uint32_t s_key[GROUPS][CH];
   __shared__ int64_t s_goff[GROUPS][CH];
@@ -267,36 +268,42 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   const int64_t start = chunk * CH;
   if (start >= fa.n) return;
   if (!COALESCE && fa.err_flag && *fa.err_flag) return;
-  const int cnt = int(fa.n - start < CH ? fa.n - start : CH);
+  const int64_t limit = start + CH < fa.n ? start + CH : fa.n;  // owned run starts
   const int64_t nvec = dim / VEC;
 
-  // stage keys, grad-row offsets and weights of this chunk
-  for (int i = lane; i < cnt; i += LPB) {
-    const uint32_t k = fa.keys[start + i];
-    s_key[g][i] = k;
-    int64_t goff = 0;
-    float w = 1.f;
-    if (k != fa.sentinel) {
-      const int t = table_of_row(ts, k);
-      const uint32_t slot = fa.vals[start + i];
-      goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
-      if (ts.t[t].weights) w = __ldg(ts.t[t].weights + (slot - ts.cap_base[t]));
+  // stage keys, gradient-row offsets and weights of slots [base, base+CH)
+  auto stage = [&](int64_t base) -> int {
+    const int cnt = int(fa.n - base < CH ? fa.n - base : CH);
+    __syncwarp(mask);
+    for (int i = lane; i < cnt; i += LPB) {
+      const uint32_t k = fa.keys[base + i];
+      s_key[g][i] = k;
+      int64_t goff = 0;
+      float w = 1.f;
+      if (k != fa.sentinel) {
+        const int t = table_of_row(ts, k);
+        const uint32_t slot = fa.vals[base + i];
+        goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
+        if (ts.t[t].weights) w = __ldg(ts.t[t].weights + (slot - ts.cap_base[t]));
+      }
+      s_goff[g][i] = goff;
+      s_w[g][i] = w;
     }
-    s_goff[g][i] = goff;
-    s_w[g][i] = w;
-  }
-  const uint32_t prev = start > 0 ? fa.keys[start - 1] : fa.sentinel;
-  __syncwarp(mask);
+    __syncwarp(mask);
+    return cnt;
+  };
 
-  int i0 = 0;
-  if (start > 0) {
-    uint32_t before = prev;
-    while (i0 < cnt && s_key[g][i0] == before) { before = s_key[g][i0]; ++i0; }
+  int64_t base = start;
+  int cnt = stage(base);
+  int i = 0;
+  if (start > 0) {  // skip the tail of a run that started in an earlier chunk
+    const uint32_t prev = fa.keys[start - 1];
+    while (i < cnt && s_key[g][i] == prev) ++i;
   }
-  if (i0 >= cnt) return;
-  uint32_t cur = s_key[g][i0];
+  if (i >= cnt) return;
+  uint32_t cur = s_key[g][i];
   if (cur == fa.sentinel) return;
-  int64_t run_start = start + i0;
+  int64_t run_start = base + i;
 
   V acc[NV];
 #pragma unroll
@@ -323,57 +330,45 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
     }
   };
 
-  constexpr int U = 4;
-  int i = i0;
-  bool done = false;
-  for (; i < cnt && !done; i += U) {
-    V r[U][NV];
+  // Runs starting in [start, limit) are ours; the last one is followed past
+  // `limit` batch by batch (a long run of a hot row keeps U rows in flight).
+  while (true) {
+    for (; i < cnt; i += U) {
+      V r[U][NV];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ii = i + u;
-      const bool live = ii < cnt && s_key[g][min(ii, cnt - 1)] != fa.sentinel;
-      const V* src = reinterpret_cast<const V*>(fa.grad + s_goff[g][min(ii, cnt - 1)]);
+      for (int u = 0; u < U; ++u) {
+        const int ii = i + u < cnt ? i + u : cnt - 1;
+        const bool live = (i + u < cnt) && s_key[g][ii] != fa.sentinel;
+        const V* src = reinterpret_cast<const V*>(fa.grad + s_goff[g][ii]);
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const int64_t c = lane + int64_t(v) * LPB;
-        r[u][v] = (live && c < nvec) ? ldg_vec(src + c) : vzero<V>();
+        for (int v = 0; v < NV; ++v) {
+          const int64_t c = lane + int64_t(v) * LPB;
+          r[u][v] = (live && c < nvec) ? ldg_vec(src + c) : vzero<V>();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int ii = i + u;
+        if (ii >= cnt) break;
+        const uint32_t k = s_key[g][ii];
+        if (k != cur) {
+          flush(cur, run_start);
+          if (k == fa.sentinel || base + ii >= limit) return;
+          cur = k;
+          run_start = base + ii;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
+        }
+        const float w = s_w[g][ii];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = vadd(acc[v], vmul(w, r[u][v]));  // fl(1*x)==x
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ii = i + u;
-      if (ii >= cnt || done) continue;
-      const uint32_t k = s_key[g][ii];
-      if (k != cur) {
-        flush(cur, run_start);
-        if (k == fa.sentinel) { done = true; continue; }
-        cur = k;
-        run_start = start + ii;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
-      }
-      const float w = s_w[g][ii];
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-        acc[v] = vadd(acc[v], vmul(w, r[u][v]));  // fl(1*x) == x
-    }
-  }
-  if (done) return;
-  // the last run may continue past the chunk: follow it sequentially
-  for (int64_t p = start + cnt; p < fa.n; ++p) {
-    const uint32_t k = fa.keys[p];
-    if (k != cur) break;
-    const int t = table_of_row(ts, k);
-    const uint32_t slot = fa.vals[p];
-    const int64_t goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
-    const float w = ts.t[t].weights ? __ldg(ts.t[t].weights + (slot - ts.cap_base[t])) : 1.f;
-    const V* src = reinterpret_cast<const V*>(fa.grad + goff);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int64_t c = lane + int64_t(v) * LPB;
-      const V x = c < nvec ? ldg_vec(src + c) : vzero<V>();
-      acc[v] = vadd(acc[v], vmul(w, x));
-    }
+    base += CH;
+    if (base >= fa.n) break;
+    if (fa.keys[base] != cur) break;  // our last run ends exactly here
+    cnt = stage(base);
+    i = 0;
   }
   flush(cur, run_start);
 }

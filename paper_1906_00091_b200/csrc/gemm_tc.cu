@@ -2,8 +2,10 @@
 //
 //   D[M x N] = sum_k A(m, k) * B(n, k)        (fp32 in, fp32 out)
 //
-// computed as 3xTF32: x = hi + lo with hi = x rounded to the nearest TF32
-// (cvt.rna.tf32.f32) and lo = x - hi (exact in fp32),
+// computed as 3xTF32: x = hi + lo with hi = x truncated to TF32 and lo =
+// x - hi (exact in fp32).  The tensor core itself ignores the low 13 mantissa
+// bits of a kind::tf32 operand, so the TMA-landed fp32 tile IS the hi operand
+// and only lo is materialised (by the splitter warps),
 // then D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.  Single
 // TF32 fails the reference tolerance on updated weights (SURVEY Appendix A:
 // 6e-2); 3xTF32 matches fp32 (1.6e-7 loss, 9e-7 weights).
@@ -16,13 +18,14 @@
 //   data grad    dX = gZ W       A = gZ (K-major)   B = W (MN-major)
 //   weight grad  dW = gZ^T X     A = gZ (MN-major)  B = X (MN-major)
 //
-// CTA = 6 warps, one 128 x BN output tile, 3-stage smem ring:
+// CTA = 6 warps, one 128 x BN output tile; a 4-stage TMA ring of raw tiles
+// and a 2-slot ring of lo tiles:
 //   warp 0     TMA producer (one thread)
 //   warp 1     TMEM allocator + MMA issuer (one thread)
-//   warps 2-5  hi/lo splitter for each landed stage, then the epilogue
+//   warps 2-5  lo splitter for each landed stage, then the epilogue
 //              (tcgen05.ld 32x32b -> bias/ReLU/mask -> global)
-// Barriers: full[s] (TMA tx), conv[s] (4 splitter warps), empty[s]
-// (tcgen05.commit), acc_full (tcgen05.commit after the last k-block).
+// Barriers: full[t] (TMA tx), empty_t[t] / empty_l[l] (tcgen05.commit),
+// conv[l] (4 splitter warps), acc_full (commit after the last k-block).
 #include <cuda.h>
 
 #include "gemm.cuh"
@@ -33,7 +36,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-constexpr int STAGES = 3;
+constexpr int TSTAGES = 4;  // TMA ring of raw fp32 tiles
+constexpr int LSTAGES = 2;  // ring of split-off lo tiles
 constexpr int THREADS = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -137,26 +141,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
-// x = hi + lo: hi = x rounded to nearest TF32 (|lo| <= 2^-12 |x|), lo exact.
-__device__ __forceinline__ float4 split_hi(float4 v, float4& lo) {
-  float4 h;
-  h.x = tf32_rna(v.x);
-  h.y = tf32_rna(v.y);
-  h.z = tf32_rna(v.z);
-  h.w = tf32_rna(v.w);
-  lo.x = v.x - h.x;
-  lo.y = v.y - h.y;
-  lo.z = v.z - h.z;
-  lo.w = v.w - h.w;
-  return h;
-}
-
 struct TcArgs {
   int64_t M, N, K;
   int k_tiles_per_split;
@@ -170,7 +154,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                TcArgs args) {
   constexpr uint32_t A_BYTES = BM * BK * 4;  // 16 KB
   constexpr uint32_t B_BYTES = BN * BK * 4;
-  constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;  // one TMA stage (= the hi operands)
+  constexpr uint32_t LO_BYTES = A_BYTES + B_BYTES;   // one lo slot
   // NBIG interleaved accumulators for hi*hi (k-block it -> it % NBIG) plus
   // one for the small cross terms; summed in fp32 in the epilogue.  The
   // tensor core's fp32 accumulation truncates, so its error grows with the
@@ -186,12 +171,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + STAGES;
-  uint64_t* empty = bars + 2 * STAGES;
-  uint64_t* acc_full = bars + 3 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  uint8_t* raw_ring = smem;                            // TSTAGES x RAW_BYTES
+  uint8_t* lo_ring = smem + TSTAGES * RAW_BYTES;       // LSTAGES x LO_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_ring + LSTAGES * LO_BYTES);
+  uint64_t* full = bars;                               // TMA landed      [T]
+  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, raw   [T]
+  uint64_t* conv = bars + 2 * TSTAGES;                 // lo ready        [L]
+  uint64_t* empty_l = bars + 2 * TSTAGES + LSTAGES;    // MMA done, lo    [L]
+  uint64_t* acc_full = bars + 2 * TSTAGES + 2 * LSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
@@ -200,10 +188,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const int nk = kt1 - kt0;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < TSTAGES; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&empty_t[s], 1);
+    }
+    for (int s = 0; s < LSTAGES; ++s) {
       mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty_l[s], 1);
     }
     mbar_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -223,13 +214,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
+    // ---- TMA producer: raw fp32 tiles (the tensor core reads them as the
+    // hi operand: kind::tf32 ignores the low 13 mantissa bits)
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
-        const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        uint8_t* st = smem + s * STAGE_BYTES;
+        const int s = it % TSTAGES;
+        if (it >= TSTAGES) mbar_wait(&empty_t[s], ((it / TSTAGES) - 1) & 1);
+        uint8_t* st = raw_ring + s * RAW_BYTES;
         const int k0 = (kt0 + it) * BK;
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        mbar_expect_tx(&full[s], RAW_BYTES);
         if (A_MN) {
 #pragma unroll
           for (int c = 0; c < BM / 32; ++c)
@@ -237,7 +230,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         } else {
           tma_load_2d(st, &tmA, &full[s], k0, int(m0));
         }
-        uint8_t* sb = st + 2 * A_BYTES;
+        uint8_t* sb = st + A_BYTES;
         if (B_MN) {
 #pragma unroll
           for (int c = 0; c < BN / 32; ++c)
@@ -250,15 +243,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
+    // ---- MMA issuer
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&conv[s], (it / STAGES) & 1);
+        const int t = it % TSTAGES, l = it % LSTAGES;
+        mbar_wait(&conv[l], (it / LSTAGES) & 1);
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t a_lo = a_hi + A_BYTES;
-        const uint32_t b_hi = a_hi + 2 * A_BYTES;
-        const uint32_t b_lo = b_hi + B_BYTES;
+        const uint32_t a_hi = smem_u32(raw_ring + t * RAW_BYTES);
+        const uint32_t b_hi = a_hi + A_BYTES;
+        const uint32_t a_lo = smem_u32(lo_ring + l * LO_BYTES);
+        const uint32_t b_lo = a_lo + A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
@@ -275,41 +269,39 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t small = tmem + uint32_t(NBIG * BN);
           const uint32_t acc_small = (it > 0 || kk > 0) ? 1u : 0u;
           const uint32_t acc_big = (it >= NBIG || kk > 0) ? 1u : 0u;
+#ifndef DLRM_EXP_ONE_MMA
           mma_tf32(small, dal, dbh, IDESC, acc_small);
           mma_tf32(small, dah, dbl, IDESC, 1u);
+#endif
           mma_tf32(big, dah, dbh, IDESC, acc_big);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&empty_t[t]);
+        mma_commit(&empty_l[l]);
       }
       mma_commit(acc_full);
     }
   } else {
-    // ---- splitter warps (2..5): hi/lo split of every landed stage
+    // ---- splitter warps (2..5): lo = x - trunc_tf32(x) for every landed tile
     const int ct = threadIdx.x - 64;  // 0..127
     for (int it = 0; it < nk; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      float4* ahi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
-      float4* alo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + A_BYTES);
-      float4* bhi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * A_BYTES);
-      float4* blo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * A_BYTES + B_BYTES);
+      const int t = it % TSTAGES, l = it % LSTAGES;
+      mbar_wait(&full[t], (it / TSTAGES) & 1);
+      if (it >= LSTAGES) mbar_wait(&empty_l[l], ((it / LSTAGES) - 1) & 1);
+      const float4* src = reinterpret_cast<const float4*>(raw_ring + t * RAW_BYTES);
+      float4* dst = reinterpret_cast<float4*>(lo_ring + l * LO_BYTES);
+#ifndef DLRM_EXP_NOSPLIT
 #pragma unroll 4
-      for (int i = ct; i < int(A_BYTES / 16); i += 128) {
-        float4 lo;
-        const float4 h = split_hi(ahi[i], lo);
-        ahi[i] = h;
-        alo[i] = lo;
+      for (int i = ct; i < int(RAW_BYTES / 16); i += 128) {
+        const float4 x = src[i];
+        dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                             x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
+                             x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
+                             x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
       }
-#pragma unroll 4
-      for (int i = ct; i < int(B_BYTES / 16); i += 128) {
-        float4 lo;
-        const float4 h = split_hi(bhi[i], lo);
-        bhi[i] = h;
-        blo[i] = lo;
-      }
+#endif
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
+      if (lane == 0) mbar_arrive(&conv[l]);
     }
     // ---- epilogue: TMEM lanes [32q, 32q+32) belong to warp with warp%4 == q
     mbar_wait(acc_full, 0);
@@ -319,14 +311,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const GemmEpilogue& ep = args.ep;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16], t[16];
+      float v[16], tt[16];
       const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(c0);
       tmem_ld16(lane_base + uint32_t(NBIG * BN), v);  // cross terms
       const int used = nk < NBIG ? nk : NBIG;
       for (int j = 0; j < used; ++j) {
-        tmem_ld16(lane_base + uint32_t(j * BN), t);
+        tmem_ld16(lane_base + uint32_t(j * BN), tt);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += t[i];
+        for (int i = 0; i < 16; ++i) v[i] += tt[i];
       }
       if (row < args.M) {
 #pragma unroll
@@ -367,7 +359,7 @@ bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 constexpr size_t smem_bytes(int bn) {
-  return size_t(STAGES) * (2 * BM * BK * 4 + 2 * bn * BK * 4) + 1024 + 256;
+  return size_t(TSTAGES + LSTAGES) * (BM * BK * 4 + bn * BK * 4) + 1024 + 256;
 }
 
 template <bool A_MN, bool B_MN, int BN>
