@@ -19,9 +19,13 @@ from .model import (DlrmCache, DlrmConfig, DlrmGradients, DlrmModel, MlpCache,
                     mlp_forward, mlp_param_count, param_count)
 from .optim import Sgd, make_optimizer, sgd_step, sgd_step_rows
 from .trainer import StepEngine, StepResult
-from .parallel import (CommLog, DevicePlan, ShuffleSlice, allreduce,
+from .parallel import (CommLog, DevicePlan, ParallelTrainer, ShuffleSlice,
+                       allreduce,
                        allreduce_max, butterfly_shuffle, format_comm_report,
                        inverse_shuffle, make_plan, partition_tables,
                        shard_bounds, train_step)
+
+from .distributed import (ExchangeLayout, HybridTrainer, LocalExchange,
+                          NcclExchange, RankEngine)
 
 __version__ = "0.1.0"

@@ -1,0 +1,451 @@
+"""Hybrid parallelism on one box: embedding tables model-parallel (whole table
+per GPU, the reference's ``partition_tables`` plan), bottom/top MLPs data-
+parallel over contiguous batch shards (``shard_bounds``), a personalized
+all-to-all of pooled embeddings forward and of their gradients backward, and
+an MLP-gradient allreduce overlapped with the rest of the backward pass.
+
+Reference: ``dlrmkit.parallel.ParallelTrainer.step`` (ref parallel.py:363-506)
+simulates exactly this in one process (butterfly_shuffle 146-176,
+inverse_shuffle 179-208, allreduce 211-224).  Here each rank is a process
+with its own GPU:
+
+    phase A  owner lookups over the GLOBAL batch -> sample-major send buffer
+             [B_g, T_own, d] (rows of each destination shard are contiguous)
+    a2a      all_to_all_single: rank r receives [src][b in shard r][T_own(src)][d]
+    phase B  local bottom MLP, interaction reading features straight out of
+             the receive buffer (per-feature pointer + stride), top MLP, loss
+             head (gradient / global batch), backward into a flat gradient
+             buffer; interaction backward writes feature gradients straight
+             into the backward send buffer (same layout as the receive one)
+    a2a      reverse all_to_all_single -> owner gets [B_g, T_own, d]
+    allreduce  top-MLP gradients start as soon as the top backward is done
+             (second communicator, overlaps interaction/bottom backward and
+             the reverse a2a); bottom-MLP gradients after the bottom backward
+    phase C  sorted sparse backward + SGD on owned tables; dense SGD on the
+             (identical) MLP replicas
+
+The exchange objects only move tensors, so they run unchanged over gloo on
+CPU (tests/test_distributed_cpu.py, world_size 2); the kernels need the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .embedding import LookupIndexError
+from .model import DlrmModel, ceil4
+from .parallel import DevicePlan, shard_bounds
+from .trainer import INT64_MAX, StepResult
+
+__all__ = ["ExchangeLayout", "NcclExchange", "LocalExchange", "RankEngine",
+           "HybridTrainer"]
+
+
+class ExchangeLayout:
+    """Split sizes and feature addresses of the pooled-embedding exchange for
+    one rank (pure index arithmetic — bit-exact with the reference plan)."""
+
+    def __init__(self, plan: DevicePlan, rank: int, dim: int):
+        plan.validate()
+        self.plan, self.rank, self.d = plan, rank, dim
+        G = plan.num_devices
+        self.owned = [plan.owned(r) for r in range(G)]
+        self.lo, self.hi = plan.shard(rank)
+        self.B_local = self.hi - self.lo
+        self.B_global = plan.batch_size
+        T_me = len(self.owned[rank])
+        self.T_own = T_me
+        # forward: send rows [lo_r, hi_r) of my [B_g, T_me, d] buffer to r
+        self.send_split = [(plan.shard(r)[1] - plan.shard(r)[0]) * T_me * dim
+                           for r in range(G)]
+        # forward: receive my shard of every source's owned tables
+        self.recv_split = [self.B_local * len(self.owned[s]) * dim
+                           for s in range(G)]
+        self.recv_off = np.concatenate([[0], np.cumsum(self.recv_split)]).astype(np.int64)
+        # table t -> (element offset in the receive buffer, row stride)
+        self.feature = {}
+        for s in range(G):
+            Ts = len(self.owned[s])
+            for j, t in enumerate(self.owned[s]):
+                self.feature[t] = (int(self.recv_off[s]) + j * dim, Ts * dim)
+
+    @property
+    def send_numel(self) -> int:
+        return self.B_global * self.T_own * self.d
+
+    @property
+    def recv_numel(self) -> int:
+        return int(self.recv_off[-1])
+
+
+class NcclExchange:
+    """torch.distributed transport (NCCL on GPUs, gloo on CPU): the forward
+    and reverse all-to-all on one communicator, gradient allreduces on a
+    second one so they overlap the reverse all-to-all."""
+
+    def __init__(self, layout: ExchangeLayout, group=None, ar_group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.L = layout
+        self.group = group
+        self.ar_group = ar_group if ar_group is not None else group
+
+    def forward(self, send: torch.Tensor, recv: torch.Tensor):
+        self.dist.all_to_all_single(recv, send, self.L.recv_split,
+                                    self.L.send_split, group=self.group)
+
+    def backward(self, gsend: torch.Tensor, grecv: torch.Tensor):
+        self.dist.all_to_all_single(grecv, gsend, self.L.send_split,
+                                    self.L.recv_split, group=self.group)
+
+    def allreduce_async(self, t: torch.Tensor):
+        return self.dist.all_reduce(t, group=self.ar_group, async_op=True)
+
+    def allreduce(self, t: torch.Tensor):
+        self.dist.all_reduce(t, group=self.ar_group)
+
+
+class LocalExchange:
+    """In-process transport for G virtual ranks on one device (the
+    reference's simulator semantics; used by ParallelTrainer)."""
+
+    def __init__(self, layouts):
+        self.layouts = layouts
+
+    def forward_all(self, sends, recvs):
+        G = len(self.layouts)
+        for dst in range(G):
+            off = 0
+            for src in range(G):
+                Ls = self.layouts[src]
+                so = int(np.sum(Ls.send_split[:dst]))
+                n = Ls.send_split[dst]
+                recvs[dst][off:off + n].copy_(sends[src][so:so + n])
+                off += n
+
+    def backward_all(self, gsends, grecvs):
+        G = len(self.layouts)
+        for owner in range(G):
+            Lo = self.layouts[owner]
+            off = 0
+            for src in range(G):
+                Lsrc = self.layouts[src]
+                n = Lo.send_split[src]
+                so = int(Lsrc.recv_off[owner])
+                grecvs[owner][off:off + n].copy_(gsends[src][so:so + n])
+                off += n
+
+    @staticmethod
+    def allreduce_all(tensors):
+        acc = tensors[0].clone()
+        for t in tensors[1:]:
+            acc += t
+        for t in tensors:
+            t.copy_(acc)
+
+
+class RankEngine:
+    """One rank's buffers and kernel sequence for the hybrid step.
+
+    The model's MLP parameters are re-homed into a flat buffer (``params``)
+    with a same-layout gradient buffer (``grads``); the rank's owned tables
+    into one buffer ``W_own``.  Tables not owned by this rank are left alone.
+    """
+
+    def __init__(self, model: DlrmModel, layout: ExchangeLayout,
+                 capacities=None, lr: float = 0.1):
+        _lib.require_cuda()
+        cfg = model.config
+        self.model, self.cfg, self.L = model, cfg, layout
+        self.lr = float(lr)
+        d = self.d = cfg.sparse_dim
+        self.T = cfg.num_tables
+        self.nf = self.T + 1
+        Bl, Bg = self.Bl, self.Bg = layout.B_local, layout.B_global
+        dev = self.dev = _lib.device()
+        f32 = dict(dtype=torch.float32, device=dev)
+
+        # parameters + gradients (flat, identical layout)
+        self.layers = model.bottom.layers + model.top.layers
+        self.Lb, self.Lt = len(model.bottom.layers), len(model.top.layers)
+        n = sum(l.n_out * ceil4(l.n_in) + ceil4(l.n_out) for l in self.layers)
+        self.params = torch.zeros(n, **f32)
+        self.grads = torch.zeros(n, **f32)
+        self.gslots = []
+        off = 0
+        for l in self.layers:
+            nw = l.n_out * ceil4(l.n_in)
+            w = self.params[off:off + nw].view(l.n_out, ceil4(l.n_in))
+            gw = self.grads[off:off + nw].view(l.n_out, ceil4(l.n_in))
+            off += nw
+            b = self.params[off:off + l.n_out]
+            gb = self.grads[off:off + l.n_out]
+            off += ceil4(l.n_out)
+            l.rebind(w, b)
+            self.gslots.append((gw, gb))
+        self.split_at = sum(l.n_out * ceil4(l.n_in) + ceil4(l.n_out)
+                            for l in self.layers[:self.Lb])   # bottom | top
+
+        # owned tables in one buffer
+        own = layout.owned[layout.rank]
+        self.own = own
+        rows = [model.tables[t].num_rows for t in own]
+        self.row_base = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+        self.total_rows = int(self.row_base[-1])
+        self.W_own = torch.empty(max(self.total_rows, 1) * d, **f32)
+        for j, t in enumerate(own):
+            v = self.W_own[self.row_base[j] * d:self.row_base[j + 1] * d].view(rows[j], d)
+            v.copy_(model.tables[t].weights)
+            model.tables[t].weights = v
+        To = len(own)
+        caps = capacities if capacities is not None else [Bg] * To
+        self.caps = [max(1, int(c)) for c in caps]
+        self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
+
+        # inputs
+        self.x = torch.zeros((Bl, ceil4(cfg.dense_dim)), **f32)
+        self.labels = torch.zeros(Bl, **f32)
+        self.offsets = torch.zeros((max(To, 1), Bg + 1), dtype=torch.int64, device=dev)
+        self.indices = torch.zeros(max(int(self.cap_base[-1]), 1), dtype=torch.int64, device=dev)
+
+        # exchange buffers
+        self.send = torch.zeros(max(layout.send_numel, 1), **f32)
+        self.recv = torch.zeros(max(layout.recv_numel, 1), **f32)
+        self.gsend = torch.zeros(max(layout.recv_numel, 1), **f32)
+        self.grecv = torch.zeros(max(layout.send_numel, 1), **f32)
+
+        # activations / gradients
+        bl, tl = model.bottom.layers, model.top.layers
+        self.bact = [torch.zeros((Bl, ceil4(l.n_out)), **f32) for l in bl]
+        self.width = cfg.top_in_dim
+        self.R = torch.zeros((Bl, ceil4(self.width)), **f32)
+        self.tact = [torch.zeros((Bl, ceil4(l.n_out)), **f32) for l in tl[:-1]]
+        self.prob = torch.zeros(Bl, **f32)
+        self.glogit = torch.zeros(Bl, **f32)
+        self.gtop = [torch.zeros((Bl, ceil4(l.n_out)), **f32) for l in tl[:-1]]
+        self.gR = torch.zeros((Bl, ceil4(self.width)), **f32)
+        self.gbot = [torch.zeros((Bl, ceil4(l.n_out)), **f32) for l in bl]
+
+        # workspaces, step result [loss_sum, correct, err]
+        self.emb_ws_bytes = _lib.size("dlrm_emb_bwd_workspace_size",
+                                      max(int(self.cap_base[-1]), 1),
+                                      max(self.total_rows, 1))
+        self.emb_ws = torch.empty(self.emb_ws_bytes, dtype=torch.uint8, device=dev)
+        lin = max(_lib.size("dlrm_linear_bwd_weight_workspace_size", Bl,
+                            l.n_out, l.n_in) for l in self.layers)
+        lin = max(lin, _lib.size("dlrm_head_bwd_workspace_size", Bl, tl[-1].n_in),
+                  _lib.size("dlrm_bce_head_workspace_size", Bl))
+        self.lin_ws_bytes = lin
+        self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
+        self.stats = torch.zeros(3, **f32)
+        self.err_pos = torch.empty(max(To, 1), dtype=torch.int64, device=dev)
+        self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._build_descs()
+
+    def _build_descs(self):
+        d, L = self.d, self.L
+        To = len(self.own)
+        descs = [_lib.TableDesc(
+            self.offsets[j].data_ptr(), self.indices.data_ptr() + 8 * int(self.cap_base[j]),
+            None, int(self.row_base[j]), self.model.tables[t].num_rows, j * d,
+            self.caps[j], self.model.tables[t].table_id) for j, t in enumerate(self.own)]
+        self._descs = _lib.table_array(descs) if descs else None
+        feats = [(self.bact[-1].data_ptr(), self.bact[-1].stride(0))]
+        gfeats = [(self.gbot[-1].data_ptr(), self.gbot[-1].stride(0))]
+        for t in range(self.T):
+            off, stride = L.feature[t]
+            feats.append((self.recv.data_ptr() + 4 * off, stride))
+            gfeats.append((self.gsend.data_ptr() + 4 * off, stride))
+        self._feats = _lib.make_features(feats)
+        self._gfeat = (C.c_void_p * self.nf)(*[p for p, _ in gfeats])
+        self._gstride = (C.c_int64 * self.nf)(*[s for _, s in gfeats])
+
+    # ------------------------------------------------------------------
+    def load(self, dense_local, labels_local, offsets_owned, indices_owned):
+        """dense/labels: this rank's shard; offsets/indices: one global-batch
+        bag set per OWNED table (host arrays or device tensors)."""
+        from .trainer import _to_dev, _to_dev_f32
+        self.x[:, :self.cfg.dense_dim].copy_(_to_dev_f32(dense_local, self.dev))
+        self.labels.copy_(_to_dev_f32(labels_local, self.dev))
+        for j in range(len(self.own)):
+            i = indices_owned[j]
+            n = int(i.shape[0])
+            if n > self.caps[j]:
+                raise OverflowError(f"table {self.own[j]}: {n} indices exceed "
+                                    f"capacity {self.caps[j]}")
+            self.offsets[j].copy_(_to_dev(offsets_owned[j], torch.int64, self.dev))
+            cb = int(self.cap_base[j])
+            self.indices[cb:cb + n].copy_(_to_dev(i, torch.int64, self.dev))
+        self._host_indices = indices_owned
+
+    # ------------------------------------------------------------------
+    def phase_a(self, stream=None):
+        """Error reset + owner lookups over the global batch -> send buffer."""
+        s = _lib.stream_handle(stream)
+        P = _lib.ptr
+        To = len(self.own)
+        _lib.call("dlrm_err_reset", P(self.err_pos), max(To, 1), P(self.err_flag), s)
+        if To:
+            _lib.call("dlrm_emb_fwd", P(self.W_own), self.d,
+                      C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.send),
+                      To * self.d, P(self.err_pos), P(self.err_flag), s)
+
+    def phase_b_forward(self, stream=None):
+        s = _lib.stream_handle(stream)
+        P, call, L = _lib.ptr, _lib.call, self.layers
+        Bl, relu = self.Bl, _lib.ACT["relu"]
+        a, lda = self.x, self.x.stride(0)
+        for i in range(self.Lb):
+            l, out = L[i], self.bact[i]
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
+            a, lda = out, out.stride(0)
+        call("dlrm_interact_fwd", C.c_void_p(C.addressof(self._feats)), self.nf,
+             self.d, Bl, P(self.R), self.R.stride(0), self.R.shape[1], s)
+        a, lda = self.R, self.R.stride(0)
+        for i in range(self.Lt - 1):
+            l, out = L[self.Lb + i], self.tact[i]
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
+            a, lda = out, out.stride(0)
+        head = L[-1]
+        call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), Bl,
+             head.n_in, P(self.labels), float(self.Bg), None, P(self.prob),
+             P(self.glogit), None, P(self.stats), P(self.lin_ws),
+             self.lin_ws_bytes, s)
+        self._head_in = (a, lda)
+
+    def phase_b_top_backward(self, stream=None):
+        s = _lib.stream_handle(stream)
+        P, call, L = _lib.ptr, _lib.call, self.layers
+        Bl = self.Bl
+        a, lda = self._head_in
+        head = L[-1]
+        gw, gb = self.gslots[-1]
+        ga = self.gtop[-1] if self.Lt > 1 else self.gR
+        call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), Bl,
+             head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw),
+             P(gb), None, None, 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+        for i in range(self.Lt - 2, -1, -1):
+            li = self.Lb + i
+            l = L[li]
+            gz = self.gtop[i]
+            xin = self.R if i == 0 else self.tact[i - 1]
+            dx = self.gR if i == 0 else self.gtop[i - 1]
+            mask = None if i == 0 else self.tact[i - 1]
+            call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage), l.ldw,
+                 P(mask), mask.stride(0) if mask is not None else 0, P(dx),
+                 dx.stride(0), Bl, l.n_out, l.n_in, s)
+            gw, gb = self.gslots[li]
+            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
+                 Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+
+    def phase_b_interaction_backward(self, stream=None):
+        s = _lib.stream_handle(stream)
+        _lib.call("dlrm_interact_bwd", C.c_void_p(C.addressof(self._feats)),
+                  self.nf, self.d, self.Bl, _lib.ptr(self.gR), self.gR.stride(0),
+                  C.cast(self._gfeat, C.c_void_p), C.cast(self._gstride, C.c_void_p),
+                  1, s)
+
+    def phase_b_bottom_backward(self, stream=None):
+        s = _lib.stream_handle(stream)
+        P, call, L = _lib.ptr, _lib.call, self.layers
+        Bl = self.Bl
+        for i in range(self.Lb - 1, -1, -1):
+            l = L[i]
+            gz = self.gbot[i]
+            xin = self.x if i == 0 else self.bact[i - 1]
+            if i > 0:
+                dx = self.gbot[i - 1]
+                call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
+                     l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
+                     dx.stride(0), Bl, l.n_out, l.n_in, s)
+            gw, gb = self.gslots[i]
+            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
+                 Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+
+    def publish_error(self):
+        """stats[2] <- this rank's error flag (allreduced with the loss)."""
+        self.stats[2].copy_(self.err_flag[0].to(torch.float32))
+
+    def adopt_global_error(self):
+        """err_flag <- any rank raised (after the stats allreduce)."""
+        self.err_flag.copy_((self.stats[2:3] > 0).to(torch.int32))
+
+    def phase_c(self, stream=None):
+        s = _lib.stream_handle(stream)
+        P = _lib.ptr
+        To = len(self.own)
+        if To:
+            _lib.call("dlrm_emb_bwd_sgd", P(self.W_own), self.d,
+                      C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.grecv),
+                      To * self.d, self.lr, P(self.err_flag), self.total_rows,
+                      P(self.emb_ws), self.emb_ws_bytes, s)
+        _lib.call("dlrm_sgd_dense", P(self.params), P(self.grads),
+                  self.params.numel(), self.lr, P(self.err_flag), s)
+
+    def local_error(self):
+        """(table_id, position, index, rows) of this rank's first bad index."""
+        if not int(self.err_flag.item()):
+            return None
+        pos = self.err_pos.cpu().numpy()
+        for j, t in enumerate(self.own):
+            if pos[j] != INT64_MAX:
+                k = int(pos[j])
+                idx = self._host_indices[j]
+                val = int(idx[k].item() if isinstance(idx, torch.Tensor) else idx[k])
+                tab = self.model.tables[t]
+                return tab.table_id, k, val, tab.num_rows
+        return None
+
+
+class HybridTrainer:
+    """One process per GPU: ``torchrun --nproc-per-node G``.  All ranks build
+    the same model (same seed) and the same plan; rank r keeps the tables the
+    plan assigns to it and an MLP replica."""
+
+    def __init__(self, model: DlrmModel, plan: DevicePlan, rank: int,
+                 capacities=None, lr: float = 0.1, group=None, ar_group=None):
+        self.layout = ExchangeLayout(plan, rank, model.config.sparse_dim)
+        self.engine = RankEngine(model, self.layout, capacities, lr)
+        self.ex = NcclExchange(self.layout, group, ar_group)
+        self.rank = rank
+        self.comm_stream = torch.cuda.Stream()
+
+    def load(self, *args):
+        self.engine.load(*args)
+
+    def step(self) -> StepResult:
+        e, ex = self.engine, self.ex
+        cur = torch.cuda.current_stream()
+        e.phase_a()
+        ex.forward(e.send, e.recv)
+        e.phase_b_forward()
+        e.phase_b_top_backward()
+        # top-MLP gradients reduce on the second communicator while the
+        # interaction / bottom backward and the reverse exchange run
+        top = e.grads[e.split_at:]
+        h_top = ex.allreduce_async(top)
+        e.phase_b_interaction_backward()
+        ex.backward(e.gsend, e.grecv)
+        e.phase_b_bottom_backward()
+        h_bot = ex.allreduce_async(e.grads[:e.split_at])
+        e.publish_error()
+        ex.allreduce(e.stats)
+        e.adopt_global_error()
+        h_top.wait()
+        h_bot.wait()
+        e.phase_c()
+        if float(e.stats[2].item()) > 0:
+            err = e.local_error()
+            if err is not None:
+                raise LookupIndexError(*err)
+            raise RuntimeError("a peer rank reported an out-of-range index")
+        st = e.stats.cpu()
+        return StepResult(float(st[0]) / e.Bg, float(st[1]) / e.Bg, e.prob.clone())

@@ -25,6 +25,7 @@ __all__ = [
     "DevicePlan", "ShuffleSlice", "CommLog", "StepResult", "partition_tables",
     "shard_bounds", "make_plan", "butterfly_shuffle", "inverse_shuffle",
     "allreduce", "allreduce_max", "train_step", "format_comm_report",
+    "ParallelTrainer",
 ]
 
 
@@ -247,3 +248,106 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
     if timer is not None and hasattr(timer, "seconds"):
         timer.seconds.setdefault("train_step", 0.0)
     return eng.result()
+
+
+# --------------------------------------------------------------------------
+# in-process hybrid-parallel simulator  (ref parallel.py:310-525)
+
+class ParallelTrainer:
+    """Replicated-MLP, partitioned-table trainer over ``plan.num_devices``
+    virtual devices on the current GPU — the reference's simulator API, run
+    through the same per-rank kernel sequence (``distributed.RankEngine``)
+    as the multi-process ``HybridTrainer``, with the exchanges done as
+    device copies.  Dense gradients are summed in ascending replica order.
+
+    Unlike the reference (float64 grid reductions) the fp32 sum over shards
+    is not partition-invariant, so results match serial training within
+    tolerance, not bit for bit (SURVEY §7 hard part 6)."""
+
+    def __init__(self, model: DlrmModel, plan: DevicePlan,
+                 optimizer_name: str = "sgd", lr: float = 0.1,
+                 eps: float = 1e-10, concurrent: bool = False,
+                 capacities=None):
+        from .distributed import ExchangeLayout, LocalExchange, RankEngine
+        if optimizer_name != "sgd":
+            raise NotImplementedError("the fused step implements SGD only")
+        plan.validate()
+        if len(plan.table_assignment) != model.config.num_tables:
+            raise ValueError("plan does not cover the model's tables")
+        self.plan, self.config = plan, model.config
+        self.tables = list(model.tables)
+        G = plan.num_devices
+        self.layouts = [ExchangeLayout(plan, r, model.config.sparse_dim)
+                        for r in range(G)]
+        self.engines = []
+        for r in range(G):
+            replica = DlrmModel(model.config, model.bottom.copy(),
+                                model.top.copy(), self.tables)
+            own = self.layouts[r].owned[r]
+            caps = None if capacities is None else [capacities[t] for t in own]
+            self.engines.append(RankEngine(replica, self.layouts[r], caps, lr))
+        self.ex = LocalExchange(self.layouts)
+        self.comm = CommLog()
+        self.step_count = 0
+        self.concurrent = concurrent
+
+    def close(self):
+        pass
+
+    def replica_params(self, device: int = 0):
+        m = self.engines[device].model
+        return m.bottom, m.top
+
+    def max_replica_divergence(self) -> float:
+        p0 = self.engines[0].params
+        return max([float((e.params - p0).abs().max()) for e in self.engines[1:]],
+                   default=0.0)
+
+    def step(self, dense_x, batches, labels, timer=None) -> StepResult:
+        plan = self.plan
+        n_total = int(dense_x.shape[0])
+        if n_total != plan.batch_size:
+            raise ValueError(f"batch size {n_total} does not match plan "
+                             f"({plan.batch_size})")
+        G, step = plan.num_devices, self.step_count
+        for r, e in enumerate(self.engines):
+            lo, hi = plan.shard(r)
+            own = self.layouts[r].owned[r]
+            e.load(dense_x[lo:hi], labels[lo:hi],
+                   [batches[t].offsets for t in own],
+                   [batches[t].indices for t in own])
+        for e in self.engines:
+            e.phase_a()
+        self.ex.forward_all([e.send for e in self.engines],
+                            [e.recv for e in self.engines])
+        moved = sum(4 * n for r, L in enumerate(self.layouts)
+                    for dst, n in enumerate(L.send_split) if dst != r)
+        self.comm.add(step, "butterfly_shuffle", moved, G)
+        for e in self.engines:
+            e.phase_b_forward()
+            e.phase_b_top_backward()
+            e.phase_b_interaction_backward()
+        self.ex.backward_all([e.gsend for e in self.engines],
+                             [e.grecv for e in self.engines])
+        self.comm.add(step, "grad_reverse_shuffle", moved, G)
+        for e in self.engines:
+            e.phase_b_bottom_backward()
+            e.publish_error()
+        self.ex.allreduce_all([e.stats for e in self.engines])
+        self.comm.add(step, "loss_gather", 12 * (G - 1), G)
+        self.ex.allreduce_all([e.grads for e in self.engines])
+        self.comm.add(step, "grad_allreduce",
+                      2 * (G - 1) * 4 * self.engines[0].grads.numel(), G)
+        for e in self.engines:
+            e.adopt_global_error()
+            e.phase_c()
+        if float(self.engines[0].stats[2].item()) > 0:
+            for r, e in enumerate(self.engines):
+                err = e.local_error()
+                if err is not None:
+                    from .embedding import LookupIndexError
+                    raise RuntimeError(f"device {r}: {LookupIndexError(*err)}")
+        self.step_count += 1
+        st = self.engines[0].stats.cpu()
+        probs = torch.cat([e.prob for e in self.engines])
+        return StepResult(float(st[0]) / n_total, float(st[1]) / n_total, probs)
