@@ -342,8 +342,31 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
 int g_tc_mode = 0;  // 0: use tcgen05 where the shape allows; 1: never
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library does not link libcuda (it must dlopen on GPU-less build hosts).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
 bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
             int64_t ld_elems, int box_inner, int box_outer, CUtensorMapSwizzle swz) {
+  EncodeTiledFn cuTensorMapEncodeTiled = encode_fn();
+  if (!cuTensorMapEncodeTiled) return false;
   cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
   cuuint64_t strides[1] = {cuuint64_t(ld_elems) * 4};
   cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
