@@ -36,9 +36,14 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-constexpr int TSTAGES = 4;  // TMA ring of raw fp32 tiles
-constexpr int LSTAGES = 2;  // ring of split-off lo tiles
-constexpr int THREADS = 192;
+#ifndef DLRM_EXP_TSTAGES
+#define DLRM_EXP_TSTAGES 4
+#define DLRM_EXP_LSTAGES 2
+#endif
+constexpr int TSTAGES = DLRM_EXP_TSTAGES;  // TMA ring of raw fp32 tiles
+constexpr int LSTAGES = DLRM_EXP_LSTAGES;  // ring of split-off lo tiles
+constexpr int SPLIT_WARPS = 8;  // splitter + epilogue warps (2 per TMEM lane quarter)
+constexpr int THREADS = 64 + 32 * SPLIT_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -193,7 +198,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&empty_t[s], 1);
     }
     for (int s = 0; s < LSTAGES; ++s) {
-      mbar_init(&conv[s], 4);
+      mbar_init(&conv[s], SPLIT_WARPS);
       mbar_init(&empty_l[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -247,12 +252,24 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
         const int t = it % TSTAGES, l = it % LSTAGES;
+#ifdef DLRM_EXP_PURE
+        mbar_wait(&full[t], (it / TSTAGES) & 1);
+#else
         mbar_wait(&conv[l], (it / LSTAGES) & 1);
+#endif
         tc_fence_after();
         const uint32_t a_hi = smem_u32(raw_ring + t * RAW_BYTES);
         const uint32_t b_hi = a_hi + A_BYTES;
+#ifdef DLRM_EXP_PURE
+        const uint32_t a_lo = a_hi;
+#else
         const uint32_t a_lo = smem_u32(lo_ring + l * LO_BYTES);
+#endif
         const uint32_t b_lo = a_lo + A_BYTES;
+#ifdef DLRM_EXP_TMAONLY
+        mbar_arrive(&empty_t[t]);
+        continue;
+#endif
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
@@ -276,14 +293,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           mma_tf32(big, dah, dbh, IDESC, acc_big);
         }
         mma_commit(&empty_t[t]);
+#ifndef DLRM_EXP_PURE
         mma_commit(&empty_l[l]);
+#endif
       }
       mma_commit(acc_full);
     }
   } else {
     // ---- splitter warps (2..5): lo = x - trunc_tf32(x) for every landed tile
-    const int ct = threadIdx.x - 64;  // 0..127
+    const int ct = threadIdx.x - 64;  // 0 .. 32*SPLIT_WARPS-1
+#ifdef DLRM_EXP_PURE
+    for (int it = 0; it < 0; ++it) {
+#else
     for (int it = 0; it < nk; ++it) {
+#endif
       const int t = it % TSTAGES, l = it % LSTAGES;
       mbar_wait(&full[t], (it / TSTAGES) & 1);
       if (it >= LSTAGES) mbar_wait(&empty_l[l], ((it / LSTAGES) - 1) & 1);
@@ -291,7 +314,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       float4* dst = reinterpret_cast<float4*>(lo_ring + l * LO_BYTES);
 #ifndef DLRM_EXP_NOSPLIT
 #pragma unroll 4
-      for (int i = ct; i < int(RAW_BYTES / 16); i += 128) {
+      for (int i = ct; i < int(RAW_BYTES / 16); i += 32 * SPLIT_WARPS) {
         const float4 x = src[i];
         dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
                              x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
@@ -303,28 +326,38 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[l]);
     }
-    // ---- epilogue: TMEM lanes [32q, 32q+32) belong to warp with warp%4 == q
+    // ---- epilogue: TMEM lanes [32q, 32q+32) are readable by warps with
+    // warp%4 == q; the two warps of a quarter take half of the columns each.
+    // Each 32x16 block goes registers -> smem (transpose) -> coalesced
+    // row-segment stores (lane = column).
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int q = warp & 3;
-    const int64_t row = m0 + 32 * q + lane;
+    const int half = (warp - 2) / 4;
+    float* tile = reinterpret_cast<float*>(lo_ring) + (warp - 2) * (32 * 17);
     const GemmEpilogue& ep = args.ep;
+    const int used = nk < NBIG ? nk : NBIG;
+    constexpr int CW = BN / 2 < 16 ? 16 : BN / 2;  // columns per warp
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = half * CW; c0 < BN && c0 < (half + 1) * CW; c0 += 16) {
       float v[16], tt[16];
       const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(c0);
       tmem_ld16(lane_base + uint32_t(NBIG * BN), v);  // cross terms
-      const int used = nk < NBIG ? nk : NBIG;
       for (int j = 0; j < used; ++j) {
         tmem_ld16(lane_base + uint32_t(j * BN), tt);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] += tt[i];
       }
-      if (row < args.M) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          apply_epilogue(ep, row, n0 + c0 + j, args.N, v[j], blockIdx.z);
+      for (int i = 0; i < 16; ++i) tile[lane * 17 + i] = v[i];
+      __syncwarp();
+      const int c = lane & 15;
+#pragma unroll 4
+      for (int r = lane >> 4; r < 32; r += 2) {
+        const int64_t row = m0 + 32 * q + r;
+        if (row < args.M) apply_epilogue(ep, row, n0 + c0 + c, args.N, tile[r * 17 + c], blockIdx.z);
       }
+      __syncwarp();
     }
   }
   tc_fence_before();
@@ -400,16 +433,45 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   return check_launch("tc_gemm_kernel");
 }
 
-// Pick the N tile: the largest of {128, 64, 32, 16} that still gives >= ~100
-// CTAs (148 SMs, one CTA each), else 16.
-int pick_bn(int64_t M, int64_t n_grid) {
+// Tile planner: pick the N tile (and, where a workspace exists, the split-K
+// factor) minimising a simple time model fitted on B200 measurements of this
+// kernel: per CTA  F + k_iters * (C0 + C1 * BN)  cycles, waves of 148 CTAs,
+// plus the partial-sum reduction when split.
+struct TcPlan {
+  int bn;
+  int splits;
+};
+
+TcPlan plan_tc(int64_t M, int64_t n_grid, int64_t kt, bool allow_split, int min_bn,
+               int64_t out_elems) {
+  constexpr double F = 9000, C0 = 600, C1 = 7.5;
+  TcPlan best{128, 1};
+  double best_t = 1e30;
   const int64_t mt = ceil_div(M, BM);
-  for (int bn : {128, 64, 32}) {
-    if (n_grid >= bn && mt * ceil_div(n_grid, bn) >= 100) return bn;
+  for (int bn : {128, 64, 32, 16}) {
+    if (bn < min_bn) continue;
+    if (bn > 16 && n_grid <= bn / 2) continue;  // mostly empty tile
+    const int64_t tiles = mt * ceil_div(n_grid, bn);
+    int64_t smax = allow_split ? (tiles < kNumSMs ? kNumSMs / tiles : 1) : 1;
+    if (smax > kt / 4) smax = kt / 4;
+    if (smax > 16) smax = 16;
+    if (smax < 1) smax = 1;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int64_t ctas = tiles * sp;
+      const double waves = double(ceil_div(ctas, kNumSMs));
+      double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn));
+      if (sp > 1) t += 2000.0 + 0.002 * double(sp + 1) * double(out_elems);
+      if (t < best_t) {
+        best_t = t;
+        best = TcPlan{bn, int(sp)};
+      }
+    }
   }
-  if (n_grid > 64) return 32;
-  if (n_grid > 32) return 64 <= n_grid ? 64 : 32;
-  return n_grid > 16 ? 32 : 16;
+  return best;
+}
+
+int pick_bn(int64_t M, int64_t n_grid) {
+  return plan_tc(M, n_grid, 8, false, 16, 0).bn;
 }
 
 template <bool A_MN, bool B_MN>
@@ -448,7 +510,7 @@ bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw, 
 int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* b,
                   float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
                   int act, cudaStream_t s) {
-  const int bn = pick_bn(M, n_grid);
+  const int bn = plan_tc(M, n_grid, ceil_div(K, BK), false, 16, 0).bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
                    map_operand(&mb, W, false, N, K, ldw, bn),
@@ -463,7 +525,7 @@ bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t
                            const float* dX, int64_t ldx, int64_t M, int64_t N, int64_t K) {
   (void)dX;
   (void)ldx;
-  return tc_enabled() && M >= 1 && K >= 32 && N >= 1 && aligned16(gZ) && aligned16(W) &&
+  return tc_enabled() && M >= 1 && K >= 1 && N >= 1 && aligned16(gZ) && aligned16(W) &&
          ldg % 4 == 0 && ldw % 4 == 0;
 }
 
@@ -471,8 +533,7 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
                        const float* mask, int64_t ldm, float* dX, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, cudaStream_t s) {
   // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
-  int bn = pick_bn(M, K);
-  if (bn < 32) bn = 32;
+  const int bn = plan_tc(M, K, ceil_div(N, BK), false, 32, 0).bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
                    map_operand(&mb, W, true, K, N, ldw, bn),
@@ -485,25 +546,21 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
                              int64_t M, int64_t N, int64_t K) {
-  return tc_enabled() && M >= 32 && N >= 32 && K >= 32 && aligned16(gZ) && aligned16(X) &&
+  // K < 32: one mostly-empty 32-wide MN-major box per k-step; the SIMT
+  // kernel is faster there (measured 41 vs 68 us at 2048 x 512 x 13)
+  return tc_enabled() && M >= 1 && N >= 1 && K >= 32 && aligned16(gZ) && aligned16(X) &&
          ldg % 4 == 0 && ldx % 4 == 0;
 }
 
 namespace {
-int weight_splits(int64_t M, int64_t N, int64_t K, int bn) {
-  const int64_t tiles = ceil_div(N, BM) * ceil_div(K, bn);
-  const int64_t kt = ceil_div(M, BK);
-  int64_t s = ceil_div(2 * kNumSMs, tiles);
-  if (s > kt / 4) s = kt / 4;
-  if (s > 16) s = 16;
-  return int(s < 1 ? 1 : s);
+TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
+  return plan_tc(N, K, ceil_div(M, BK), true, 32, N * K);
 }
 }  // namespace
 
 size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K) {
-  const int bn = pick_bn(N, K);
-  const int sp = weight_splits(M, N, K, bn);
-  return size_t(sp) * N * K + size_t(ceil_div(M, 256) + 1) * N;
+  const TcPlan p = weight_plan(M, N, K);
+  return size_t(p.splits) * N * K + size_t(ceil_div(M, 256) + 1) * N;
 }
 
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
@@ -511,8 +568,8 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
                          int64_t ldw, float lr, const int32_t* err_flag, float* ws,
                          cudaStream_t s) {
   // dW (N x K) = gZ^T X: GEMM m = N (MN-major in gZ), n = K (MN-major in X), k = M
-  const int bn = pick_bn(N, K) < 32 ? 32 : pick_bn(N, K);
-  const int sp = weight_splits(M, N, K, bn);
+  const TcPlan pl = weight_plan(M, N, K);
+  const int bn = pl.bn, sp = pl.splits;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
                    map_operand(&mb, X, true, K, M, ldx, bn),

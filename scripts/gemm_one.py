@@ -2,7 +2,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1906_00091_b200 import _lib
-B, K, N = 2048, 1024, 1024
+B, K, N = 2048, int(os.environ.get("K", 1024)), 1024
 X = torch.randn((B, K), device="cuda"); W = torch.randn((N, K), device="cuda")
 b = torch.zeros(N, device="cuda"); Y = torch.empty((B, N), device="cuda")
 s = _lib.stream_handle()

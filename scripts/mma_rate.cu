@@ -1,0 +1,69 @@
+// Microbenchmark: issue rate of tcgen05.mma kind::tf32 / kind::f16 from smem.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t addr) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(64) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+template <int KIND, int N>
+__global__ void mma_loop(int iters, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar))); }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t tmem = tslot;
+  // idesc: f32 accum; kind tf32 (a/b fmt 2) or f16 with bf16 (fmt 1)
+  const uint32_t fmt = KIND == 0 ? 2u : 1u;
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+  if (threadIdx.x == 0) {
+    uint64_t a = desc(smem_u32(smem)), b = desc(smem_u32(smem + 32768));
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      if (KIND == 0)
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(i));
+      else
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem), "l"(a), "l"(b), "r"(idesc), "r"(i));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(smem_u32(&bar)));
+    long long t1 = clock64();
+    cycles[blockIdx.x] = t1 - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int KIND, int N>
+void run(const char* name) {
+  unsigned long long* d; cudaMalloc(&d, 148 * 8);
+  auto k = mma_loop<KIND, N>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+  int iters = 4096;
+  k<<<148, 128, 100000>>>(iters, d);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<148, 128, 100000>>>(iters, d);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long c[148]; cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
+  int K = KIND == 0 ? 8 : 16;
+  double flops = 2.0 * 128 * N * K * iters * 148;
+  printf("%s N=%d: %.1f cycles/mma, %.1f TFLOP/s (err=%s)\n", name, N, double(c[0]) / iters,
+         flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+}
+int main() {
+  run<0, 128>("tf32"); run<0, 256>("tf32"); run<0, 64>("tf32");
+  run<1, 128>("bf16"); run<1, 256>("bf16");
+  return 0;
+}
