@@ -217,10 +217,9 @@ def run_ours(args, c, rank, world, dist):
                             seed=1 + rank)
     P = args.pool
     hbs = [src.next_batch() for _ in range(P)]
+    # index capacity per table = the largest batch of the stream (the captured
+    # graph is valid for every batch of the pool; the sort runs over it)
     caps = [max(int(hb.indices[t].size) for hb in hbs) for t in range(cfg.num_tables)]
-    caps = [max(cp, B * c["k"] if c["fixed"] else cp) for cp in caps]
-    if not c["fixed"]:
-        caps = [B * c["k"]] * cfg.num_tables  # worst case: graph valid for any batch
     eng = StepEngine(model, B, caps, lr=0.1)
 
     # device-resident pool and pinned host pool

@@ -83,13 +83,17 @@ __device__ __forceinline__ unsigned subgroup_mask() {
 
 // ---------------------------------------------------------------------------
 // forward: one LPB-lane sub-warp per bag; NV vectors of VEC floats per lane.
+#ifndef DLRM_EMB_U1
+#define DLRM_EMB_U1 4
+#define DLRM_EMB_MINB1 4
+#endif
 template <int VEC, int LPB, int NV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, NV == 1 ? DLRM_EMB_MINB1 : 2)
 emb_fwd_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
                int64_t num_bags, float* __restrict__ out, int64_t out_stride,
                int64_t* err_pos, int32_t* err_flag) {
   using V = typename VecT<VEC>::T;
-  constexpr int U = 4;  // rows in flight per lane
+  constexpr int U = NV == 1 ? DLRM_EMB_U1 : (NV == 2 ? 4 : 2);  // rows in flight per lane
   const int lane = threadIdx.x & (LPB - 1);
   const int64_t group = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LPB;
   const int64_t total = num_bags * ts.nt;
@@ -110,14 +114,21 @@ emb_fwd_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
   for (int i = 0; i < NV; ++i) acc[i] = vzero<V>();
   bool first = true;
 
+  // indices of the next LPB positions are prefetched one chunk ahead
+  int64_t nxt_idx = 0;
+  float nxt_w = 1.f;
+  if (lo + lane < hi) {
+    nxt_idx = __ldg(idxp + lo + lane);
+    if (wts) nxt_w = __ldg(wts + lo + lane);
+  }
   for (int64_t p0 = lo; p0 < hi; p0 += LPB) {
     const int64_t my = p0 + lane;
-    int64_t myidx = 0;
-    float myw = 1.f;
-    if (my < hi) {
-      myidx = __ldg(idxp + my);
-      if (wts) myw = __ldg(wts + my);
-      if (myidx < 0 || myidx >= num_rows) record_error(err_pos, err_flag, t, my);
+    const int64_t myidx = nxt_idx;
+    const float myw = nxt_w;
+    if (my < hi && (myidx < 0 || myidx >= num_rows)) record_error(err_pos, err_flag, t, my);
+    if (p0 + LPB + lane < hi) {
+      nxt_idx = __ldg(idxp + p0 + LPB + lane);
+      if (wts) nxt_w = __ldg(wts + p0 + LPB + lane);
     }
     const int cnt = int(hi - p0 < LPB ? hi - p0 : LPB);
     for (int q = 0; q < cnt; q += U) {
@@ -155,6 +166,90 @@ emb_fwd_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
     const int64_t v = lane + int64_t(i) * LPB;
     if (v < nvec) o[v] = acc[i];
   }
+}
+
+// forward for multi-hot bags: one WARP per bag.  A row is LPB = d/4 lanes,
+// so one warp-wide load instruction fetches RPI = 32/LPB consecutive rows of
+// the bag (U instructions in flight); rows are then folded in strict
+// ascending position order by broadcasting each row's float4 with shuffles
+// (every lane group keeps the same accumulator).  No divergence between bags
+// sharing a warp, 2..8x more rows in flight per warp than one sub-warp/bag.
+#ifndef DLRM_EMBW_U
+#define DLRM_EMBW_U 4
+#endif
+template <int LPB>
+__global__ void __launch_bounds__(256, 4)
+emb_fwd_warp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
+                    int64_t num_bags, float* __restrict__ out, int64_t out_stride,
+                    int64_t* err_pos, int32_t* err_flag) {
+  constexpr int RPI = 32 / LPB;
+  constexpr int U = RPI >= 4 ? DLRM_EMBW_U / 2 : DLRM_EMBW_U;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPB, col = lane % LPB;
+  const int64_t bag = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  if (bag >= num_bags * ts.nt) return;
+  const int t = int(bag / num_bags);
+  const int64_t j = bag - int64_t(t) * num_bags;
+  const int64_t* offs = ts.t[t].offsets;
+  const int64_t* idxp = ts.t[t].indices;
+  const float* wts = ts.t[t].weights;
+  const int64_t row_base = ts.t[t].row_base;
+  const int64_t num_rows = ts.t[t].num_rows;
+  const int64_t lo = __ldg(offs + j), hi = __ldg(offs + j + 1);
+  const float4* Wv = reinterpret_cast<const float4*>(W);
+  const int64_t nvec = dim / 4;
+
+  float4 acc = vzero4();
+  bool first = true;
+  int64_t nxt_idx = 0;
+  float nxt_w = 1.f;
+  if (lo + lane < hi) {
+    nxt_idx = __ldg(idxp + lo + lane);
+    if (wts) nxt_w = __ldg(wts + lo + lane);
+  }
+  for (int64_t p0 = lo; p0 < hi; p0 += 32) {
+    const int64_t myidx = nxt_idx;
+    const float myw = nxt_w;
+    if (p0 + lane < hi && (myidx < 0 || myidx >= num_rows))
+      record_error(err_pos, err_flag, t, p0 + lane);
+    if (p0 + 32 + lane < hi) {
+      nxt_idx = __ldg(idxp + p0 + 32 + lane);
+      if (wts) nxt_w = __ldg(wts + p0 + 32 + lane);
+    }
+    const int cnt = int(hi - p0 < 32 ? hi - p0 : 32);
+    for (int q = 0; q < cnt; q += RPI * U) {
+      float4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int pos = q + u * RPI + sub;
+        const int src = pos < cnt ? pos : cnt - 1;
+        const int64_t ri = __shfl_sync(0xffffffffu, myidx, src);
+        const bool ok = pos < cnt && ri >= 0 && ri < num_rows;
+        r[u] = ok ? __ldg(Wv + (row_base + ri) * nvec + col) : vzero4();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int s = 0; s < RPI; ++s) {
+          const int pos = q + u * RPI + s;
+          const int from = s * LPB + col;
+          float4 v;
+          v.x = __shfl_sync(0xffffffffu, r[u].x, from);
+          v.y = __shfl_sync(0xffffffffu, r[u].y, from);
+          v.z = __shfl_sync(0xffffffffu, r[u].z, from);
+          v.w = __shfl_sync(0xffffffffu, r[u].w, from);
+          const float w = __shfl_sync(0xffffffffu, myw, pos < cnt ? pos : 0);
+          if (pos < cnt) {
+            if (wts) v = vmul(w, v);
+            acc = first ? v : vadd(acc, v);
+            first = false;
+          }
+        }
+      }
+    }
+  }
+  if (sub == 0 && col < nvec)
+    reinterpret_cast<float4*>(out + ts.t[t].out_offset + j * out_stride)[col] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -544,6 +639,21 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
   bool v4 = vec4_ok(dim, W_all, out_stride, 0) &&
             (reinterpret_cast<uintptr_t>(out) % 16) == 0;
   for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
+  int64_t cap_total = 0;
+  for (int i = 0; i < nt; ++i) cap_total += tables[i].capacity;
+  const double avg_pool = double(cap_total) / double(num_bags * nt);
+  const int64_t nv0 = dim / 4;
+  if (v4 && (nv0 == 4 || nv0 == 8 || nv0 == 16 || nv0 == 32) && avg_pool >= 32.0 / nv0) {
+    const int64_t threads = num_bags * nt * 32;
+    const unsigned blocks = unsigned(ceil_div(threads, 256));
+    switch (nv0) {
+      case 4: emb_fwd_warp_kernel<4><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      case 8: emb_fwd_warp_kernel<8><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      case 16: emb_fwd_warp_kernel<16><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      default: emb_fwd_warp_kernel<32><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+    }
+    return check_launch("emb_fwd_warp_kernel");
+  }
   if (v4) {
     const int64_t nv = dim / 4;
     if (nv <= 1) launch_fwd<4, 1, 1>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s);
