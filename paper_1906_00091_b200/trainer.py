@@ -62,7 +62,7 @@ class StepEngine:
 
     def __init__(self, model: DlrmModel, batch_size: int, capacities=None,
                  lr: float = 0.1, weighted: bool = False,
-                 n_total: int | None = None):
+                 n_total: int | None = None, input_sets: int = 1):
         _lib.require_cuda()
         cfg = model.config
         self.model, self.cfg = model, cfg
@@ -104,17 +104,30 @@ class StepEngine:
             v.copy_(tab.weights)
             tab.weights = v
 
-        # ---- inputs
+        # ---- inputs: one contiguous block per input set, laid out exactly
+        # like a packed host batch (pack_host_batch) so a step's inputs move
+        # with ONE copy; views x / labels / offsets / indices (/ weights)
         self.k0 = cfg.dense_dim
-        self.x = torch.zeros((B, ceil4(self.k0)), **f32)
-        self.offsets = torch.zeros((T, B + 1), dtype=torch.int64, device=dev)
         self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
-        self.indices = torch.zeros(int(self.cap_base[-1]), dtype=torch.int64,
-                                   device=dev)
-        self.iweights = (torch.ones(int(self.cap_base[-1]), **f32)
-                         if weighted else None)
-        self.labels = torch.zeros(B, **f32)
-
+        a16 = lambda n: (n + 15) // 16 * 16
+        lay = {}
+        o = 0
+        for name, nbytes in (("x", B * ceil4(self.k0) * 4), ("labels", B * 4),
+                             ("offsets", T * (B + 1) * 8),
+                             ("indices", int(self.cap_base[-1]) * 8),
+                             ("iweights", int(self.cap_base[-1]) * 4 if weighted else 0)):
+            lay[name] = (o, nbytes)
+            o = a16(o + nbytes)
+        self.block_layout, self.block_bytes = lay, o
+        self.input_sets = []
+        for _ in range(max(1, int(input_sets))):
+            blk = torch.zeros(o, dtype=torch.uint8, device=dev)
+            v = self._views(blk)
+            if weighted:
+                v["iweights"].fill_(1.0)
+            self.input_sets.append(v)
+        self.graphs = {}
+        self._set = 0
         # ---- activations
         self.Z = torch.zeros((B, nf * d), **f32)
         bl = model.bottom.layers
@@ -148,24 +161,81 @@ class StepEngine:
         self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
 
+        for v in self.input_sets:
+            v["descs"] = self._make_descs(v)
+        self.use_set(0)
         self._build_descs()
         self.graph = None
         self.launches_per_step = None
 
     # ------------------------------------------------------------------
-    def _build_descs(self):
-        d, nf, B = self.d, self.nf, self.B
+    def _views(self, blk):
+        B, T, lay = self.B, self.T, self.block_layout
+        def view(name, dtype, shape):
+            o, n = lay[name]
+            if n == 0:
+                return None
+            return blk[o:o + n].view(dtype).view(*shape)
+        return {"block": blk,
+                "x": view("x", torch.float32, (B, ceil4(self.k0))),
+                "labels": view("labels", torch.float32, (B,)),
+                "offsets": view("offsets", torch.int64, (T, B + 1)),
+                "indices": view("indices", torch.int64, (int(self.cap_base[-1]),)),
+                "iweights": view("iweights", torch.float32, (int(self.cap_base[-1]),))}
+
+    def _make_descs(self, v):
+        d = self.d
         descs = []
         for t in range(self.T):
             cb = int(self.cap_base[t])
             descs.append(_lib.TableDesc(
-                self.offsets[t].data_ptr(),
-                self.indices.data_ptr() + 8 * cb,
-                (self.iweights.data_ptr() + 4 * cb) if self.weighted else None,
+                v["offsets"][t].data_ptr(),
+                v["indices"].data_ptr() + 8 * cb,
+                (v["iweights"].data_ptr() + 4 * cb) if self.weighted else None,
                 int(self.row_base[t]), self.rows[t], (1 + t) * d,
                 self.caps[t], self.model.tables[t].table_id))
-        self._descs = _lib.table_array(descs)
-        self._descs_p = C.cast(self._descs, C.c_void_p)
+        arr = _lib.table_array(descs)
+        return arr, C.cast(arr, C.c_void_p)
+
+    def use_set(self, k: int):
+        """Point the step at input set k (its buffers and descriptors)."""
+        v = self.input_sets[k]
+        self._set = k
+        self.x, self.labels = v["x"], v["labels"]
+        self.offsets, self.indices, self.iweights = v["offsets"], v["indices"], v["iweights"]
+        self._descs, self._descs_p = v["descs"]
+        self.graph = self.graphs.get(k)
+
+    def pack_host_batch(self, dense, offsets, indices, labels, weights=None):
+        """One pinned host buffer in the input-block layout (done once per
+        batch by the data pipeline; a step then needs a single H2D copy)."""
+        blk = torch.zeros(self.block_bytes, dtype=torch.uint8).pin_memory()
+        v = self._views(blk)
+        v["x"][:, :self.k0].copy_(torch.as_tensor(np.asarray(dense, np.float32)))
+        v["labels"].copy_(torch.as_tensor(np.asarray(labels, np.float32)))
+        for t in range(self.T):
+            v["offsets"][t].copy_(torch.as_tensor(np.asarray(offsets[t], np.int64)))
+            i = np.asarray(indices[t], np.int64)
+            if i.size > self.caps[t]:
+                raise OverflowError(f"table {t}: {i.size} indices exceed capacity "
+                                    f"{self.caps[t]}")
+            cb = int(self.cap_base[t])
+            v["indices"][cb:cb + i.size].copy_(torch.as_tensor(i))
+            if self.weighted:
+                w = np.ones(i.size, np.float32) if weights is None or weights[t] is None \
+                    else np.asarray(weights[t], np.float32)
+                v["iweights"][cb:cb + i.size].copy_(torch.as_tensor(w))
+        self._host_indices = indices
+        return blk
+
+    def stage(self, packed: torch.Tensor, k: int = 0, stream=None):
+        """Copy a packed batch (pinned host or device) into input set k."""
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.input_sets[k]["block"].copy_(packed, non_blocking=True)
+
+    def _build_descs(self):
+        d, nf, B = self.d, self.nf, self.B
         self._feats = _lib.make_features(
             [(self.Z.data_ptr() + 4 * f * d, nf * d) for f in range(nf)])
         self._feats_p = C.c_void_p(C.addressof(self._feats))
@@ -307,8 +377,9 @@ class StepEngine:
 
     # ------------------------------------------------------------------
     def capture(self):
-        """Record launch() into a CUDA graph.  Capturing executes nothing, so
-        run one eager step first (kernel attributes, CUB initialisation)."""
+        """Record launch() for the current input set into a CUDA graph.
+        Capturing executes nothing, so run one eager step first (kernel
+        attributes, CUB initialisation)."""
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
@@ -316,6 +387,7 @@ class StepEngine:
             self.launch()
         self.launches_per_step = _lib.launch_count() - n0
         self.graph = g
+        self.graphs[self._set] = g
         return g
 
     def profile_stages(self, reps: int = 5, flush=None) -> dict:
