@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(fold_groups<LPB>() * LPB)
 emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   using V = typename VecT<VEC>::T;
   constexpr int CH = 32;  // sorted slots staged per batch
-  constexpr int U = 8;    // gradient rows in flight per lane
+  constexpr int U = COALESCE ? 8 : 4;  // gradient rows in flight per lane
   constexpr int GROUPS = fold_groups<LPB>();
   __shared__ uint32_t s_key[GROUPS][CH];
   __shared__ int64_t s_goff[GROUPS][CH];
@@ -400,9 +400,20 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   if (cur == fa.sentinel) return;
   int64_t run_start = base + i;
 
-  V acc[NV];
+  V acc[NV], wcur[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
+  // SGD mode: the table row of each run is prefetched when the run's first
+  // element is loaded, so the read-modify-write at the run's end does not
+  // wait a full memory latency per row
+  if constexpr (!COALESCE) {
+    const V* wr0 = reinterpret_cast<const V*>(fa.W + int64_t(cur) * dim);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = lane + int64_t(v) * LPB;
+      wcur[v] = c < nvec ? wr0[c] : vzero<V>();
+    }
+  }
 
   auto flush = [&](uint32_t row, int64_t rs) {
     if constexpr (COALESCE) {
@@ -420,7 +431,7 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int64_t c = lane + int64_t(v) * LPB;
-        if (c < nvec) wrow[c] = vsgd(wrow[c], fa.lr, acc[v]);
+        if (c < nvec) wrow[c] = vsgd(wcur[v], fa.lr, acc[v]);
       }
     }
   };
@@ -430,15 +441,27 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   while (true) {
     for (; i < cnt; i += U) {
       V r[U][NV];
+      V wr[COALESCE ? 1 : U][NV];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int ii = i + u < cnt ? i + u : cnt - 1;
-        const bool live = (i + u < cnt) && s_key[g][ii] != fa.sentinel;
+        const uint32_t k = s_key[g][ii];
+        const bool live = (i + u < cnt) && k != fa.sentinel;
         const V* src = reinterpret_cast<const V*>(fa.grad + s_goff[g][ii]);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const int64_t c = lane + int64_t(v) * LPB;
           r[u][v] = (live && c < nvec) ? ldg_vec(src + c) : vzero<V>();
+        }
+        if constexpr (!COALESCE) {
+          const uint32_t prev = (i + u == 0) ? cur : s_key[g][ii - (ii > 0 ? 1 : 0)];
+          const bool starts = live && (i + u == 0 ? k != cur : k != prev);
+          const V* wsrc = reinterpret_cast<const V*>(fa.W + int64_t(k) * dim);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const int64_t c = lane + int64_t(v) * LPB;
+            wr[u][v] = (starts && c < nvec) ? wsrc[c] : vzero<V>();
+          }
         }
       }
 #pragma unroll
@@ -452,7 +475,10 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
           cur = k;
           run_start = base + ii;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) acc[v] = vzero<V>();
+          for (int v = 0; v < NV; ++v) {
+            acc[v] = vzero<V>();
+            if constexpr (!COALESCE) wcur[v] = wr[u][v];
+          }
         }
         const float w = s_w[g][ii];
 #pragma unroll

@@ -111,6 +111,63 @@ colreduce_partial_kernel(const float* __restrict__ X, int64_t ldx,
   }
 }
 
+// Vectorised variant (C % 4 == 0, 16-byte aligned rows): a block covers 128
+// columns (32 lanes x float4) and 8 row-groups; 4 independent row streams
+// per thread keep 4 loads in flight.  Same fixed combine order.
+__global__ void __launch_bounds__(256)
+colreduce_partial4_kernel(const float* __restrict__ X, int64_t ldx,
+                          const float* __restrict__ scale, int64_t R, int64_t C,
+                          int64_t rows_per_chunk, float* __restrict__ partial) {
+  __shared__ float4 red[8][32];
+  const int cx = threadIdx.x % 32, ry = threadIdx.x / 32;
+  const int64_t c4 = int64_t(blockIdx.x) * 32 + cx;  // float4 column index
+  const int64_t r0 = int64_t(blockIdx.y) * rows_per_chunk;
+  const int64_t r1 = r0 + rows_per_chunk < R ? r0 + rows_per_chunk : R;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (4 * c4 < C) {
+    const float4* Xv = reinterpret_cast<const float4*>(X);
+    const int64_t ld4 = ldx / 4;
+    int64_t r = r0 + ry;
+    for (; r + 24 < r1; r += 32) {
+      float4 v[4];
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = __ldg(Xv + (r + 8 * u) * ld4 + c4);
+        sc[u] = scale ? __ldg(scale + r + 8 * u) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a.x = fmaf(sc[u], v[u].x, a.x);
+        a.y = fmaf(sc[u], v[u].y, a.y);
+        a.z = fmaf(sc[u], v[u].z, a.z);
+        a.w = fmaf(sc[u], v[u].w, a.w);
+      }
+    }
+    for (; r < r1; r += 8) {
+      const float4 v = __ldg(Xv + r * ld4 + c4);
+      const float sc = scale ? __ldg(scale + r) : 1.f;
+      a.x = fmaf(sc, v.x, a.x);
+      a.y = fmaf(sc, v.y, a.y);
+      a.z = fmaf(sc, v.z, a.z);
+      a.w = fmaf(sc, v.w, a.w);
+    }
+  }
+  red[ry][cx] = a;
+  __syncthreads();
+  if (ry == 0 && 4 * c4 < C) {
+    float4 t = red[0][cx];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+      t.x += red[i][cx].x;
+      t.y += red[i][cx].y;
+      t.z += red[i][cx].z;
+      t.w += red[i][cx].w;
+    }
+    reinterpret_cast<float4*>(partial + int64_t(blockIdx.y) * C)[c4] = t;
+  }
+}
+
 // stage 2: out[c] = sum_z partial[z][c] (ascending z); optional store and
 // fused SGD (p -= fl(lr*g)), skipped when *err_flag.
 __global__ void colreduce_final_kernel(const float* __restrict__ partial,
@@ -123,6 +180,36 @@ __global__ void colreduce_final_kernel(const float* __restrict__ partial,
   for (int z = 1; z < splits; ++z) s += partial[int64_t(z) * C + c];
   if (out) out[c] = s;
   if (upd && !(err_flag && *err_flag)) upd[c] = __fsub_rn(upd[c], __fmul_rn(lr, s));
+}
+
+// dW split-K reduction, 4 consecutive columns per thread (N % 4 == 0).
+__global__ void splitk_final4_kernel(const float* __restrict__ part, int64_t M,
+                                     int64_t N, int splits, float* dW,
+                                     int64_t lddw, float* Wu, int64_t ldw,
+                                     float lr, const int32_t* err_flag) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // float4 index
+  const int64_t n4 = N / 4;
+  if (e >= M * n4) return;
+  const int64_t m = e / n4, c = (e - m * n4) * 4;
+  const float4* P = reinterpret_cast<const float4*>(part);
+  float4 s = P[e];
+  for (int z = 1; z < splits; ++z) {
+    const float4 v = P[int64_t(z) * M * n4 + e];
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  if (dW) {
+    dW[m * lddw + c] = s.x; dW[m * lddw + c + 1] = s.y;
+    dW[m * lddw + c + 2] = s.z; dW[m * lddw + c + 3] = s.w;
+  }
+  if (Wu && !(err_flag && *err_flag)) {
+    float4* w = reinterpret_cast<float4*>(Wu + m * ldw + c);
+    float4 o = *w;
+    o.x = __fsub_rn(o.x, __fmul_rn(lr, s.x));
+    o.y = __fsub_rn(o.y, __fmul_rn(lr, s.y));
+    o.z = __fsub_rn(o.z, __fmul_rn(lr, s.z));
+    o.w = __fsub_rn(o.w, __fmul_rn(lr, s.w));
+    *w = o;
+  }
 }
 
 // dW split-K reduction: dW[m, n] = sum_z part[z][m][n]; optional SGD.
@@ -159,16 +246,24 @@ int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
               int64_t C, float* out, float* upd, float lr,
               const int32_t* err_flag, float* ws, size_t ws_floats,
               cudaStream_t s) {
-  int64_t splits = ceil_div(R, 256);
-  const int64_t col_blocks = ceil_div(C, 32);
-  if (splits * col_blocks > 4 * kNumSMs) splits = ceil_div(4 * kNumSMs, col_blocks);
+  const bool vec = C % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(ws) & 15) == 0;
+  const int64_t col_blocks = vec ? ceil_div(C, 128) : ceil_div(C, 32);
+  // >= 64 rows per chunk, ~2 waves of blocks
+  int64_t splits = ceil_div(R, 64);
+  if (splits * col_blocks > 2 * kNumSMs) splits = ceil_div(2 * kNumSMs, col_blocks);
   if (splits < 1) splits = 1;
   while (splits > 1 && size_t(splits * C) > ws_floats) --splits;
   DLRM_REQUIRE(size_t(splits * C) <= ws_floats, "column-reduction workspace too small");
   const int64_t rpc = R == 0 ? 1 : ceil_div(R, splits);
   splits = R == 0 ? 1 : ceil_div(R, rpc);
-  colreduce_partial_kernel<<<dim3(unsigned(col_blocks), unsigned(splits)), 256, 0, s>>>(
-      X, ldx, scale, R, C, rpc, ws);
+  if (vec) {
+    colreduce_partial4_kernel<<<dim3(unsigned(ceil_div(C, 128)), unsigned(splits)), 256, 0, s>>>(
+        X, ldx, scale, R, C, rpc, ws);
+  } else {
+    colreduce_partial_kernel<<<dim3(unsigned(ceil_div(C, 32)), unsigned(splits)), 256, 0, s>>>(
+        X, ldx, scale, R, C, rpc, ws);
+  }
   if (int rc = check_launch("colreduce_partial_kernel")) return rc;
   colreduce_final_kernel<<<unsigned(ceil_div(C, 256)), 256, 0, s>>>(
       ws, C, int(splits), out, upd, lr, err_flag);
@@ -178,8 +273,16 @@ int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
 int splitk_reduce(const float* part, int64_t M, int64_t N, int splits, float* dW,
                   int64_t lddw, float* Wu, int64_t ldw, float lr,
                   const int32_t* err_flag, cudaStream_t s) {
-  splitk_final_kernel<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(
-      part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+  const bool v4 = N % 4 == 0 && (ldw % 4 == 0 || !Wu) &&
+                  (reinterpret_cast<uintptr_t>(part) & 15) == 0 &&
+                  (!Wu || (reinterpret_cast<uintptr_t>(Wu) & 15) == 0);
+  if (v4) {
+    splitk_final4_kernel<<<unsigned(ceil_div(M * N / 4, 256)), 256, 0, s>>>(
+        part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+  } else {
+    splitk_final_kernel<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(
+        part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+  }
   return check_launch("splitk_final_kernel");
 }
 

@@ -560,7 +560,7 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
 
 size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K) {
   const TcPlan p = weight_plan(M, N, K);
-  return size_t(p.splits) * N * K + size_t(ceil_div(M, 256) + 1) * N;
+  return size_t(p.splits) * N * K + size_t(ceil_div(M, 64) + 1) * N;
 }
 
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,

@@ -180,6 +180,6 @@ extern "C" int dlrm_head_bwd(const float* A, int64_t lda, const float* w,
 }
 
 extern "C" size_t dlrm_head_bwd_workspace_size(int64_t M, int64_t K) {
-  return size_t(ceil_div(M > 0 ? M : 1, 256) + 1) * size_t(K > 1 ? K : 1) *
+  return size_t(ceil_div(M > 0 ? M : 1, 64) + 1) * size_t(K > 1 ? K : 1) *
              sizeof(float) + 256;
 }

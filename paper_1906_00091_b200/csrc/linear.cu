@@ -19,7 +19,7 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 }
 
 size_t colreduce_ws_floats(int64_t R, int64_t C) {
-  return size_t(ceil_div(R, 256) + 1) * size_t(C);
+  return size_t(ceil_div(R, 64) + 1) * size_t(C);
 }
 
 }  // namespace
