@@ -14,6 +14,8 @@
 // Gathers are 128-bit (float4) per lane, LPB = min(32, d/4) lanes per bag,
 // indices loaded coalesced by the sub-warp and broadcast with shuffles, 4 row
 // loads in flight per lane.
+#include <stdlib.h>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -186,70 +188,186 @@ emb_fwd_warp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
   constexpr int U = RPI >= 4 ? DLRM_EMBW_U / 2 : DLRM_EMBW_U;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPB, col = lane % LPB;
-  const int64_t bag = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
-  if (bag >= num_bags * ts.nt) return;
-  const int t = int(bag / num_bags);
-  const int64_t j = bag - int64_t(t) * num_bags;
-  const int64_t* offs = ts.t[t].offsets;
-  const int64_t* idxp = ts.t[t].indices;
-  const float* wts = ts.t[t].weights;
-  const int64_t row_base = ts.t[t].row_base;
-  const int64_t num_rows = ts.t[t].num_rows;
-  const int64_t lo = __ldg(offs + j), hi = __ldg(offs + j + 1);
+  const int64_t total = num_bags * ts.nt;
+  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x / 32);
   const float4* Wv = reinterpret_cast<const float4*>(W);
   const int64_t nvec = dim / 4;
 
-  float4 acc = vzero4();
-  bool first = true;
-  int64_t nxt_idx = 0;
-  float nxt_w = 1.f;
-  if (lo + lane < hi) {
-    nxt_idx = __ldg(idxp + lo + lane);
-    if (wts) nxt_w = __ldg(wts + lo + lane);
+  // persistent: each warp walks bags bag, bag + nwarps, ...; the next bag's
+  // bounds are fetched while the current one is being folded
+  int64_t bag = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+  int64_t nlo = 0, nhi = 0;
+  if (bag < total) {
+    const int t0 = int(bag / num_bags);
+    const int64_t j0 = bag - int64_t(t0) * num_bags;
+    nlo = __ldg(ts.t[t0].offsets + j0);
+    nhi = __ldg(ts.t[t0].offsets + j0 + 1);
   }
-  for (int64_t p0 = lo; p0 < hi; p0 += 32) {
-    const int64_t myidx = nxt_idx;
-    const float myw = nxt_w;
-    if (p0 + lane < hi && (myidx < 0 || myidx >= num_rows))
-      record_error(err_pos, err_flag, t, p0 + lane);
-    if (p0 + 32 + lane < hi) {
-      nxt_idx = __ldg(idxp + p0 + 32 + lane);
-      if (wts) nxt_w = __ldg(wts + p0 + 32 + lane);
+  for (; bag < total; bag += nwarps) {
+    const int t = int(bag / num_bags);
+    const int64_t j = bag - int64_t(t) * num_bags;
+    const int64_t* idxp = ts.t[t].indices;
+    const float* wts = ts.t[t].weights;
+    const int64_t row_base = ts.t[t].row_base;
+    const int64_t num_rows = ts.t[t].num_rows;
+    const int64_t lo = nlo, hi = nhi;
+    const int64_t nb = bag + nwarps;
+    if (nb < total) {
+      const int tn = int(nb / num_bags);
+      const int64_t jn = nb - int64_t(tn) * num_bags;
+      nlo = __ldg(ts.t[tn].offsets + jn);
+      nhi = __ldg(ts.t[tn].offsets + jn + 1);
     }
-    const int cnt = int(hi - p0 < 32 ? hi - p0 : 32);
-    for (int q = 0; q < cnt; q += RPI * U) {
-      float4 r[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int pos = q + u * RPI + sub;
-        const int src = pos < cnt ? pos : cnt - 1;
-        const int64_t ri = __shfl_sync(0xffffffffu, myidx, src);
-        const bool ok = pos < cnt && ri >= 0 && ri < num_rows;
-        r[u] = ok ? __ldg(Wv + (row_base + ri) * nvec + col) : vzero4();
+    float4 acc = vzero4();
+    bool first = true;
+    int64_t nxt_idx = 0;
+    float nxt_w = 1.f;
+    if (lo + lane < hi) {
+      nxt_idx = __ldg(idxp + lo + lane);
+      if (wts) nxt_w = __ldg(wts + lo + lane);
+    }
+    for (int64_t p0 = lo; p0 < hi; p0 += 32) {
+      const int64_t myidx = nxt_idx;
+      const float myw = nxt_w;
+      if (p0 + lane < hi && (myidx < 0 || myidx >= num_rows))
+        record_error(err_pos, err_flag, t, p0 + lane);
+      if (p0 + 32 + lane < hi) {
+        nxt_idx = __ldg(idxp + p0 + 32 + lane);
+        if (wts) nxt_w = __ldg(wts + p0 + 32 + lane);
       }
+      const int cnt = int(hi - p0 < 32 ? hi - p0 : 32);
+      for (int q = 0; q < cnt; q += RPI * U) {
+        float4 r[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < U; ++u) {
+          const int pos = q + u * RPI + sub;
+          const int src = pos < cnt ? pos : cnt - 1;
+          const int64_t ri = __shfl_sync(0xffffffffu, myidx, src);
+          const bool ok = pos < cnt && ri >= 0 && ri < num_rows;
+          r[u] = ok ? __ldg(Wv + (row_base + ri) * nvec + col) : vzero4();
+        }
 #pragma unroll
-        for (int s = 0; s < RPI; ++s) {
-          const int pos = q + u * RPI + s;
-          const int from = s * LPB + col;
-          float4 v;
-          v.x = __shfl_sync(0xffffffffu, r[u].x, from);
-          v.y = __shfl_sync(0xffffffffu, r[u].y, from);
-          v.z = __shfl_sync(0xffffffffu, r[u].z, from);
-          v.w = __shfl_sync(0xffffffffu, r[u].w, from);
-          const float w = __shfl_sync(0xffffffffu, myw, pos < cnt ? pos : 0);
-          if (pos < cnt) {
-            if (wts) v = vmul(w, v);
-            acc = first ? v : vadd(acc, v);
-            first = false;
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int s = 0; s < RPI; ++s) {
+            const int pos = q + u * RPI + s;
+            const int from = s * LPB + col;
+            float4 v;
+            v.x = __shfl_sync(0xffffffffu, r[u].x, from);
+            v.y = __shfl_sync(0xffffffffu, r[u].y, from);
+            v.z = __shfl_sync(0xffffffffu, r[u].z, from);
+            v.w = __shfl_sync(0xffffffffu, r[u].w, from);
+            const float w = __shfl_sync(0xffffffffu, myw, pos < cnt ? pos : 0);
+            if (pos < cnt) {
+              if (wts) v = vmul(w, v);
+              acc = first ? v : vadd(acc, v);
+              first = false;
+            }
           }
         }
       }
     }
+    if (sub == 0 && col < nvec)
+      reinterpret_cast<float4*>(out + ts.t[t].out_offset + j * out_stride)[col] = acc;
   }
-  if (sub == 0 && col < nvec)
-    reinterpret_cast<float4*>(out + ts.t[t].out_offset + j * out_stride)[col] = acc;
+}
+
+// forward for multi-hot bags, cp.async variant: each warp streams the rows of
+// its bags into a 2-slot shared-memory ring with cp.async (16 B per lane, no
+// registers held by in-flight rows), then folds each landed chunk of CH rows in
+// strict ascending position order while the next chunk is in flight.
+// Persistent warps walk bags bag, bag + nwarps, ...
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = ok ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kCpWarps = 12;
+
+template <int NVEC>
+__global__ void __launch_bounds__(32 * kCpWarps, 1)
+emb_fwd_cp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int64_t num_bags,
+                  float* __restrict__ out, int64_t out_stride, int64_t* err_pos,
+                  int32_t* err_flag) {
+  constexpr int CH = 32;                            // rows per chunk
+  constexpr int PER_LANE = CH * NVEC / 32;          // 16-byte copies per lane per chunk
+  extern __shared__ float4 ring[];                  // [warp][2][CH][NVEC]
+  const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
+  float4* myring = ring + size_t(wib) * 2 * CH * NVEC;
+  const int64_t total = num_bags * ts.nt;
+  const int64_t nwarps = int64_t(gridDim.x) * kCpWarps;
+  const float4* Wv = reinterpret_cast<const float4*>(W);
+  const int col = lane % NVEC;
+
+  for (int64_t bag = int64_t(blockIdx.x) * kCpWarps + wib; bag < total; bag += nwarps) {
+    const int t = int(bag / num_bags);
+    const int64_t j = bag - int64_t(t) * num_bags;
+    const int64_t* idxp = ts.t[t].indices;
+    const float* wts = ts.t[t].weights;
+    const int64_t row_base = ts.t[t].row_base;
+    const int64_t num_rows = ts.t[t].num_rows;
+    const int64_t lo = __ldg(ts.t[t].offsets + j), hi = __ldg(ts.t[t].offsets + j + 1);
+    const int nchunks = int((hi - lo + CH - 1) / CH);
+
+    // issue chunk c into slot c & 1 (cp.async 16 B per lane, zero-fill for
+    // out-of-range rows); returns this lane's weight for position `lane`
+    auto issue = [&](int c) -> float {
+      const int64_t p0 = lo + int64_t(c) * CH;
+      const int cnt = int(hi - p0 < CH ? hi - p0 : CH);
+      int64_t myidx = 0;
+      float myw = 1.f;
+      if (lane < cnt) {
+        myidx = __ldg(idxp + p0 + lane);
+        if (wts) myw = __ldg(wts + p0 + lane);
+        if (myidx < 0 || myidx >= num_rows) record_error(err_pos, err_flag, t, p0 + lane);
+      }
+      float4* slot = myring + (c & 1) * CH * NVEC;
+#pragma unroll
+      for (int i = 0; i < PER_LANE; ++i) {
+        const int e = lane + 32 * i;  // element id in [0, CH*NVEC)
+        const int r = e / NVEC, cc = e % NVEC;
+        const int64_t ri = __shfl_sync(0xffffffffu, myidx, r);
+        const bool ok = r < cnt && ri >= 0 && ri < num_rows;
+        cp_async16(slot + r * NVEC + cc, Wv + (row_base + (ok ? ri : 0)) * NVEC + cc, ok);
+      }
+      cp_async_commit();
+      return myw;
+    };
+
+    float4 acc = vzero4();
+    bool first = true;
+    float w_cur = 1.f, w_nxt = 1.f;
+    if (nchunks > 0) w_cur = issue(0);
+    for (int c = 0; c < nchunks; ++c) {
+      if (c + 1 < nchunks) {
+        w_nxt = issue(c + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const int64_t p0 = lo + int64_t(c) * CH;
+      const int cnt = int(hi - p0 < CH ? hi - p0 : CH);
+      const float4* slot = myring + (c & 1) * CH * NVEC;
+      for (int r = 0; r < cnt; ++r) {
+        float4 v = slot[r * NVEC + col];   // out-of-range rows were zero-filled
+        if (wts) v = vmul(__shfl_sync(0xffffffffu, w_cur, r), v);
+        acc = first ? v : vadd(acc, v);
+        first = false;
+      }
+      __syncwarp();
+      w_cur = w_nxt;
+    }
+    if (lane < NVEC)
+      reinterpret_cast<float4*>(out + ts.t[t].out_offset + j * out_stride)[lane] = acc;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -669,9 +787,29 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
   for (int i = 0; i < nt; ++i) cap_total += tables[i].capacity;
   const double avg_pool = double(cap_total) / double(num_bags * nt);
   const int64_t nv0 = dim / 4;
+  if (v4 && (nv0 == 4 || nv0 == 8 || nv0 == 16) && avg_pool >= 8.0 &&
+      !getenv("DLRM_EMB_NO_CP")) {
+    const size_t smem = size_t(kCpWarps) * 2 * 32 * nv0 * 16;
+    DLRM_REQUIRE(smem <= 200 * 1024, "embedding ring exceeds shared memory");
+    const int64_t want = ceil_div(num_bags * nt, kCpWarps);
+    const unsigned blocks = unsigned(want < 2 * kNumSMs ? want : 2 * kNumSMs);
+    auto launch_cp = [&](auto kern) -> int {
+      DLRM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      kern<<<blocks, 32 * kCpWarps, smem, s>>>(W_all, dim, ts, num_bags, out, out_stride,
+                                                err_pos, err_flag);
+      return check_launch("emb_fwd_cp_kernel");
+    };
+    switch (nv0) {
+      case 4: return launch_cp(emb_fwd_cp_kernel<4>);
+      case 8: return launch_cp(emb_fwd_cp_kernel<8>);
+      default: return launch_cp(emb_fwd_cp_kernel<16>);
+    }
+  }
   if (v4 && (nv0 == 4 || nv0 == 8 || nv0 == 16 || nv0 == 32) && avg_pool >= 32.0 / nv0) {
     const int64_t threads = num_bags * nt * 32;
-    const unsigned blocks = unsigned(ceil_div(threads, 256));
+    int64_t want = ceil_div(threads, 256);
+    if (want > 4 * kNumSMs) want = 4 * kNumSMs;  // persistent: 4 blocks per SM
+    const unsigned blocks = unsigned(want);
     switch (nv0) {
       case 4: emb_fwd_warp_kernel<4><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
       case 8: emb_fwd_warp_kernel<8><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;

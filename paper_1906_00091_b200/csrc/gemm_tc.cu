@@ -27,6 +27,7 @@
 // Barriers: full[t] (TMA tx), empty_t[t] / empty_l[l] (tcgen05.commit),
 // conv[l] (4 splitter warps), acc_full (commit after the last k-block).
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "gemm.cuh"
 #include "gemm_tc.cuh"
@@ -151,7 +152,17 @@ struct TcArgs {
   int k_tiles_per_split;
   int k_tiles;
   GemmEpilogue ep;
+  int a3d, b3d;  // MN-major operand described as a 3D tensor: one TMA box per tile
 };
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -228,7 +239,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint8_t* st = raw_ring + s * RAW_BYTES;
         const int k0 = (kt0 + it) * BK;
         mbar_expect_tx(&full[s], RAW_BYTES);
-        if (A_MN) {
+        if (A_MN && args.a3d) {
+          tma_load_3d(st, &tmA, &full[s], 0, k0, int(m0 / 32));
+        } else if (A_MN) {
 #pragma unroll
           for (int c = 0; c < BM / 32; ++c)
             tma_load_2d(st + c * 32 * BK * 4, &tmA, &full[s], int(m0 + 32 * c), k0);
@@ -236,7 +249,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           tma_load_2d(st, &tmA, &full[s], k0, int(m0));
         }
         uint8_t* sb = st + A_BYTES;
-        if (B_MN) {
+        if (B_MN && args.b3d) {
+          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
+        } else if (B_MN) {
 #pragma unroll
           for (int c = 0; c < BN / 32; ++c)
             tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
@@ -485,10 +500,32 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64
   }
 }
 
+// MN-major operand whose MN extent is a multiple of 32, seen as the 3D
+// tensor (32 [stride 1], k [stride ld], mn/32 [stride 32]): one box
+// {32, BK, rows/32} lands exactly the [chunk][k][32] tile layout.
+bool encode3(CUtensorMap* map, const float* base, int64_t mn, int64_t k, int64_t ld,
+             int rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {32, cuuint64_t(k), cuuint64_t(mn / 32)};
+  cuuint64_t strides[2] = {cuuint64_t(ld) * 4, 128};
+  cuuint32_t box[3] = {32, cuuint32_t(BK), cuuint32_t(rows / 32)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+bool use3d(bool mn_major, int64_t mn, int rows) {
+  return mn_major && mn % 32 == 0 && rows % 32 == 0 && rows >= 32 && !getenv("DLRM_NO_TMA3D");
+}
+
 // TMA boxes: K-major operand -> box {BK, rows}; MN-major -> box {32 (or 16), BK}
 bool map_operand(CUtensorMap* m, const float* p, bool mn_major, int64_t mn, int64_t k,
                  int64_t ld, int rows) {
   if (!aligned16(p) || (ld % 4) != 0) return false;
+  if (use3d(mn_major, mn, rows)) return encode3(m, p, mn, k, ld, rows);
   if (mn_major)
     return encode(m, p, mn, k, ld, rows < 32 ? rows : 32, BK,
                   CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -515,7 +552,8 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
                    map_operand(&mb, W, false, N, K, ldw, bn),
                "tensor map encoding failed (linear_fwd)");
-  TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M}};
+  TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M}, 0,
+           0};
   a.k_tiles = int(ceil_div(K, BK));
   a.k_tiles_per_split = a.k_tiles;
   return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
@@ -538,7 +576,8 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
                    map_operand(&mb, W, true, K, N, ldw, bn),
                "tensor map encoding failed (linear_bwd_data)");
-  TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M}};
+  TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M}, 0,
+           use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(N, BK));
   a.k_tiles_per_split = a.k_tiles;
   return launch<false, true>(ma, mb, a, K, bn, 1, s);
@@ -574,7 +613,8 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
                    map_operand(&mb, X, true, K, M, ldx, bn),
                "tensor map encoding failed (linear_bwd_weight)");
-  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N}};
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N},
+           use3d(true, N, BM), use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(M, BK));
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, sp));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));

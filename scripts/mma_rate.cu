@@ -7,7 +7,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 __device__ __forceinline__ uint64_t desc(uint32_t addr) {
   return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(64) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
-template <int KIND, int N>
+// MN-major SWIZZLE_128B_BASE32B: LBO = 32 fp32 x 32 rows = 4096 B, SBO = 512 B
+__device__ __forceinline__ uint64_t desc_mn(uint32_t addr) {
+  return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t(4096 >> 4) << 16) | (uint64_t(512 >> 4) << 32) | (uint64_t(1) << 46) | (uint64_t(1) << 61);
+}
+template <int KIND, int N, int AMN = 0, int BMN = 0>
 __global__ void mma_loop(int iters, unsigned long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tslot;
@@ -24,9 +28,10 @@ __global__ void mma_loop(int iters, unsigned long long* cycles) {
   uint32_t tmem = tslot;
   // idesc: f32 accum; kind tf32 (a/b fmt 2) or f16 with bf16 (fmt 1)
   const uint32_t fmt = KIND == 0 ? 2u : 1u;
-  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(AMN) << 15) | (uint32_t(BMN) << 16) | (uint32_t(N >> 3) << 17) | (uint32_t(128 >> 4) << 24);
   if (threadIdx.x == 0) {
-    uint64_t a = desc(smem_u32(smem)), b = desc(smem_u32(smem + 32768));
+    uint64_t a = AMN ? desc_mn(smem_u32(smem)) : desc(smem_u32(smem));
+    uint64_t b = BMN ? desc_mn(smem_u32(smem + 32768)) : desc(smem_u32(smem + 32768));
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
       if (KIND == 0)
@@ -44,10 +49,10 @@ __global__ void mma_loop(int iters, unsigned long long* cycles) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-template <int KIND, int N>
+template <int KIND, int N, int AMN = 0, int BMN = 0>
 void run(const char* name) {
   unsigned long long* d; cudaMalloc(&d, 148 * 8);
-  auto k = mma_loop<KIND, N>;
+  auto k = mma_loop<KIND, N, AMN, BMN>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
   int iters = 4096;
   k<<<148, 128, 100000>>>(iters, d);
@@ -59,11 +64,12 @@ void run(const char* name) {
   unsigned long long c[148]; cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
   int K = KIND == 0 ? 8 : 16;
   double flops = 2.0 * 128 * N * K * iters * 148;
-  printf("%s N=%d: %.1f cycles/mma, %.1f TFLOP/s (err=%s)\n", name, N, double(c[0]) / iters,
+  printf("%s N=%d A_MN=%d B_MN=%d: %.1f cycles/mma, %.1f TFLOP/s (err=%s)\n", name, N, AMN, BMN, double(c[0]) / iters,
          flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
   run<0, 128>("tf32"); run<0, 256>("tf32"); run<0, 64>("tf32");
+  run<0, 128, 0, 1>("tf32"); run<0, 128, 1, 1>("tf32"); run<0, 128, 1, 0>("tf32"); run<0, 64, 1, 1>("tf32");
   run<1, 128>("bf16"); run<1, 256>("bf16");
   return 0;
 }
