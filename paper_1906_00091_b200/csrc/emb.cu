@@ -458,7 +458,11 @@ struct FoldArgs {
   const uint32_t* uid;  // coalesce mode
   int64_t* rows_out;
   float* values_out;
+  uint32_t* long_count;  // runs longer than kLongRun are deferred here
+  uint4* long_runs;      // (start, end, row, 0)
 };
+
+constexpr int kLongRun = 96;
 
 template <int LPB>
 constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
@@ -606,10 +610,86 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
     base += CH;
     if (base >= fa.n) break;
     if (fa.keys[base] != cur) break;  // our last run ends exactly here
+    if (base - run_start >= CH) {
+      // a hot row: find the run end (galloping search on the sorted keys);
+      // a long run is handed to emb_long_run_kernel, which folds it with a
+      // whole CTA (the strict order is kept there), and dropped here
+      int64_t lo2 = base, step = CH;
+      int64_t hi2 = base + step;
+      while (hi2 < fa.n && fa.keys[hi2] == cur) {
+        lo2 = hi2;
+        step *= 2;
+        hi2 = lo2 + step;
+      }
+      if (hi2 > fa.n) hi2 = fa.n;
+      while (hi2 - lo2 > 1) {  // keys[lo2] == cur, keys[hi2] != cur (or end)
+        const int64_t mid = (lo2 + hi2) >> 1;
+        if (fa.keys[mid] == cur) lo2 = mid; else hi2 = mid;
+      }
+      const int64_t run_end = lo2 + 1;
+      if (run_end - run_start > kLongRun) {
+        if (lane == 0) {
+          const uint32_t slot = atomicAdd(fa.long_count, 1u);
+          fa.long_runs[slot] = make_uint4(uint32_t(run_start), uint32_t(run_end), cur, 0u);
+        }
+        return;
+      }
+    }
     cnt = stage(base);
     i = 0;
   }
   flush(cur, run_start);
+}
+
+// One CTA per deferred long run (a hot row): stage CHUNK gradient rows at a
+// time into shared memory with all threads, then fold them in strict
+// ascending slot order (lanes = columns) — the same result as the per-run
+// fold, with the loads of a hot row spread over a whole CTA.
+template <bool COALESCE>
+__global__ void __launch_bounds__(256)
+emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
+  constexpr int CHUNK = 64;
+  extern __shared__ float s_rows[];  // [CHUNK][dim]
+  __shared__ int64_t s_goff[CHUNK];
+  __shared__ float s_w[CHUNK];
+  const uint32_t r = blockIdx.x;
+  if (r >= max_runs || r >= *fa.long_count) return;
+  if (!COALESCE && fa.err_flag && *fa.err_flag) return;
+  const uint4 run = fa.long_runs[r];
+  const int64_t s0 = run.x, s1 = run.y;
+  const uint32_t row = run.z;
+  const int t = table_of_row(ts, row);
+  float acc = 0.f;  // thread c < dim owns column c
+  for (int64_t p0 = s0; p0 < s1; p0 += CHUNK) {
+    const int cnt = int(s1 - p0 < CHUNK ? s1 - p0 : CHUNK);
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      const uint32_t slot = fa.vals[p0 + threadIdx.x];
+      s_goff[threadIdx.x] = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
+      s_w[threadIdx.x] = ts.t[t].weights ? __ldg(ts.t[t].weights + (slot - ts.cap_base[t])) : 1.f;
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < int64_t(cnt) * dim; e += blockDim.x) {
+      const int i = int(e / dim), c = int(e - int64_t(i) * dim);
+      s_rows[e] = __ldg(fa.grad + s_goff[i] + c);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+      float a = acc;
+      for (int i = 0; i < cnt; ++i) a = __fadd_rn(a, __fmul_rn(s_w[i], s_rows[i * dim + c]));
+      acc = a;
+    }
+  }
+  for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+    if constexpr (COALESCE) {
+      const uint32_t u = fa.uid[s0];
+      fa.values_out[int64_t(u) * dim + c] = acc;
+      if (c == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
+    } else {
+      float* w = fa.W + int64_t(row) * dim + c;
+      *w = __fsub_rn(*w, __fmul_rn(fa.lr, acc));
+    }
+  }
 }
 
 __global__ void err_reset_kernel(int64_t* err_pos, int32_t nt, int32_t* err_flag) {
@@ -667,8 +747,9 @@ void launch_fwd(const float* W, int64_t dim, const TableSet& ts, int64_t nb,
 }
 
 struct WsLayout {
-  size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, temp, total,
+  size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, longs, temp, total,
       temp_bytes;
+  uint32_t max_long;
 };
 
 WsLayout ws_layout(int64_t n) {
@@ -687,7 +768,9 @@ WsLayout ws_layout(int64_t n) {
   L.flags = L.bag + e;
   L.uid = L.flags + e;
   L.err = L.uid + e;
-  L.temp = L.err + align_up((DLRM_MAX_TABLES + 1) * 8, a);
+  L.longs = L.err + align_up((DLRM_MAX_TABLES + 1) * 8, a);
+  L.max_long = uint32_t((n > 0 ? n : 1) / kLongRun + 1);
+  L.temp = L.longs + align_up(16 + size_t(L.max_long) * 16, a);
   L.temp_bytes = align_up(sort_bytes > scan_bytes ? sort_bytes : scan_bytes, a);
   L.total = L.temp + L.temp_bytes;
   return L;
@@ -729,6 +812,26 @@ void launch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim,
   const int64_t chunks = ceil_div(fa.n, 32);
   emb_fold_kernel<VEC, LPB, NV, CO>
       <<<unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, 0, s>>>(fa, ts, dim);
+}
+
+template <bool CO>
+int dispatch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim, bool v4,
+                  cudaStream_t s);
+
+// fold + deferred long runs (hot rows)
+template <bool CO>
+int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
+             const WsLayout& L, cudaStream_t s) {
+  fa.long_count = reinterpret_cast<uint32_t*>(ws + L.longs);
+  fa.long_runs = reinterpret_cast<uint4*>(ws + L.longs + 16);
+  DLRM_CUDA(cudaMemsetAsync(fa.long_count, 0, sizeof(uint32_t), s));
+  if (int rc = dispatch_fold<CO>(fa, ts, dim, v4, s)) return rc;
+  const size_t smem = size_t(64) * dim * 4;
+  auto k = emb_long_run_kernel<CO>;
+  if (smem > 48 * 1024)
+    DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  k<<<L.max_long, 256, smem, s>>>(fa, ts, dim, L.max_long);
+  return check_launch("emb_long_run_kernel");
 }
 
 template <bool CO>
@@ -887,7 +990,7 @@ extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
   bool v4 = vec4_ok(dim, W_all, grad_stride, 0) &&
             (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
   for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
-  return dispatch_fold<false>(fa, ts, dim, v4, s);
+  return run_fold<false>(fa, ts, dim, v4, ws, L, s);
 }
 
 extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
@@ -944,7 +1047,7 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
   fa.values_out = values_out;
   bool v4 = vec4_ok(dim, values_out, grad_stride, one.out_offset) &&
             (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
-  return dispatch_fold<true>(fa, ts, dim, v4, s);
+  return run_fold<true>(fa, ts, dim, v4, ws, L, s);
 }
 
 extern "C" int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,

@@ -133,6 +133,17 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// issue only (no wait): several loads can be in flight before one wait::ld
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -343,34 +354,45 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     // ---- epilogue: TMEM lanes [32q, 32q+32) are readable by warps with
     // warp%4 == q; the two warps of a quarter take half of the columns each.
-    // Each 32x16 block goes registers -> smem (transpose) -> coalesced
-    // row-segment stores (lane = column).
+    // Per 32x16 block: all accumulator loads in flight, one wait, sum,
+    // registers -> smem (transpose) -> float4 row-segment stores (4 lanes per
+    // 64-byte row segment, 8 rows per instruction).
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    float* tile = reinterpret_cast<float*>(lo_ring) + (warp - 2) * (32 * 17);
+    float* tile = reinterpret_cast<float*>(lo_ring) + (warp - 2) * (32 * 20);
     const GemmEpilogue& ep = args.ep;
     const int used = nk < NBIG ? nk : NBIG;
     constexpr int CW = BN / 2 < 16 ? 16 : BN / 2;  // columns per warp
 #pragma unroll 1
     for (int c0 = half * CW; c0 < BN && c0 < (half + 1) * CW; c0 += 16) {
-      float v[16], tt[16];
+      uint32_t ra[NBIG + 1][16];
       const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(c0);
-      tmem_ld16(lane_base + uint32_t(NBIG * BN), v);  // cross terms
-      for (int j = 0; j < used; ++j) {
-        tmem_ld16(lane_base + uint32_t(j * BN), tt);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += tt[i];
+      for (int j = 0; j <= NBIG; ++j) tmem_ld16_issue(lane_base + uint32_t(j * BN), ra[j]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(ra[NBIG][i]);  // cross terms
+#pragma unroll
+      for (int j = 0; j < NBIG; ++j) {
+        if (j < used) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += __uint_as_float(ra[j][i]);
+        }
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) tile[lane * 17 + i] = v[i];
+      for (int i = 0; i < 16; i += 4)
+        *reinterpret_cast<float4*>(tile + lane * 20 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
       __syncwarp();
-      const int c = lane & 15;
-#pragma unroll 4
-      for (int r = lane >> 4; r < 32; r += 2) {
+      const int c4 = (lane & 3) * 4;
+#pragma unroll
+      for (int r = lane >> 2; r < 32; r += 8) {
         const int64_t row = m0 + 32 * q + r;
-        if (row < args.M) apply_epilogue(ep, row, n0 + c0 + c, args.N, tile[r * 17 + c], blockIdx.z);
+        if (row < args.M)
+          apply_epilogue4(ep, row, n0 + c0 + c4, args.N,
+                          *reinterpret_cast<const float4*>(tile + r * 20 + c4), blockIdx.z);
       }
       __syncwarp();
     }
@@ -552,8 +574,9 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
                    map_operand(&mb, W, false, N, K, ldw, bn),
                "tensor map encoding failed (linear_fwd)");
-  TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M}, 0,
-           0};
+  TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M,
+                                        aligned16(Y) && ldy % 4 == 0 && aligned16(b)},
+           0, 0};
   a.k_tiles = int(ceil_div(K, BK));
   a.k_tiles_per_split = a.k_tiles;
   return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
@@ -576,8 +599,10 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
                    map_operand(&mb, W, true, K, N, ldw, bn),
                "tensor map encoding failed (linear_bwd_data)");
-  TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M}, 0,
-           use3d(true, K, bn)};
+  TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M,
+                                        aligned16(dX) && ldx % 4 == 0 &&
+                                            (!mask || (aligned16(mask) && ldm % 4 == 0))},
+           0, use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(N, BK));
   a.k_tiles_per_split = a.k_tiles;
   return launch<false, true>(ma, mb, a, K, bn, 1, s);
@@ -613,7 +638,8 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
                    map_operand(&mb, X, true, K, M, ldx, bn),
                "tensor map encoding failed (linear_bwd_weight)");
-  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N},
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N,
+                                        aligned16(ws) && K % 4 == 0},
            use3d(true, N, BM), use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(M, BK));
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, sp));

@@ -97,7 +97,8 @@ def test_error_payload(idx, pos, val):
 
 @pytest.mark.parametrize("m,d,nb,k,dist", [
     (1000, 16, 512, 1, "u"), (5000, 64, 300, 40, "u"), (20000, 128, 256, 100, "z"),
-    (3000, 256, 64, 17, "u"), (777, 3, 100, 9, "u"), (400, 20, 128, 5, "z")])
+    (3000, 256, 64, 17, "u"), (777, 3, 100, 9, "u"), (400, 20, 128, 5, "z"),
+    (3, 16, 4096, 1, "u"), (5, 64, 2048, 3, "u"), (2, 3, 700, 2, "u")])
 def test_random_bags_bit_exact(m, d, nb, k, dist):
     rng = np.random.default_rng(m + d)
     W = rng.standard_normal((m, d)).astype(np.float32)
@@ -135,12 +136,15 @@ def _multi_table_case(seed, d, sizes, B, k, zipf=False, weighted=False):
 
 
 @pytest.mark.parametrize("d,zipf,weighted", [(16, False, False), (64, True, False),
-                                              (128, False, True), (32, True, True)])
+                                              (128, False, True), (32, True, True),
+                                              (16, "tiny", False), (64, "tiny", True)])
 def test_fused_multitable_fwd_and_bwd_sgd(d, zipf, weighted):
     """dlrm_emb_fwd over 3 tables into a strided [B, nf, d] buffer, then the
     capacity-padded sort + segmented fold + SGD (dlrm_emb_bwd_sgd) vs the
     oracle's lookup_backward + sgd_step_rows per table, bit for bit."""
     sizes, B, k, lr = [3000, 17, 50000], 257, 30, 0.05
+    if zipf == "tiny":  # hot rows: runs of hundreds of slots (long-run path)
+        sizes, B, k, zipf = [3, 4, 50000], 1500, 4, False
     Ws, offs, idxs, wts = _multi_table_case(d, d, sizes, B, k, zipf, weighted)
     dev = torch.device("cuda")
     T, nf = len(sizes), len(sizes) + 1
