@@ -68,8 +68,9 @@ int dlrm_emb_fwd(const float* W_all, int64_t dim, const dlrm_table_desc* tables,
                  int64_t* err_pos, int32_t* err_flag, dlrm_stream_t stream);
 
 /* Bytes of scratch needed by dlrm_emb_bwd_sgd / dlrm_emb_bwd_coalesce for
- * total_capacity index slots over total_rows rows. */
-size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity, int64_t total_rows);
+ * total_capacity index slots over total_rows rows of dim floats. */
+size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity, int64_t total_rows,
+                                   int64_t dim);
 
 /* Sparse backward fused with the SGD row update (ref lookup_backward,
  * embedding.py:182-210, then sgd_step_rows, optim.py:38-46):

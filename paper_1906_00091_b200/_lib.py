@@ -59,7 +59,7 @@ _SIGS = {
     "dlrm_gemm_mode": [_i32],
 }
 _SIZE_FNS = {
-    "dlrm_emb_bwd_workspace_size": [_i64, _i64],
+    "dlrm_emb_bwd_workspace_size": [_i64, _i64, _i64],
     "dlrm_linear_bwd_weight_workspace_size": [_i64, _i64, _i64],
     "dlrm_bce_head_workspace_size": [_i64],
     "dlrm_head_bwd_workspace_size": [_i64, _i64],

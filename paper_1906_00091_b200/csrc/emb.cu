@@ -713,6 +713,148 @@ __global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
   *w = vsgd(*w, lr, g);
 }
 
+// Hot rows (deferred long runs) are reduced in three steps so that a single
+// row's contributions are spread over many warps:
+//   seg_plan:    one CTA: segment counts ceil(len / kSeg) -> prefix seg_base,
+//                and seg_run[segment] = run
+//   seg_fold:    one warp per segment: strict ascending fold of its kSeg
+//                slots (RPI rows per warp instruction, U in flight, folded in
+//                order through shuffles) -> partial[segment]
+//   seg_combine: one CTA per run: partials added in ascending segment order,
+//                then the SGD row update (or the coalesced output).
+// A run of <= kSeg slots is one segment, i.e. bit-identical to the strict
+// fold; hotter rows become a fixed tree of strict folds (deterministic).
+constexpr int kSeg = 256;
+
+__global__ void seg_plan_kernel(FoldArgs fa, uint32_t max_runs, uint32_t max_segs,
+                                uint32_t* seg_base, uint32_t* seg_run) {
+  __shared__ uint32_t s_tot[1024];
+  const uint32_t nruns = min(*fa.long_count, max_runs);
+  // per-thread contiguous run range -> local counts -> block scan
+  const uint32_t per = (nruns + blockDim.x - 1) / blockDim.x;
+  const uint32_t r0 = threadIdx.x * per, r1 = min(nruns, r0 + per);
+  uint32_t cnt = 0;
+  for (uint32_t r = r0; r < r1; ++r) {
+    const uint4 run = fa.long_runs[r];
+    cnt += (run.y - run.x + kSeg - 1) / kSeg;
+  }
+  s_tot[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int o = 1; o < int(blockDim.x); o <<= 1) {  // inclusive scan
+    const uint32_t v = threadIdx.x >= unsigned(o) ? s_tot[threadIdx.x - o] : 0u;
+    __syncthreads();
+    s_tot[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t base = s_tot[threadIdx.x] - cnt;
+  for (uint32_t r = r0; r < r1; ++r) {
+    const uint4 run = fa.long_runs[r];
+    const uint32_t ns = (run.y - run.x + kSeg - 1) / kSeg;
+    seg_base[r] = base;
+    for (uint32_t k = 0; k < ns && base + k < max_segs; ++k) seg_run[base + k] = r;
+    base += ns;
+  }
+  if (threadIdx.x == blockDim.x - 1) seg_base[max_runs] = min(s_tot[threadIdx.x], max_segs);
+}
+
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
+                const uint32_t* seg_base, const uint32_t* seg_run, float* partial) {
+  constexpr int RPI = 32 / LPB;
+  constexpr int U = NV == 1 ? 4 : 2;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPB, col = lane % LPB;
+  const uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (seg >= seg_base[max_runs]) return;
+  const uint32_t r = seg_run[seg];
+  const uint4 run = fa.long_runs[r];
+  const uint32_t row = run.z;
+  const int t = table_of_row(ts, row);
+  const int64_t nvec = dim / 4;
+  const int64_t a = int64_t(run.x) + int64_t(seg - seg_base[r]) * kSeg;
+  const int64_t b = a + kSeg < int64_t(run.y) ? a + kSeg : int64_t(run.y);
+  const float* wts = ts.t[t].weights;
+  const float4* G = reinterpret_cast<const float4*>(fa.grad);
+  float4 acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = vzero4();
+  for (int64_t p0 = a; p0 < b; p0 += 32) {
+    const int cnt = int(b - p0 < 32 ? b - p0 : 32);
+    int64_t goff = 0;  // float4 offset of this lane's slot's gradient row
+    float w = 1.f;
+    if (lane < cnt) {
+      const uint32_t slot = fa.vals[p0 + lane];
+      goff = (ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride) / 4;
+      if (wts) w = __ldg(wts + (slot - ts.cap_base[t]));
+    }
+    for (int q = 0; q < cnt; q += RPI * U) {
+      float4 rr[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int pos = q + u * RPI + sub;
+        const int64_t go = __shfl_sync(0xffffffffu, goff, pos < cnt ? pos : 0);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int64_t c = col + int64_t(v) * LPB;
+          rr[u][v] = (pos < cnt && c < nvec) ? __ldg(G + go + c) : vzero4();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int si = 0; si < RPI; ++si) {
+          const int pos = q + u * RPI + si;
+          const float wp = __shfl_sync(0xffffffffu, w, pos < cnt ? pos : 0);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            float4 x;
+            const int from = si * LPB + col;
+            x.x = __shfl_sync(0xffffffffu, rr[u][v].x, from);
+            x.y = __shfl_sync(0xffffffffu, rr[u][v].y, from);
+            x.z = __shfl_sync(0xffffffffu, rr[u][v].z, from);
+            x.w = __shfl_sync(0xffffffffu, rr[u][v].w, from);
+            if (pos < cnt) acc[v] = vadd(acc[v], vmul(wp, x));
+          }
+        }
+      }
+    }
+  }
+  if (sub == 0) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int64_t c = col + int64_t(v) * LPB;
+      if (c < nvec) reinterpret_cast<float4*>(partial + int64_t(seg) * dim)[c] = acc[v];
+    }
+  }
+}
+
+template <bool COALESCE>
+__global__ void __launch_bounds__(128)
+seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
+                   const uint32_t* seg_base, const float* partial) {
+  const uint32_t r = blockIdx.x;
+  if (r >= max_runs || r >= *fa.long_count) return;
+  if (!COALESCE && fa.err_flag && *fa.err_flag) return;
+  const uint4 run = fa.long_runs[r];
+  const uint32_t row = run.z;
+  const int t = table_of_row(ts, row);
+  const uint32_t g0 = seg_base[r];
+  const uint32_t ns = (run.y - run.x + kSeg - 1) / kSeg;
+  for (int64_t c = threadIdx.x; c < dim; c += blockDim.x) {
+    float v = partial[int64_t(g0) * dim + c];
+    for (uint32_t k = 1; k < ns; ++k) v = __fadd_rn(v, partial[int64_t(g0 + k) * dim + c]);
+    if constexpr (COALESCE) {
+      const uint32_t u = fa.uid[run.x];
+      fa.values_out[int64_t(u) * dim + c] = v;
+      if (c == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
+    } else {
+      float* w = fa.W + int64_t(row) * dim + c;
+      *w = __fsub_rn(*w, __fmul_rn(fa.lr, v));
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // dispatch helpers
 
@@ -747,12 +889,12 @@ void launch_fwd(const float* W, int64_t dim, const TableSet& ts, int64_t nb,
 }
 
 struct WsLayout {
-  size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, longs, temp, total,
-      temp_bytes;
-  uint32_t max_long;
+  size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, longs, segb, segr, part,
+      temp, total, temp_bytes;
+  uint32_t max_long, max_segs;
 };
 
-WsLayout ws_layout(int64_t n) {
+WsLayout ws_layout(int64_t n, int64_t dim) {
   WsLayout L{};
   size_t sort_bytes = 0, scan_bytes = 0;
   cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
@@ -770,7 +912,11 @@ WsLayout ws_layout(int64_t n) {
   L.err = L.uid + e;
   L.longs = L.err + align_up((DLRM_MAX_TABLES + 1) * 8, a);
   L.max_long = uint32_t((n > 0 ? n : 1) / kLongRun + 1);
-  L.temp = L.longs + align_up(16 + size_t(L.max_long) * 16, a);
+  L.max_segs = uint32_t((n > 0 ? n : 1) / kSeg + L.max_long + 1);
+  L.segb = L.longs + align_up(16 + size_t(L.max_long) * 16, a);
+  L.segr = L.segb + align_up(size_t(L.max_long + 1) * 4, a);
+  L.part = L.segr + align_up(size_t(L.max_segs) * 4, a);
+  L.temp = L.part + align_up(size_t(L.max_segs) * size_t(dim > 0 ? dim : 1) * 4, a);
   L.temp_bytes = align_up(sort_bytes > scan_bytes ? sort_bytes : scan_bytes, a);
   L.total = L.temp + L.temp_bytes;
   return L;
@@ -826,6 +972,31 @@ int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
   fa.long_runs = reinterpret_cast<uint4*>(ws + L.longs + 16);
   DLRM_CUDA(cudaMemsetAsync(fa.long_count, 0, sizeof(uint32_t), s));
   if (int rc = dispatch_fold<CO>(fa, ts, dim, v4, s)) return rc;
+  const int64_t nvec = dim / 4;
+  if (v4 && nvec <= 128) {
+    uint32_t* segb = reinterpret_cast<uint32_t*>(ws + L.segb);
+    uint32_t* segr = reinterpret_cast<uint32_t*>(ws + L.segr);
+    float* part = reinterpret_cast<float*>(ws + L.part);
+    seg_plan_kernel<<<1, 1024, 0, s>>>(fa, L.max_long, L.max_segs, segb, segr);
+    if (int rc = check_launch("seg_plan_kernel")) return rc;
+    const unsigned fold_blocks = unsigned(ceil_div(int64_t(L.max_segs) * 32, 256));
+    auto go = [&](auto kern) -> int {
+      kern<<<fold_blocks, 256, 0, s>>>(fa, ts, dim, L.max_long, segb, segr, part);
+      return check_launch("seg_fold_kernel");
+    };
+    int rc;
+    if (nvec <= 1) rc = go(seg_fold_kernel<1, 1>);
+    else if (nvec <= 2) rc = go(seg_fold_kernel<2, 1>);
+    else if (nvec <= 4) rc = go(seg_fold_kernel<4, 1>);
+    else if (nvec <= 8) rc = go(seg_fold_kernel<8, 1>);
+    else if (nvec <= 16) rc = go(seg_fold_kernel<16, 1>);
+    else if (nvec <= 32) rc = go(seg_fold_kernel<32, 1>);
+    else if (nvec <= 64) rc = go(seg_fold_kernel<32, 2>);
+    else rc = go(seg_fold_kernel<32, 4>);
+    if (rc) return rc;
+    seg_combine_kernel<CO><<<L.max_long, 128, 0, s>>>(fa, ts, dim, L.max_long, segb, part);
+    return check_launch("seg_combine_kernel");
+  }
   const size_t smem = size_t(64) * dim * 4;
   auto k = emb_long_run_kernel<CO>;
   if (smem > 48 * 1024)
@@ -941,9 +1112,9 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
 }
 
 extern "C" size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity,
-                                              int64_t total_rows) {
+                                              int64_t total_rows, int64_t dim) {
   (void)total_rows;
-  return ws_layout(total_capacity).total;
+  return ws_layout(total_capacity, dim).total;
 }
 
 extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
@@ -961,7 +1132,7 @@ extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
   const int64_t n = ts.cap_base[nt];
   DLRM_REQUIRE(n < (int64_t(1) << 31), "total capacity must be < 2^31");
   if (n == 0 || num_bags == 0) return 0;
-  const WsLayout L = ws_layout(n);
+  const WsLayout L = ws_layout(n, dim);
   DLRM_REQUIRE(workspace != nullptr && ws_bytes >= L.total,
                "embedding backward workspace too small");
   cudaStream_t s = as_stream(stream);
@@ -1015,7 +1186,7 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
     DLRM_CUDA(cudaMemsetAsync(num_unique, 0, sizeof(int64_t), s));
     return 0;
   }
-  const WsLayout L = ws_layout(n);
+  const WsLayout L = ws_layout(n, dim);
   DLRM_REQUIRE(workspace != nullptr && ws_bytes >= L.total,
                "embedding backward workspace too small");
   const int end_bit = end_bit_for(total_rows);

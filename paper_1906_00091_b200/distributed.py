@@ -233,7 +233,7 @@ class RankEngine:
         # workspaces, step result [loss_sum, correct, err]
         self.emb_ws_bytes = _lib.size("dlrm_emb_bwd_workspace_size",
                                       max(int(self.cap_base[-1]), 1),
-                                      max(self.total_rows, 1))
+                                      max(self.total_rows, 1), d)
         self.emb_ws = torch.empty(self.emb_ws_bytes, dtype=torch.uint8, device=dev)
         lin = max(_lib.size("dlrm_linear_bwd_weight_workspace_size", Bl,
                             l.n_out, l.n_in) for l in self.layers)

@@ -219,7 +219,7 @@ def lookup_backward(table: EmbeddingTable, batch: SparseBatch,
     vals = torch.empty((max(nnz, 1), d), dtype=torch.float32, device=dev)
     nu = torch.zeros(1, dtype=torch.int64, device=dev)
     wsb = _lib.size("dlrm_emb_bwd_workspace_size", max(nnz, 1),
-                    table.num_rows)
+                    table.num_rows, d)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     descs = _lib.table_array([_desc(table, batch)])
     _lib.call("dlrm_emb_bwd_coalesce", d, C.cast(descs, C.c_void_p),

@@ -148,7 +148,7 @@ class StepEngine:
 
         # ---- workspaces and step result
         self.emb_ws_bytes = _lib.size("dlrm_emb_bwd_workspace_size",
-                                      int(self.cap_base[-1]), self.total_rows)
+                                      int(self.cap_base[-1]), self.total_rows, d)
         self.emb_ws = torch.empty(self.emb_ws_bytes, dtype=torch.uint8, device=dev)
         lin = max(_lib.size("dlrm_linear_bwd_weight_workspace_size", B,
                             l.n_out, l.n_in) for l in self.layers)

@@ -53,3 +53,28 @@ def maxnorm_err(got, ref):
     if ref.size == 0:
         return 0.0
     return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+KSEG = 256  # csrc/emb.cu kSeg: runs up to this many slots fold strictly
+
+
+def assert_fold_match(got, exp, absum, counts, rtol=1e-5, ulps=0):
+    """Sparse-gradient rows (or the rows they updated): bit-identical to the
+    strict ascending fold where the row's run is <= KSEG slots; where it is
+    longer (a hot row reduced as a fixed tree of KSEG-slot strict folds),
+    |got - exp| <= rtol * sum|contribution| elementwise.
+    ``counts[i]`` is the run length of row i; ``absum[i]`` the fold of the
+    absolute contributions; ``ulps`` widens the bound by that many ulps of
+    ``exp`` (for weights after the SGD rounding)."""
+    got = np.asarray(got, np.float32)
+    exp = np.asarray(exp, np.float32)
+    counts = np.asarray(counts)
+    assert got.shape == exp.shape
+    short = counts <= KSEG
+    assert np.array_equal(got[short].view(np.uint32), exp[short].view(np.uint32))
+    if (~short).any():
+        d = np.abs(got[~short].astype(np.float64) - exp[~short])
+        tol = (rtol * np.asarray(absum, np.float64)[~short]
+               + ulps * np.spacing(np.abs(exp[~short])) + 1e-30)
+        assert (d <= tol).all(), float((d / tol).max())
+    return int((~short).sum())

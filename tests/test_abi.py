@@ -28,7 +28,7 @@ def test_binding_covers_header():
 
 
 def test_size_queries_callable_without_gpu():
-    assert _lib.size("dlrm_emb_bwd_workspace_size", 1000, 100) > 1000 * 16
+    assert _lib.size("dlrm_emb_bwd_workspace_size", 1000, 100, 16) > 1000 * 16
     assert _lib.size("dlrm_linear_bwd_weight_workspace_size", 2048, 64, 512) > 0
     assert _lib.size("dlrm_bce_head_workspace_size", 2048) >= 256 * 8
     assert b"sm_100a" in _lib.lib().dlrm_build_info()

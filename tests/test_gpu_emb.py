@@ -1,8 +1,11 @@
 """Embedding-bag kernels on the GPU vs the oracle.
 
 Bit-exact against the float32 restatement of the reference's fold order
-(oracle.fp32) for pooled rows, unique-row lists and updated tables; within
-1e-5 (scaled by the row) of the float64 reference fixtures.
+(oracle.fp32) for pooled rows and unique-row lists, and for gradient rows /
+updated table rows whose run is <= 256 slots; hotter rows (reduced as a fixed
+tree of 256-slot strict folds) within 1e-5 of the sum of absolute
+contributions.  Within 1e-5 (scaled by the row) of the float64 reference
+fixtures.
 """
 
 import ctypes as C
@@ -17,6 +20,8 @@ from paper_1906_00091_b200 import (EmbeddingTable, LookupIndexError,
                                    offsets_from_lengths, sgd_step_rows)
 from paper_1906_00091_b200 import _lib
 from paper_1906_00091_b200.rng import zipf_indices
+
+from tests._util import assert_fold_match
 
 pytestmark = pytest.mark.gpu
 
@@ -113,13 +118,18 @@ def test_random_bags_bit_exact(m, d, nb, k, dist):
     g = rng.standard_normal((nb, d)).astype(np.float32)
     sg = lookup_backward(EmbeddingTable(W), b, g)
     rows, vals = fp32.lookup_backward(b.offsets.cpu().numpy(), idx, g, w)
+    _, absum = fp32.lookup_backward(b.offsets.cpu().numpy(), idx, np.abs(g),
+                                    None if w is None else np.abs(w))
+    counts = np.bincount(idx, minlength=m)
     assert np.array_equal(np32(sg.rows), rows)
-    assert np.array_equal(np32(sg.values).view(np.uint32), vals.view(np.uint32))
+    assert_fold_match(np32(sg.values), vals, absum, counts[rows])
     # sparse SGD
     t = EmbeddingTable(W)
     sgd_step_rows(t.weights, sg, 0.1)
     exp_w = fp32.sgd_rows(W, rows, vals, 0.1)
-    assert np.array_equal(np32(t.weights).view(np.uint32), exp_w.view(np.uint32))
+    absum_w = np.zeros_like(W)
+    absum_w[rows] = 0.1 * absum
+    assert_fold_match(np32(t.weights), exp_w, absum_w, counts, ulps=1)
 
 
 def _multi_table_case(seed, d, sizes, B, k, zipf=False, weighted=False):
@@ -143,6 +153,7 @@ def test_fused_multitable_fwd_and_bwd_sgd(d, zipf, weighted):
     capacity-padded sort + segmented fold + SGD (dlrm_emb_bwd_sgd) vs the
     oracle's lookup_backward + sgd_step_rows per table, bit for bit."""
     sizes, B, k, lr = [3000, 17, 50000], 257, 30, 0.05
+    orig_zipf = zipf
     if zipf == "tiny":  # hot rows: runs of hundreds of slots (long-run path)
         sizes, B, k, zipf = [3, 4, 50000], 1500, 4, False
     Ws, offs, idxs, wts = _multi_table_case(d, d, sizes, B, k, zipf, weighted)
@@ -177,18 +188,27 @@ def test_fused_multitable_fwd_and_bwd_sgd(d, zipf, weighted):
         assert np.array_equal(Zh[:, 1 + t].view(np.uint32), exp.view(np.uint32))
     G = torch.as_tensor(np.random.default_rng(1).standard_normal((B, nf * d)),
                         dtype=torch.float32, device=dev)
-    wsb = _lib.size("dlrm_emb_bwd_workspace_size", int(cap_base[-1]), int(row_base[-1]))
+    wsb = _lib.size("dlrm_emb_bwd_workspace_size", int(cap_base[-1]), int(row_base[-1]), d)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     _lib.call("dlrm_emb_bwd_sgd", _lib.ptr(W_all), d, C.cast(descs, C.c_void_p),
               T, B, _lib.ptr(G), nf * d, lr, _lib.ptr(ef), int(row_base[-1]),
               _lib.ptr(ws), wsb, s)
     Wh = np32(W_all).reshape(-1, d)
     Gh = np32(G).reshape(B, nf, d)
+    n_hot = 0
     for t in range(T):
         rows, vals = fp32.lookup_backward(offs[t], idxs[t], Gh[:, 1 + t], wts[t])
+        _, absum = fp32.lookup_backward(
+            offs[t], idxs[t], np.abs(Gh[:, 1 + t]),
+            None if wts[t] is None else np.abs(wts[t]))
         exp = fp32.sgd_rows(Ws[t], rows, vals, lr)
+        absum_w = np.zeros_like(exp)
+        absum_w[rows] = lr * absum
         got = Wh[row_base[t]:row_base[t + 1]]
-        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), t
+        n_hot += assert_fold_match(got, exp, absum_w,
+                                   np.bincount(idxs[t], minlength=sizes[t]), ulps=1)
+    if orig_zipf == "tiny":
+        assert n_hot > 0  # the segment-tree path was exercised
 
 
 def test_bwd_sgd_skips_update_on_error():
@@ -208,7 +228,7 @@ def test_bwd_sgd_skips_update_on_error():
     _lib.call("dlrm_emb_fwd", _lib.ptr(W), d, C.cast(descs, C.c_void_p), 1, B,
               _lib.ptr(out), d, _lib.ptr(ep), _lib.ptr(ef), s)
     assert int(ef.item()) == 1 and int(ep.item()) == B - 1
-    wsb = _lib.size("dlrm_emb_bwd_workspace_size", B, 10)
+    wsb = _lib.size("dlrm_emb_bwd_workspace_size", B, 10, d)
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     _lib.call("dlrm_emb_bwd_sgd", _lib.ptr(W), d, C.cast(descs, C.c_void_p), 1, B,
               _lib.ptr(torch.ones((B, d), device=dev)), d, 0.1, _lib.ptr(ef), 10,
