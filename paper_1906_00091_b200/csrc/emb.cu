@@ -272,16 +272,17 @@ emb_fwd_warp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
   }
 }
 
-// forward for multi-hot bags, cp.async variant: each warp streams the rows of
-// its bags into a 2-slot shared-memory ring with cp.async (16 B per lane, no
-// registers held by in-flight rows), then folds each landed chunk of CH rows in
-// strict ascending position order while the next chunk is in flight.
-// Persistent warps walk bags bag, bag + nwarps, ...
+// cp.async helpers (16 B per lane, zero fill when !ok)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int n = ok ? 16 : 0;  // src-size 0 -> zero fill
+#ifndef DLRM_CP_CA
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
                : "memory");
+#else
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -289,84 +290,223 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr int kCpWarps = 12;
+// ---------------------------------------------------------------------------
+// forward, streaming variant (the default for 16-byte-aligned rows).
+//
+// Work split: the positions of all tables form one space (table t's slots at
+// pre[t] + [0, nnz_t)); warp w of nwarps owns the bags whose first position
+// falls in [w, w+1) * P / nwarps, i.e. a CONTIGUOUS run of bags balanced by
+// rows, found with a 32-ary search over the offsets.  The warp then streams
+// that run's rows through an S-slot cp.async ring of CH-row chunks without
+// draining at bag boundaries (indices are fetched two chunks ahead, bag ends
+// one 32-bag window ahead), and folds every chunk in strict ascending
+// position order, emitting a bag when the position reaches its end offset.
+constexpr uint32_t kBadRow = 0xffffffffu;  // stream path: tables have < 2^32 - 1 rows
 
-template <int NVEC>
-__global__ void __launch_bounds__(32 * kCpWarps, 1)
-emb_fwd_cp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int64_t num_bags,
-                  float* __restrict__ out, int64_t out_stride, int64_t* err_pos,
-                  int32_t* err_flag) {
-  constexpr int CH = 32;                            // rows per chunk
-  constexpr int PER_LANE = CH * NVEC / 32;          // 16-byte copies per lane per chunk
-  extern __shared__ float4 ring[];                  // [warp][2][CH][NVEC]
+struct StreamIdx {
+  int64_t ix;
+  float w;
+};
+
+// first global bag g = t * nb + j with pre[t] + offs_t[j] >= a (nt * nb if none)
+__device__ __forceinline__ int64_t stream_bag_at(const TableSet& ts, int64_t nb,
+                                                 const int64_t* pre, const int64_t* last,
+                                                 int64_t a) {
+  const int lane = threadIdx.x & 31;
+  int t = -1;
+  for (int base = 0; base < ts.nt && t < 0; base += 32) {
+    const int tt = base + lane;
+    const bool hit = tt < ts.nt && pre[tt] + last[tt] >= a;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) t = base + __ffs(m) - 1;
+  }
+  if (t < 0) return int64_t(ts.nt) * nb;
+  const int64_t* offs = ts.t[t].offsets;
+  const int64_t target = a - pre[t];
+  int64_t lo = 0, hi = nb - 1;  // offs[hi] >= target; answer in [lo, hi]
+  while (hi > lo) {
+    const int64_t step = (hi - lo + 30) / 31;  // lane 31 probes >= hi
+    const int64_t jk = lo + int64_t(lane) * step;
+    const bool ge = jk >= hi || __ldg(offs + jk) >= target;
+    const int k = __ffs(__ballot_sync(0xffffffffu, ge)) - 1;
+    const int64_t nhi = lo + int64_t(k) * step < hi ? lo + int64_t(k) * step : hi;
+    lo = k == 0 ? lo : lo + int64_t(k - 1) * step + 1;
+    hi = nhi;
+  }
+  return int64_t(t) * nb + lo;
+}
+
+template <int NVM, int CH, int S, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 1)
+emb_fwd_stream_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int64_t nb,
+                      float* __restrict__ out, int64_t out_stride, int64_t* err_pos,
+                      int32_t* err_flag) {
+  constexpr int SLOT = CH * NVM;                  // float4 per ring slot
+  constexpr int PER_LANE = (SLOT + 31) / 32;      // 16-byte copies per lane per chunk
+  constexpr int NL = NVM >= 32 ? NVM / 32 : 1;    // float4 columns per lane
+  constexpr int CW = NVM >= 32 ? 32 : NVM;        // lanes per row
+  extern __shared__ float4 smem[];
+  __shared__ int64_t pre[DLRM_MAX_TABLES + 1], last[DLRM_MAX_TABLES];
   const int lane = threadIdx.x & 31, wib = threadIdx.x / 32;
-  float4* myring = ring + size_t(wib) * 2 * CH * NVEC;
-  const int64_t total = num_bags * ts.nt;
-  const int64_t nwarps = int64_t(gridDim.x) * kCpWarps;
+  float4* ring = smem + size_t(wib) * S * SLOT;
+  float* wring = reinterpret_cast<float*>(smem + size_t(WARPS) * S * SLOT) + wib * S * CH;
   const float4* Wv = reinterpret_cast<const float4*>(W);
-  const int col = lane % NVEC;
+  const int64_t nvec = dim / 4;
 
-  for (int64_t bag = int64_t(blockIdx.x) * kCpWarps + wib; bag < total; bag += nwarps) {
-    const int t = int(bag / num_bags);
-    const int64_t j = bag - int64_t(t) * num_bags;
+  if (threadIdx.x < ts.nt) {
+    pre[threadIdx.x + 1] = __ldg(ts.t[threadIdx.x].offsets + nb);
+    last[threadIdx.x] = __ldg(ts.t[threadIdx.x].offsets + nb - 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    pre[0] = 0;
+    for (int t = 0; t < ts.nt; ++t) pre[t + 1] += pre[t];
+  }
+  __syncthreads();
+  const int64_t P = pre[ts.nt];
+  const int64_t nwarps = int64_t(gridDim.x) * WARPS;
+  const int64_t gw = int64_t(blockIdx.x) * WARPS + wib;
+  const int64_t g0 = gw == 0 ? 0 : stream_bag_at(ts, nb, pre, last, P * gw / nwarps);
+  const int64_t g1 = gw == nwarps - 1 ? int64_t(ts.nt) * nb
+                                      : stream_bag_at(ts, nb, pre, last, P * (gw + 1) / nwarps);
+
+  for (int64_t g = g0; g < g1;) {
+    const int t = int(g / nb);
+    const int64_t j0 = g - int64_t(t) * nb;
+    const int64_t j1 = (g1 - int64_t(t) * nb) < nb ? g1 - int64_t(t) * nb : nb;
+    g = int64_t(t) * nb + j1;
+    const int64_t* offs = ts.t[t].offsets;
     const int64_t* idxp = ts.t[t].indices;
     const float* wts = ts.t[t].weights;
     const int64_t row_base = ts.t[t].row_base;
     const int64_t num_rows = ts.t[t].num_rows;
-    const int64_t lo = __ldg(ts.t[t].offsets + j), hi = __ldg(ts.t[t].offsets + j + 1);
-    const int nchunks = int((hi - lo + CH - 1) / CH);
+    float* obase = out + ts.t[t].out_offset;
+    const int64_t P0 = __ldg(offs + j0), P1 = __ldg(offs + j1);
+    const int nch = int(ceil_div(P1 - P0, CH));
+    const float4* Wt = Wv + row_base * NVM;
 
-    // issue chunk c into slot c & 1 (cp.async 16 B per lane, zero-fill for
-    // out-of-range rows); returns this lane's weight for position `lane`
-    auto issue = [&](int c) -> float {
-      const int64_t p0 = lo + int64_t(c) * CH;
-      const int cnt = int(hi - p0 < CH ? hi - p0 : CH);
-      int64_t myidx = 0;
-      float myw = 1.f;
-      if (lane < cnt) {
-        myidx = __ldg(idxp + p0 + lane);
-        if (wts) myw = __ldg(wts + p0 + lane);
-        if (myidx < 0 || myidx >= num_rows) record_error(err_pos, err_flag, t, p0 + lane);
+    // bag ends: lane k of win holds offs[wb + 1 + k]; win_nx the next window
+    int64_t wb = j0;
+    auto load_win = [&](int64_t base) -> int64_t {
+      const int64_t jj = base + 1 + lane;
+      return jj <= j1 ? __ldg(offs + jj) : P1;
+    };
+    int64_t win = load_win(wb), win_nx = load_win(wb + 32);
+    int64_t j = j0;
+    int64_t bend = __shfl_sync(0xffffffffu, win, 0);
+
+    // index prefetch queue: q0 feeds the next issue, q1 the one after
+    auto load_idx = [&](int c) -> StreamIdx {
+      StreamIdx r{0, 1.f};
+      const int64_t p = P0 + int64_t(c) * CH + lane;
+      if (lane < CH && c < nch && p < P1) {
+        r.ix = __ldg(idxp + p);
+        if (wts) r.w = __ldg(wts + p);
       }
-      float4* slot = myring + (c & 1) * CH * NVEC;
+      return r;
+    };
+    StreamIdx q0 = load_idx(0), q1 = load_idx(1);
+    int issued = 0, islot = 0;
+    auto issue = [&]() {
+      if (issued < nch) {
+        const int64_t p0 = P0 + int64_t(issued) * CH;
+        const int cnt = int(P1 - p0 < CH ? P1 - p0 : CH);
+        // one validated 32-bit row id per lane; kBadRow lanes are zero-filled
+        const int64_t ix = q0.ix;
+        uint32_t myrow = kBadRow;
+        if (lane < cnt) {
+          if (ix < 0 || ix >= num_rows) record_error(err_pos, err_flag, t, p0 + lane);
+          else myrow = uint32_t(ix);
+        }
+        float4* slot = ring + islot * SLOT;
+        if (wts && lane < CH) wring[islot * CH + lane] = q0.w;
 #pragma unroll
-      for (int i = 0; i < PER_LANE; ++i) {
-        const int e = lane + 32 * i;  // element id in [0, CH*NVEC)
-        const int r = e / NVEC, cc = e % NVEC;
-        const int64_t ri = __shfl_sync(0xffffffffu, myidx, r);
-        const bool ok = r < cnt && ri >= 0 && ri < num_rows;
-        cp_async16(slot + r * NVEC + cc, Wv + (row_base + (ok ? ri : 0)) * NVEC + cc, ok);
+        for (int i = 0; i < PER_LANE; ++i) {
+          const int e = lane + 32 * i;
+          const int r = e / NVM, cc = e % NVM;
+          const uint32_t rr = __shfl_sync(0xffffffffu, myrow, r < CH ? r : 0);
+          const bool ok = rr != kBadRow;
+          if (e < SLOT) cp_async16(slot + e, Wt + size_t(ok ? rr : 0u) * NVM + cc, ok);
+        }
       }
       cp_async_commit();
-      return myw;
+      ++issued;
+      islot = islot == S - 1 ? 0 : islot + 1;
+      q0 = q1;
+      q1 = load_idx(issued + 1);
     };
 
-    float4 acc = vzero4();
+    float4 acc[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) acc[k] = vzero4();
     bool first = true;
-    float w_cur = 1.f, w_nxt = 1.f;
-    if (nchunks > 0) w_cur = issue(0);
-    for (int c = 0; c < nchunks; ++c) {
-      if (c + 1 < nchunks) {
-        w_nxt = issue(c + 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+    auto emit = [&]() {
+      float4* o = reinterpret_cast<float4*>(obase + j * out_stride);
+#pragma unroll
+      for (int k = 0; k < NL; ++k) {
+        const int col = lane % CW + 32 * k;
+        if (lane < CW && col < nvec) o[col] = acc[k];
+        acc[k] = vzero4();
+      }
+      first = true;
+      ++j;
+      if (j - wb == 32) {
+        wb += 32;
+        win = win_nx;
+        win_nx = load_win(wb + 32);
+      }
+      bend = __shfl_sync(0xffffffffu, win, int(j - wb));
+    };
+
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) issue();
+    for (int c = 0, cs = 0; c < nch; ++c, cs = cs == S - 1 ? 0 : cs + 1) {
+      issue();
+      cp_async_wait<S - 1>();
+      __syncwarp();
+      const int64_t p0 = P0 + int64_t(c) * CH;
+      const int cnt = int(P1 - p0 < CH ? P1 - p0 : CH);
+      const float4* sp = ring + cs * SLOT + lane % CW;  // zero-filled past cnt / bad rows
+      const float* wsl = wring + cs * CH;
+      auto row = [&](int r, float4 (&v)[NL]) {
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+          v[k] = sp[r * NVM + 32 * k];
+          if (wts) v[k] = vmul(wsl[r], v[k]);
+        }
+      };
+      int r = 0;
+      while (r < cnt) {
+        while (p0 + r == bend) emit();
+        const int rend = bend - p0 < cnt ? int(bend - p0) : cnt;
+        if (first) {
+          float4 v[NL];
+          row(r, v);
+#pragma unroll
+          for (int k = 0; k < NL; ++k) acc[k] = v[k];
+          first = false;
+          ++r;
+        }
+        for (; r + 4 <= rend; r += 4) {
+          float4 v[4][NL];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) row(r + u, v[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int k = 0; k < NL; ++k) acc[k] = vadd(acc[k], v[u][k]);
+        }
+        for (; r < rend; ++r) {
+          float4 v[NL];
+          row(r, v);
+#pragma unroll
+          for (int k = 0; k < NL; ++k) acc[k] = vadd(acc[k], v[k]);
+        }
       }
       __syncwarp();
-      const int64_t p0 = lo + int64_t(c) * CH;
-      const int cnt = int(hi - p0 < CH ? hi - p0 : CH);
-      const float4* slot = myring + (c & 1) * CH * NVEC;
-      for (int r = 0; r < cnt; ++r) {
-        float4 v = slot[r * NVEC + col];   // out-of-range rows were zero-filled
-        if (wts) v = vmul(__shfl_sync(0xffffffffu, w_cur, r), v);
-        acc = first ? v : vadd(acc, v);
-        first = false;
-      }
-      __syncwarp();
-      w_cur = w_nxt;
     }
-    if (lane < NVEC)
-      reinterpret_cast<float4*>(out + ts.t[t].out_offset + j * out_stride)[lane] = acc;
+    cp_async_wait<0>();
+    while (j < j1) emit();
   }
 }
 
@@ -888,6 +1028,20 @@ void launch_fwd(const float* W, int64_t dim, const TableSet& ts, int64_t nb,
       W, dim, ts, nb, out, stride, ep, ef);
 }
 
+template <int NVM, int CH, int S, int WARPS>
+int launch_stream(const float* W, int64_t dim, const TableSet& ts, int64_t nb, float* out,
+                  int64_t stride, int64_t* ep, int32_t* ef, cudaStream_t s) {
+  const size_t smem = size_t(WARPS) * S * (CH * NVM * 16 + CH * 4);
+  auto kern = emb_fwd_stream_kernel<NVM, CH, S, WARPS>;
+  static bool attr = false;
+  if (!attr) {
+    DLRM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<kNumSMs, 32 * WARPS, smem, s>>>(W, dim, ts, nb, out, stride, ep, ef);
+  return check_launch("emb_fwd_stream_kernel");
+}
+
 struct WsLayout {
   size_t keys_a, keys_b, vals_a, vals_b, bag, flags, uid, err, longs, segb, segr, part,
       temp, total, temp_bytes;
@@ -1061,23 +1215,47 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
   for (int i = 0; i < nt; ++i) cap_total += tables[i].capacity;
   const double avg_pool = double(cap_total) / double(num_bags * nt);
   const int64_t nv0 = dim / 4;
-  if (v4 && (nv0 == 4 || nv0 == 8 || nv0 == 16) && avg_pool >= 8.0 &&
-      !getenv("DLRM_EMB_NO_CP")) {
-    const size_t smem = size_t(kCpWarps) * 2 * 32 * nv0 * 16;
-    DLRM_REQUIRE(smem <= 200 * 1024, "embedding ring exceeds shared memory");
-    const int64_t want = ceil_div(num_bags * nt, kCpWarps);
-    const unsigned blocks = unsigned(want < 2 * kNumSMs ? want : 2 * kNumSMs);
-    auto launch_cp = [&](auto kern) -> int {
-      DLRM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      kern<<<blocks, 32 * kCpWarps, smem, s>>>(W_all, dim, ts, num_bags, out, out_stride,
-                                                err_pos, err_flag);
-      return check_launch("emb_fwd_cp_kernel");
-    };
-    switch (nv0) {
-      case 4: return launch_cp(emb_fwd_cp_kernel<4>);
-      case 8: return launch_cp(emb_fwd_cp_kernel<8>);
-      default: return launch_cp(emb_fwd_cp_kernel<16>);
+  // streaming kernel for multi-hot bags and wide rows; pooling-1 narrow rows
+  // keep the sub-warp kernel (lower fixed latency)
+  bool stream_ok = v4 && nv0 <= 128 && (nv0 & (nv0 - 1)) == 0 && (avg_pool >= 3.0 || nv0 >= 32) &&
+                   !getenv("DLRM_EMB_NO_STREAM");
+  for (int i = 0; i < nt && stream_ok; ++i) stream_ok = tables[i].num_rows < int64_t(kBadRow);
+  if (stream_ok) {
+    static const int cfg = getenv("DLRM_EMB_FWD_CFG") ? atoi(getenv("DLRM_EMB_FWD_CFG")) : 1;
+#define DLRM_STREAM(NVM, CH, S, W) \
+  return launch_stream<NVM, CH, S, W>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag, s)
+    // (CH rows per chunk, S ring slots, W warps per CTA), ~200 KB of ring per
+    // SM; defaults measured on B200 (scripts/emb_one.py, DLRM_EMB_FWD_CFG)
+    if (nv0 == 1) DLRM_STREAM(1, 32, 4, 16);
+    if (nv0 == 2) DLRM_STREAM(2, 32, 4, 16);
+    if (nv0 == 4) {
+      if (cfg == 0) DLRM_STREAM(4, 32, 4, 16);
+      DLRM_STREAM(4, 32, 2, 16);
     }
+    if (nv0 == 8) {
+      if (cfg == 0) DLRM_STREAM(8, 32, 4, 12);
+      DLRM_STREAM(8, 32, 3, 16);
+    }
+    if (nv0 == 16) {
+      if (cfg == 0) DLRM_STREAM(16, 32, 4, 6);
+      if (cfg == 2) DLRM_STREAM(16, 16, 4, 12);
+      if (cfg == 4) DLRM_STREAM(16, 32, 3, 8);
+      DLRM_STREAM(16, 16, 3, 16);
+    }
+    if (nv0 == 32) {
+      if (cfg == 0) DLRM_STREAM(32, 16, 4, 6);
+      if (cfg == 2) DLRM_STREAM(32, 8, 4, 12);
+      if (cfg == 3) DLRM_STREAM(32, 8, 3, 16);
+      DLRM_STREAM(32, 16, 3, 8);
+    }
+    if (nv0 == 64) {
+      if (cfg == 0) DLRM_STREAM(64, 8, 4, 6);
+      if (cfg == 2) DLRM_STREAM(64, 4, 4, 12);
+      if (cfg == 3) DLRM_STREAM(64, 4, 3, 16);
+      DLRM_STREAM(64, 8, 3, 8);
+    }
+    DLRM_STREAM(128, 4, 3, 8);
+#undef DLRM_STREAM
   }
   if (v4 && (nv0 == 4 || nv0 == 8 || nv0 == 16 || nv0 == 32) && avg_pool >= 32.0 / nv0) {
     const int64_t threads = num_bags * nt * 32;

@@ -18,12 +18,19 @@ from paper_1906_00091_b200.rng import zipf_indices
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--rows", type=int, nargs="*")
+ap.add_argument("--d", type=int, nargs="*")
+ap.add_argument("--pool", type=int, nargs="*")
+ap.add_argument("--fwd-only", action="store_true")
 a = ap.parse_args()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists("MEASURED_PEAKS.json") else 6553.6
 rows_list = [10**5, 10**6, 10**7] if a.quick else [10**5, 10**6, 10**7, 10**8]
 d_list = [16, 64, 128, 256]
 pool_list = [1, 8, 32, 128]
+rows_list = a.rows or rows_list
+d_list = a.d or d_list
+pool_list = a.pool or pool_list
 dev = torch.device("cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 s = _lib.stream_handle()
@@ -67,7 +74,7 @@ for rows in rows_list:
                               P(ef), rows, P(ws), wsb, s)
                 _lib.call("dlrm_err_reset", P(ep), 1, P(ef), s)
                 tf = timeit(fwd, a.reps)
-                tb = timeit(bwd, a.reps)
+                tb = float('nan') if a.fwd_only else timeit(bwd, a.reps)
                 u = int(torch.unique(idx).numel())
                 bf = nnz * (4 * d + 8) + (B + 1) * 8 + B * 4 * d
                 bb = B * 4 * d + nnz * 8 + (B + 1) * 8 + 2 * u * 4 * d
