@@ -86,6 +86,23 @@ int dlrm_emb_bwd_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
                      int64_t total_rows, void* workspace, size_t ws_bytes,
                      dlrm_stream_t stream);
 
+/* dlrm_emb_bwd_sgd in two phases so the index-only work can run off the
+ * critical path (e.g. on a side stream during the forward pass):
+ *   prepare    keys + stable radix sort of (row, position) pairs; reads only
+ *              offsets / indices, writes the workspace;
+ *   apply_sgd  segmented fold of grad + row update from that workspace (same
+ *              arguments and semantics as dlrm_emb_bwd_sgd).
+ * apply_sgd must be ordered after prepare on the same workspace and tables.
+ * dlrm_emb_bwd_sgd == prepare; apply_sgd. */
+int dlrm_emb_bwd_prepare(int64_t dim, const dlrm_table_desc* tables, int32_t nt,
+                         int64_t num_bags, int64_t total_rows, void* workspace,
+                         size_t ws_bytes, dlrm_stream_t stream);
+int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                           int32_t nt, int64_t num_bags, const float* grad,
+                           int64_t grad_stride, float lr, const int32_t* err_flag,
+                           int64_t total_rows, void* workspace, size_t ws_bytes,
+                           dlrm_stream_t stream);
+
 /* lookup_backward parity path for ONE table: coalesced SparseRowGrad.
  * rows_out[u] ascending unique local rows, values_out[u*dim..] their folded
  * gradients, *num_unique = u (device int64).  Buffers sized for nnz rows.

@@ -37,6 +37,9 @@ _SIGS = {
     "dlrm_emb_fwd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
     "dlrm_emb_bwd_sgd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _f32, _vp,
                          _i64, _vp, _sz, _vp],
+    "dlrm_emb_bwd_prepare": [_i64, _vp, _i32, _i64, _i64, _vp, _sz, _vp],
+    "dlrm_emb_bwd_apply_sgd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _f32,
+                               _vp, _i64, _vp, _sz, _vp],
     "dlrm_emb_bwd_coalesce": [_i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _sz, _vp],
     "dlrm_sgd_rows": [_vp, _i64, _vp, _vp, _i64, _f32, _vp],

@@ -514,43 +514,53 @@ emb_fwd_stream_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int
 // backward, stage 1: one (key = global row, value = slot) pair per index slot
 // plus the bag of each live slot.  Slots past a table's nnz get the sentinel
 // key so a capacity-sized (graph-static) sort leaves them at the end.
+// Blocks [0, bag_blocks) walk bags (LPB lanes per bag, positions strided over
+// the lanes: no per-slot search for the bag); the remaining blocks walk the
+// capacity and fill the padding slots.
+template <int LPB>
 __global__ void __launch_bounds__(256)
-emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots,
+emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots, int64_t bag_blocks,
                 uint32_t sentinel, uint32_t* __restrict__ keys,
                 uint32_t* __restrict__ vals, int32_t* __restrict__ bag_of,
                 int64_t* err_pos, int32_t* err_flag) {
-  const int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (blockIdx.x < bag_blocks) {
+    const int64_t gb = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LPB;
+    const int lane = threadIdx.x % LPB;
+    if (gb >= num_bags * ts.nt) return;
+    const int t = int(gb / num_bags);
+    const int64_t j = gb - int64_t(t) * num_bags;
+    const int64_t* offs = ts.t[t].offsets;
+    const int64_t lo = __ldg(offs + j), hi = __ldg(offs + j + 1);
+    const int64_t* idxp = ts.t[t].indices;
+    const int64_t nrows = ts.t[t].num_rows, rbase = ts.t[t].row_base;
+    const int64_t cb = ts.cap_base[t], cap = ts.t[t].capacity;
+    for (int64_t k = lo + lane; k < hi; k += LPB) {
+      if (k >= cap) {  // more indices than the declared capacity: reported, not sorted
+        record_error(err_pos, err_flag, t, k);
+        break;
+      }
+      const int64_t idx = __ldg(idxp + k);
+      uint32_t key = sentinel;
+      if (idx >= 0 && idx < nrows) key = uint32_t(rbase + idx);
+      else record_error(err_pos, err_flag, t, k);
+      keys[cb + k] = key;
+      vals[cb + k] = uint32_t(cb + k);
+      bag_of[cb + k] = int32_t(j);
+    }
+    return;
+  }
+  const int64_t s = (int64_t(blockIdx.x) - bag_blocks) * blockDim.x + threadIdx.x;
   if (s >= total_slots) return;
-  // table of slot s: largest t with cap_base[t] <= s
-  int lo = 0, hi = ts.nt - 1;
+  int lo = 0, hi = ts.nt - 1;  // table of slot s: largest t with cap_base[t] <= s
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     if (ts.cap_base[mid] <= s) lo = mid; else hi = mid - 1;
   }
-  const int t = lo;
-  const int64_t k = s - ts.cap_base[t];
-  const int64_t* offs = ts.t[t].offsets;
-  const int64_t nnz = __ldg(offs + num_bags);
-  uint32_t key = sentinel;
-  int32_t bag = 0;
-  if (k < nnz) {
-    const int64_t idx = __ldg(ts.t[t].indices + k);
-    if (idx >= 0 && idx < ts.t[t].num_rows) {
-      key = uint32_t(ts.t[t].row_base + idx);
-    } else {
-      record_error(err_pos, err_flag, t, k);
-    }
-    // bag of position k: largest j with offs[j] <= k (offs nondecreasing)
-    int64_t a = 0, b = num_bags - 1;
-    while (a < b) {
-      const int64_t mid = (a + b + 1) >> 1;
-      if (__ldg(offs + mid) <= k) a = mid; else b = mid - 1;
-    }
-    bag = int32_t(a);
-  }
-  keys[s] = key;
+  const int64_t k = s - ts.cap_base[lo];
+  if (k < __ldg(ts.t[lo].offsets + num_bags)) return;  // live: written by its bag
+  keys[s] = sentinel;
   vals[s] = uint32_t(s);
-  bag_of[s] = bag;
+  bag_of[s] = 0;
 }
 
 __device__ __forceinline__ int table_of_row(const TableSet& ts, uint32_t row) {
@@ -792,9 +802,9 @@ emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
   extern __shared__ float s_rows[];  // [CHUNK][dim]
   __shared__ int64_t s_goff[CHUNK];
   __shared__ float s_w[CHUNK];
-  const uint32_t r = blockIdx.x;
-  if (r >= max_runs || r >= *fa.long_count) return;
   if (!COALESCE && fa.err_flag && *fa.err_flag) return;
+  const uint32_t nruns = min(*fa.long_count, max_runs);
+  for (uint32_t r = blockIdx.x; r < nruns; r += gridDim.x) {
   const uint4 run = fa.long_runs[r];
   const int64_t s0 = run.x, s1 = run.y;
   const uint32_t row = run.z;
@@ -830,6 +840,7 @@ emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
       *w = __fsub_rn(*w, __fmul_rn(fa.lr, acc));
     }
   }
+  }  // runs (grid-stride)
 }
 
 __global__ void err_reset_kernel(int64_t* err_pos, int32_t nt, int32_t* err_flag) {
@@ -905,8 +916,9 @@ seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
   constexpr int U = NV == 1 ? 4 : 2;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPB, col = lane % LPB;
-  const uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  if (seg >= seg_base[max_runs]) return;
+  const uint32_t nseg = seg_base[max_runs];
+  const uint32_t nwarps = gridDim.x * blockDim.x / 32;
+  for (uint32_t seg = (blockIdx.x * blockDim.x + threadIdx.x) / 32; seg < nseg; seg += nwarps) {
   const uint32_t r = seg_run[seg];
   const uint4 run = fa.long_runs[r];
   const uint32_t row = run.z;
@@ -967,15 +979,16 @@ seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
       if (c < nvec) reinterpret_cast<float4*>(partial + int64_t(seg) * dim)[c] = acc[v];
     }
   }
+  }  // segments (grid-stride)
 }
 
 template <bool COALESCE>
 __global__ void __launch_bounds__(128)
 seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
                    const uint32_t* seg_base, const float* partial) {
-  const uint32_t r = blockIdx.x;
-  if (r >= max_runs || r >= *fa.long_count) return;
   if (!COALESCE && fa.err_flag && *fa.err_flag) return;
+  const uint32_t nruns = min(*fa.long_count, max_runs);
+  for (uint32_t r = blockIdx.x; r < nruns; r += gridDim.x) {
   const uint4 run = fa.long_runs[r];
   const uint32_t row = run.z;
   const int t = table_of_row(ts, row);
@@ -993,6 +1006,7 @@ seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
       *w = __fsub_rn(*w, __fmul_rn(fa.lr, v));
     }
   }
+  }  // runs (grid-stride)
 }
 
 // ---------------------------------------------------------------------------
@@ -1051,8 +1065,11 @@ struct WsLayout {
 WsLayout ws_layout(int64_t n, int64_t dim) {
   WsLayout L{};
   size_t sort_bytes = 0, scan_bytes = 0;
-  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr), v(nullptr, nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, k, v, int(n > 0 ? n : 1));
+  // keys_a/vals_a -> keys_b/vals_b (CUB keeps its ping-pong buffers in temp);
+  // sized for the widest key range
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 32);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr,
                                 (uint32_t*)nullptr, int(n > 0 ? n : 1));
   const size_t a = 256, e = align_up(size_t(n > 0 ? n : 1) * 4, a);
@@ -1082,26 +1099,32 @@ int end_bit_for(int64_t total_rows) {
   return b;  // total_rows < 2^b, so sentinel = 2^b - 1 > every real row
 }
 
-// Sort (row, slot) pairs of all tables; returns sorted key/val pointers.
-int sort_pairs(const TableSet& ts, int64_t nb, int64_t total_rows, char* ws,
-               const WsLayout& L, int64_t n, int64_t* err_pos, int32_t* err_flag,
-               uint32_t sentinel, int end_bit, uint32_t** keys_sorted,
-               uint32_t** vals_sorted, cudaStream_t s) {
+// Sort (row, slot) pairs of all tables into keys_b / vals_b of the workspace.
+int sort_pairs(const TableSet& ts, int64_t nb, char* ws, const WsLayout& L, int64_t n,
+               int64_t* err_pos, int32_t* err_flag, uint32_t sentinel, int end_bit,
+               cudaStream_t s) {
   uint32_t* ka = reinterpret_cast<uint32_t*>(ws + L.keys_a);
   uint32_t* kb = reinterpret_cast<uint32_t*>(ws + L.keys_b);
   uint32_t* va = reinterpret_cast<uint32_t*>(ws + L.vals_a);
   uint32_t* vb = reinterpret_cast<uint32_t*>(ws + L.vals_b);
   int32_t* bag = reinterpret_cast<int32_t*>(ws + L.bag);
-  emb_keys_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(
-      ts, nb, n, sentinel, ka, va, bag, err_pos, err_flag);
-  if (int rc = check_launch("emb_keys_kernel")) return rc;
-  cub::DoubleBuffer<uint32_t> kbuf(ka, kb), vbuf(va, vb);
+  {
+    // lanes per bag from the capacity-average pooling factor
+    const double avg = double(n) / double(nb * ts.nt > 0 ? nb * ts.nt : 1);
+    const int lpb = avg >= 12.0 ? 32 : (avg >= 3.0 ? 8 : 1);
+    const int64_t bag_blocks = ceil_div(nb * ts.nt * lpb, 256);
+    const unsigned grid = unsigned(bag_blocks + ceil_div(n, 256));
+    if (lpb == 32)
+      emb_keys_kernel<32><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+    else if (lpb == 8)
+      emb_keys_kernel<8><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+    else
+      emb_keys_kernel<1><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+    if (int rc = check_launch("emb_keys_kernel")) return rc;
+  }
   size_t tb = L.temp_bytes;
-  DLRM_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, tb, kbuf, vbuf, int(n),
-                                            0, end_bit, s));
+  DLRM_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, tb, ka, kb, va, vb, int(n), 0, end_bit, s));
   count_launch(end_bit / 8 + 2);
-  *keys_sorted = kbuf.Current();
-  *vals_sorted = vbuf.Current();
   return 0;
 }
 
@@ -1133,7 +1156,9 @@ int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
     float* part = reinterpret_cast<float*>(ws + L.part);
     seg_plan_kernel<<<1, 1024, 0, s>>>(fa, L.max_long, L.max_segs, segb, segr);
     if (int rc = check_launch("seg_plan_kernel")) return rc;
-    const unsigned fold_blocks = unsigned(ceil_div(int64_t(L.max_segs) * 32, 256));
+    // persistent grids: the long-run path costs little when there are none
+    const unsigned fold_blocks =
+        unsigned(std::min<int64_t>(ceil_div(int64_t(L.max_segs) * 32, 256), 8 * kNumSMs));
     auto go = [&](auto kern) -> int {
       kern<<<fold_blocks, 256, 0, s>>>(fa, ts, dim, L.max_long, segb, segr, part);
       return check_launch("seg_fold_kernel");
@@ -1148,14 +1173,15 @@ int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
     else if (nvec <= 64) rc = go(seg_fold_kernel<32, 2>);
     else rc = go(seg_fold_kernel<32, 4>);
     if (rc) return rc;
-    seg_combine_kernel<CO><<<L.max_long, 128, 0, s>>>(fa, ts, dim, L.max_long, segb, part);
+    seg_combine_kernel<CO><<<unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 128, 0, s>>>(
+        fa, ts, dim, L.max_long, segb, part);
     return check_launch("seg_combine_kernel");
   }
   const size_t smem = size_t(64) * dim * 4;
   auto k = emb_long_run_kernel<CO>;
   if (smem > 48 * 1024)
     DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k<<<L.max_long, 256, smem, s>>>(fa, ts, dim, L.max_long);
+  k<<<unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 256, smem, s>>>(fa, ts, dim, L.max_long);
   return check_launch("emb_long_run_kernel");
 }
 
@@ -1295,42 +1321,65 @@ extern "C" size_t dlrm_emb_bwd_workspace_size(int64_t total_capacity,
   return ws_layout(total_capacity, dim).total;
 }
 
-extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
-                                const dlrm_table_desc* tables, int32_t nt,
-                                int64_t num_bags, const float* grad,
-                                int64_t grad_stride, float lr,
-                                const int32_t* err_flag, int64_t total_rows,
-                                void* workspace, size_t ws_bytes,
-                                dlrm_stream_t stream) {
+namespace dlrm {
+namespace {
+struct BwdPlan {
+  int64_t n;
+  WsLayout L;
+  int end_bit;
+  uint32_t sentinel;
+};
+
+int bwd_plan(TableSet& ts, const dlrm_table_desc* tables, int32_t nt, int64_t dim,
+             int64_t total_rows, void* workspace, size_t ws_bytes, BwdPlan* p) {
   DLRM_REQUIRE(dim >= 1 && dim <= 512, "embedding dim must be in [1, 512]");
   DLRM_REQUIRE(total_rows >= 1 && total_rows < (int64_t(1) << 31),
                "total rows must be in [1, 2^31)");
-  static thread_local TableSet ts;
   if (int rc = fill_tableset(ts, tables, nt)) return rc;
-  const int64_t n = ts.cap_base[nt];
-  DLRM_REQUIRE(n < (int64_t(1) << 31), "total capacity must be < 2^31");
-  if (n == 0 || num_bags == 0) return 0;
-  const WsLayout L = ws_layout(n, dim);
-  DLRM_REQUIRE(workspace != nullptr && ws_bytes >= L.total,
+  p->n = ts.cap_base[nt];
+  DLRM_REQUIRE(p->n < (int64_t(1) << 31), "total capacity must be < 2^31");
+  p->L = ws_layout(p->n, dim);
+  DLRM_REQUIRE(p->n == 0 || (workspace != nullptr && ws_bytes >= p->L.total),
                "embedding backward workspace too small");
-  cudaStream_t s = as_stream(stream);
-  const int end_bit = end_bit_for(total_rows);
-  const uint32_t sentinel = uint32_t((int64_t(1) << end_bit) - 1);
+  p->end_bit = end_bit_for(total_rows);
+  p->sentinel = uint32_t((int64_t(1) << p->end_bit) - 1);
+  return 0;
+}
+}  // namespace
+}  // namespace dlrm
+
+extern "C" int dlrm_emb_bwd_prepare(int64_t dim, const dlrm_table_desc* tables, int32_t nt,
+                                    int64_t num_bags, int64_t total_rows, void* workspace,
+                                    size_t ws_bytes, dlrm_stream_t stream) {
+  static thread_local TableSet ts;
+  BwdPlan p;
+  if (int rc = bwd_plan(ts, tables, nt, dim, total_rows, workspace, ws_bytes, &p)) return rc;
+  if (p.n == 0 || num_bags == 0) return 0;
   char* ws = static_cast<char*>(workspace);
-  uint32_t *ks, *vs;
-  // errors were recorded by the forward; the key pass re-records into a
-  // scratch area so the caller's err_pos is unaffected here.
-  int64_t* scratch_err = reinterpret_cast<int64_t*>(ws + L.err);
-  int32_t* scratch_flag = reinterpret_cast<int32_t*>(ws + L.err + DLRM_MAX_TABLES * 8);
-  if (int rc = sort_pairs(ts, num_bags, total_rows, ws, L, n, scratch_err,
-                          scratch_flag, sentinel, end_bit, &ks, &vs, s))
-    return rc;
+  // index errors were recorded by the forward; the key pass re-records into
+  // a scratch area so the caller's err_pos is unaffected here
+  int64_t* scratch_err = reinterpret_cast<int64_t*>(ws + p.L.err);
+  int32_t* scratch_flag = reinterpret_cast<int32_t*>(ws + p.L.err + DLRM_MAX_TABLES * 8);
+  return sort_pairs(ts, num_bags, ws, p.L, p.n, scratch_err, scratch_flag, p.sentinel,
+                    p.end_bit, as_stream(stream));
+}
+
+extern "C" int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                                      int32_t nt, int64_t num_bags, const float* grad,
+                                      int64_t grad_stride, float lr, const int32_t* err_flag,
+                                      int64_t total_rows, void* workspace, size_t ws_bytes,
+                                      dlrm_stream_t stream) {
+  static thread_local TableSet ts;
+  BwdPlan p;
+  if (int rc = bwd_plan(ts, tables, nt, dim, total_rows, workspace, ws_bytes, &p)) return rc;
+  if (p.n == 0 || num_bags == 0) return 0;
+  char* ws = static_cast<char*>(workspace);
   FoldArgs fa{};
-  fa.keys = ks;
-  fa.vals = vs;
-  fa.bag_of = reinterpret_cast<const int32_t*>(ws + L.bag);
-  fa.n = n;
-  fa.sentinel = sentinel;
+  fa.keys = reinterpret_cast<const uint32_t*>(ws + p.L.keys_b);
+  fa.vals = reinterpret_cast<const uint32_t*>(ws + p.L.vals_b);
+  fa.bag_of = reinterpret_cast<const int32_t*>(ws + p.L.bag);
+  fa.n = p.n;
+  fa.sentinel = p.sentinel;
   fa.grad = grad;
   fa.grad_stride = grad_stride;
   fa.W = W_all;
@@ -1339,7 +1388,21 @@ extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
   bool v4 = vec4_ok(dim, W_all, grad_stride, 0) &&
             (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
   for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
-  return run_fold<false>(fa, ts, dim, v4, ws, L, s);
+  return run_fold<false>(fa, ts, dim, v4, ws, p.L, as_stream(stream));
+}
+
+extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
+                                const dlrm_table_desc* tables, int32_t nt,
+                                int64_t num_bags, const float* grad,
+                                int64_t grad_stride, float lr,
+                                const int32_t* err_flag, int64_t total_rows,
+                                void* workspace, size_t ws_bytes,
+                                dlrm_stream_t stream) {
+  if (int rc = dlrm_emb_bwd_prepare(dim, tables, nt, num_bags, total_rows, workspace,
+                                    ws_bytes, stream))
+    return rc;
+  return dlrm_emb_bwd_apply_sgd(W_all, dim, tables, nt, num_bags, grad, grad_stride, lr,
+                                err_flag, total_rows, workspace, ws_bytes, stream);
 }
 
 extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
@@ -1370,10 +1433,10 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
   const int end_bit = end_bit_for(total_rows);
   const uint32_t sentinel = uint32_t((int64_t(1) << end_bit) - 1);
   char* ws = static_cast<char*>(workspace);
-  uint32_t *ks, *vs;
-  if (int rc = sort_pairs(ts, num_bags, total_rows, ws, L, n, err_pos,
-                          err_flag, sentinel, end_bit, &ks, &vs, s))
+  if (int rc = sort_pairs(ts, num_bags, ws, L, n, err_pos, err_flag, sentinel, end_bit, s))
     return rc;
+  const uint32_t* ks = reinterpret_cast<const uint32_t*>(ws + L.keys_b);
+  const uint32_t* vs = reinterpret_cast<const uint32_t*>(ws + L.vals_b);
   uint32_t* flags = reinterpret_cast<uint32_t*>(ws + L.flags);
   uint32_t* uid = reinterpret_cast<uint32_t*>(ws + L.uid);
   run_flags_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(ks, n, sentinel, flags);

@@ -29,6 +29,7 @@ update), and the host raises LookupIndexError when it reads the step result.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -160,6 +161,11 @@ class StepEngine:
         self.stats = torch.zeros(2, **f32)
         self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # the index-only half of the sparse backward (keys + radix sort) runs
+        # on a side stream, overlapped with the dense part of the step;
+        # DLRM_EMB_PREP = "start" | "after_fwd" (default) | "inline"
+        self.prep_at = os.environ.get("DLRM_EMB_PREP", "after_fwd")
+        self.side = torch.cuda.Stream(device=dev)
 
         for v in self.input_sets:
             v["descs"] = self._make_descs(v)
@@ -286,12 +292,27 @@ class StepEngine:
         """Issue the whole step on ``stream`` (default: current stream).
         ``mark(stage)`` (profiling only) is called before each stage."""
         mark = mark or (lambda name: None)
-        s = _lib.stream_handle(stream)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        s = _lib.stream_handle(main)
+        prep_done = None
+
+        def fork_prepare():
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.side.wait_event(ev)
+            call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
+                 P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(self.side))
+            done = torch.cuda.Event()
+            done.record(self.side)
+            return done
+
         L, call, P = self.layers, _lib.call, _lib.ptr
         B, d, nf, lr = self.B, self.d, self.nf, self.lr
         relu = _lib.ACT["relu"]
         ef = P(self.err_flag)
         call("dlrm_err_reset", P(self.err_pos), self.T, ef, s)
+        if self.prep_at == "start":
+            prep_done = fork_prepare()
 
         # bottom MLP forward; the last layer writes feature 0 of Z
         mark("bottom_mlp_fwd")
@@ -308,6 +329,8 @@ class StepEngine:
         mark("embedding_fwd")
         call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
              P(self.Z), nf * d, P(self.err_pos), ef, s)
+        if self.prep_at == "after_fwd":
+            prep_done = fork_prepare()
         # interaction -> R
         mark("interaction_fwd")
         call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
@@ -371,7 +394,12 @@ class StepEngine:
                  P(l.bias), lr, ef, ws, wsb, s)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
-        call("dlrm_emb_bwd_sgd", P(self.W_all), d, self._descs_p, self.T, B,
+        if prep_done is None:
+            call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
+                 P(self.emb_ws), self.emb_ws_bytes, s)
+        else:
+            main.wait_event(prep_done)
+        call("dlrm_emb_bwd_apply_sgd", P(self.W_all), d, self._descs_p, self.T, B,
              P(self.gZ), nf * d, lr, ef, self.total_rows, P(self.emb_ws),
              self.emb_ws_bytes, s)
 
