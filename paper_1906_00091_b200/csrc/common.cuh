@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "dlrm_b200.h"
 
@@ -54,6 +55,43 @@ inline int check_launch(const char* what) {
   } while (0)
 
 constexpr int kNumSMs = 148;
+
+// Programmatic dependent launch (PDL).  Every kernel of the library is
+// launched with programmatic stream serialization allowed, and starts with
+// pdl_entry(): it lets the NEXT kernel in the stream be scheduled as soon as
+// all of this grid's CTAs are resident (griddepcontrol.launch_dependents),
+// then waits for the PREVIOUS grid to complete and flush its memory
+// (griddepcontrol.wait) before touching any data.  The next kernel's launch
+// latency and prologue therefore overlap this kernel's tail.  Kernels whose
+// prologue does not read dependent data (tc_gemm: barrier init, TMEM alloc,
+// tensor-map prefetch) call pdl_trigger() / pdl_wait() separately.
+// DLRM_PDL=0 in the environment launches without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_entry() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? DLRM_EMB_MINB1 : 2)
 emb_fwd_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
                int64_t num_bags, float* __restrict__ out, int64_t out_stride,
                int64_t* err_pos, int32_t* err_flag) {
+  pdl_entry();
   using V = typename VecT<VEC>::T;
   constexpr int U = NV == 1 ? DLRM_EMB_U1 : (NV == 2 ? 4 : 2);  // rows in flight per lane
   const int lane = threadIdx.x & (LPB - 1);
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(256, 4)
 emb_fwd_warp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
                     int64_t num_bags, float* __restrict__ out, int64_t out_stride,
                     int64_t* err_pos, int32_t* err_flag) {
+  pdl_entry();
   constexpr int RPI = 32 / LPB;
   constexpr int U = RPI >= 4 ? DLRM_EMBW_U / 2 : DLRM_EMBW_U;
   const int lane = threadIdx.x & 31;
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1)
 emb_fwd_stream_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int64_t nb,
                       float* __restrict__ out, int64_t out_stride, int64_t* err_pos,
                       int32_t* err_flag) {
+  pdl_entry();
   constexpr int SLOT = CH * NVM;                  // float4 per ring slot
   constexpr int PER_LANE = (SLOT + 31) / 32;      // 16-byte copies per lane per chunk
   constexpr int NL = NVM >= 32 ? NVM / 32 : 1;    // float4 columns per lane
@@ -523,6 +526,7 @@ emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots, int64_t bag_
                 uint32_t sentinel, uint32_t* __restrict__ keys,
                 uint32_t* __restrict__ vals, int32_t* __restrict__ bag_of,
                 int64_t* err_pos, int32_t* err_flag) {
+  pdl_entry();
   if (blockIdx.x < bag_blocks) {
     const int64_t gb = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / LPB;
     const int lane = threadIdx.x % LPB;
@@ -575,6 +579,7 @@ __device__ __forceinline__ int table_of_row(const TableSet& ts, uint32_t row) {
 // Run-start flags for the coalesce path.
 __global__ void run_flags_kernel(const uint32_t* __restrict__ keys, int64_t n,
                                  uint32_t sentinel, uint32_t* __restrict__ flags) {
+  pdl_entry();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t k = keys[i];
@@ -583,6 +588,7 @@ __global__ void run_flags_kernel(const uint32_t* __restrict__ keys, int64_t n,
 
 __global__ void count_unique_kernel(const uint32_t* uid, const uint32_t* flags,
                                     int64_t n, int64_t* num_unique) {
+  pdl_entry();
   if (threadIdx.x == 0 && blockIdx.x == 0)
     *num_unique = n ? int64_t(uid[n - 1]) + int64_t(flags[n - 1]) : 0;
 }
@@ -620,6 +626,7 @@ constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
 template <int VEC, int LPB, int NV, bool COALESCE>
 __global__ void __launch_bounds__(fold_groups<LPB>() * LPB)
 emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
+  pdl_entry();
   using V = typename VecT<VEC>::T;
   constexpr int CH = 32;  // sorted slots staged per batch
   constexpr int U = COALESCE ? 8 : 4;  // gradient rows in flight per lane
@@ -798,6 +805,7 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
 template <bool COALESCE>
 __global__ void __launch_bounds__(256)
 emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
+  pdl_entry();
   constexpr int CHUNK = 64;
   extern __shared__ float s_rows[];  // [CHUNK][dim]
   __shared__ int64_t s_goff[CHUNK];
@@ -844,6 +852,7 @@ emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
 }
 
 __global__ void err_reset_kernel(int64_t* err_pos, int32_t nt, int32_t* err_flag) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nt) err_pos[i] = INT64_MAX;
   if (i == 0 && err_flag) *err_flag = 0;
@@ -854,6 +863,7 @@ __global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
                                 const int64_t* __restrict__ rows,
                                 const float* __restrict__ values, int64_t n,
                                 float lr) {
+  pdl_entry();
   using V = typename VecT<VEC>::T;
   const int64_t nvec = dim / VEC;
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -879,6 +889,7 @@ constexpr int kSeg = 256;
 
 __global__ void seg_plan_kernel(FoldArgs fa, uint32_t max_runs, uint32_t max_segs,
                                 uint32_t* seg_base, uint32_t* seg_run) {
+  pdl_entry();
   __shared__ uint32_t s_tot[1024];
   const uint32_t nruns = min(*fa.long_count, max_runs);
   // per-thread contiguous run range -> local counts -> block scan
@@ -912,6 +923,7 @@ template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
 seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
                 const uint32_t* seg_base, const uint32_t* seg_run, float* partial) {
+  pdl_entry();
   constexpr int RPI = 32 / LPB;
   constexpr int U = NV == 1 ? 4 : 2;
   const int lane = threadIdx.x & 31;
@@ -986,6 +998,7 @@ template <bool COALESCE>
 __global__ void __launch_bounds__(128)
 seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
                    const uint32_t* seg_base, const float* partial) {
+  pdl_entry();
   if (!COALESCE && fa.err_flag && *fa.err_flag) return;
   const uint32_t nruns = min(*fa.long_count, max_runs);
   for (uint32_t r = blockIdx.x; r < nruns; r += gridDim.x) {
@@ -1038,8 +1051,7 @@ void launch_fwd(const float* W, int64_t dim, const TableSet& ts, int64_t nb,
                 float* out, int64_t stride, int64_t* ep, int32_t* ef,
                 cudaStream_t s) {
   const int64_t threads = nb * ts.nt * LPB;
-  emb_fwd_kernel<VEC, LPB, NV><<<unsigned(ceil_div(threads, 256)), 256, 0, s>>>(
-      W, dim, ts, nb, out, stride, ep, ef);
+  launch(emb_fwd_kernel<VEC, LPB, NV>, unsigned(ceil_div(threads, 256)), 256, 0, s, W, dim, ts, nb, out, stride, ep, ef);
 }
 
 template <int NVM, int CH, int S, int WARPS>
@@ -1052,7 +1064,7 @@ int launch_stream(const float* W, int64_t dim, const TableSet& ts, int64_t nb, f
     DLRM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  kern<<<kNumSMs, 32 * WARPS, smem, s>>>(W, dim, ts, nb, out, stride, ep, ef);
+  launch(kern, kNumSMs, 32 * WARPS, smem, s, W, dim, ts, nb, out, stride, ep, ef);
   return check_launch("emb_fwd_stream_kernel");
 }
 
@@ -1115,11 +1127,11 @@ int sort_pairs(const TableSet& ts, int64_t nb, char* ws, const WsLayout& L, int6
     const int64_t bag_blocks = ceil_div(nb * ts.nt * lpb, 256);
     const unsigned grid = unsigned(bag_blocks + ceil_div(n, 256));
     if (lpb == 32)
-      emb_keys_kernel<32><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<32>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
     else if (lpb == 8)
-      emb_keys_kernel<8><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<8>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
     else
-      emb_keys_kernel<1><<<grid, 256, 0, s>>>(ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<1>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
     if (int rc = check_launch("emb_keys_kernel")) return rc;
   }
   size_t tb = L.temp_bytes;
@@ -1133,8 +1145,7 @@ void launch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim,
                  cudaStream_t s) {
   constexpr int GROUPS = fold_groups<LPB>();
   const int64_t chunks = ceil_div(fa.n, 32);
-  emb_fold_kernel<VEC, LPB, NV, CO>
-      <<<unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, 0, s>>>(fa, ts, dim);
+  launch(emb_fold_kernel<VEC, LPB, NV, CO>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, 0, s, fa, ts, dim);
 }
 
 template <bool CO>
@@ -1154,13 +1165,13 @@ int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
     uint32_t* segb = reinterpret_cast<uint32_t*>(ws + L.segb);
     uint32_t* segr = reinterpret_cast<uint32_t*>(ws + L.segr);
     float* part = reinterpret_cast<float*>(ws + L.part);
-    seg_plan_kernel<<<1, 1024, 0, s>>>(fa, L.max_long, L.max_segs, segb, segr);
+    launch(seg_plan_kernel, 1, 1024, 0, s, fa, L.max_long, L.max_segs, segb, segr);
     if (int rc = check_launch("seg_plan_kernel")) return rc;
     // persistent grids: the long-run path costs little when there are none
     const unsigned fold_blocks =
         unsigned(std::min<int64_t>(ceil_div(int64_t(L.max_segs) * 32, 256), 8 * kNumSMs));
     auto go = [&](auto kern) -> int {
-      kern<<<fold_blocks, 256, 0, s>>>(fa, ts, dim, L.max_long, segb, segr, part);
+      launch(kern, fold_blocks, 256, 0, s, fa, ts, dim, L.max_long, segb, segr, part);
       return check_launch("seg_fold_kernel");
     };
     int rc;
@@ -1173,15 +1184,14 @@ int run_fold(FoldArgs fa, const TableSet& ts, int64_t dim, bool v4, char* ws,
     else if (nvec <= 64) rc = go(seg_fold_kernel<32, 2>);
     else rc = go(seg_fold_kernel<32, 4>);
     if (rc) return rc;
-    seg_combine_kernel<CO><<<unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 128, 0, s>>>(
-        fa, ts, dim, L.max_long, segb, part);
+    launch(seg_combine_kernel<CO>, unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 128, 0, s, fa, ts, dim, L.max_long, segb, part);
     return check_launch("seg_combine_kernel");
   }
   const size_t smem = size_t(64) * dim * 4;
   auto k = emb_long_run_kernel<CO>;
   if (smem > 48 * 1024)
     DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k<<<unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 256, smem, s>>>(fa, ts, dim, L.max_long);
+  launch(k, unsigned(std::min<int64_t>(L.max_long, 4 * kNumSMs)), 256, smem, s, fa, ts, dim, L.max_long);
   return check_launch("emb_long_run_kernel");
 }
 
@@ -1217,8 +1227,8 @@ using namespace dlrm;
 extern "C" int dlrm_err_reset(int64_t* err_pos, int32_t nt, int32_t* err_flag,
                               dlrm_stream_t stream) {
   DLRM_REQUIRE(err_pos != nullptr && nt >= 0, "bad error buffers");
-  err_reset_kernel<<<unsigned(ceil_div(nt > 0 ? nt : 1, 128)), 128, 0,
-                     as_stream(stream)>>>(err_pos, nt, err_flag);
+  launch(err_reset_kernel, unsigned(ceil_div(nt > 0 ? nt : 1, 128)), 128, 0,
+                     as_stream(stream), err_pos, nt, err_flag);
   return check_launch("err_reset_kernel");
 }
 
@@ -1289,10 +1299,10 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
     if (want > 4 * kNumSMs) want = 4 * kNumSMs;  // persistent: 4 blocks per SM
     const unsigned blocks = unsigned(want);
     switch (nv0) {
-      case 4: emb_fwd_warp_kernel<4><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
-      case 8: emb_fwd_warp_kernel<8><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
-      case 16: emb_fwd_warp_kernel<16><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
-      default: emb_fwd_warp_kernel<32><<<blocks, 256, 0, s>>>(W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      case 4: launch(emb_fwd_warp_kernel<4>, blocks, 256, 0, s, W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      case 8: launch(emb_fwd_warp_kernel<8>, blocks, 256, 0, s, W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      case 16: launch(emb_fwd_warp_kernel<16>, blocks, 256, 0, s, W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
+      default: launch(emb_fwd_warp_kernel<32>, blocks, 256, 0, s, W_all, dim, ts, num_bags, out, out_stride, err_pos, err_flag); break;
     }
     return check_launch("emb_fwd_warp_kernel");
   }
@@ -1439,12 +1449,12 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
   const uint32_t* vs = reinterpret_cast<const uint32_t*>(ws + L.vals_b);
   uint32_t* flags = reinterpret_cast<uint32_t*>(ws + L.flags);
   uint32_t* uid = reinterpret_cast<uint32_t*>(ws + L.uid);
-  run_flags_kernel<<<unsigned(ceil_div(n, 256)), 256, 0, s>>>(ks, n, sentinel, flags);
+  launch(run_flags_kernel, unsigned(ceil_div(n, 256)), 256, 0, s, ks, n, sentinel, flags);
   if (int rc = check_launch("run_flags_kernel")) return rc;
   size_t tb = L.temp_bytes;
   DLRM_CUDA(cub::DeviceScan::ExclusiveSum(ws + L.temp, tb, flags, uid, int(n), s));
   count_launch();
-  count_unique_kernel<<<1, 32, 0, s>>>(uid, flags, n, num_unique);
+  launch(count_unique_kernel, 1, 32, 0, s, uid, flags, n, num_unique);
   if (int rc = check_launch("count_unique_kernel")) return rc;
   FoldArgs fa{};
   fa.keys = ks;
@@ -1472,10 +1482,10 @@ extern "C" int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
                   (reinterpret_cast<uintptr_t>(values) % 16) == 0;
   if (v4) {
     const int64_t e = n * (dim / 4);
-    sgd_rows_kernel<4><<<unsigned(ceil_div(e, 256)), 256, 0, s>>>(W, dim, rows, values, n, lr);
+    launch(sgd_rows_kernel<4>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, lr);
   } else {
     const int64_t e = n * dim;
-    sgd_rows_kernel<1><<<unsigned(ceil_div(e, 256)), 256, 0, s>>>(W, dim, rows, values, n, lr);
+    launch(sgd_rows_kernel<1>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, lr);
   }
   return check_launch("sgd_rows_kernel");
 }

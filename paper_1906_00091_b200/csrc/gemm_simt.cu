@@ -44,6 +44,7 @@ __device__ __forceinline__ void load_tile(float (*dst)[ROWS + 4], const Operand&
 __global__ void __launch_bounds__(256)
 gemm_simt_kernel(Operand A, Operand B, int64_t M, int64_t N, int64_t K,
                  int64_t k_chunk, GemmEpilogue ep) {
+  pdl_entry();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(256)
 colreduce_partial_kernel(const float* __restrict__ X, int64_t ldx,
                          const float* __restrict__ scale, int64_t R, int64_t C,
                          int64_t rows_per_chunk, float* __restrict__ partial) {
+  pdl_entry();
   __shared__ float red[8][33];
   const int cx = threadIdx.x % 32, ry = threadIdx.x / 32;
   const int64_t c = int64_t(blockIdx.x) * 32 + cx;
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(256)
 colreduce_partial4_kernel(const float* __restrict__ X, int64_t ldx,
                           const float* __restrict__ scale, int64_t R, int64_t C,
                           int64_t rows_per_chunk, float* __restrict__ partial) {
+  pdl_entry();
   __shared__ float4 red[8][32];
   const int cx = threadIdx.x % 32, ry = threadIdx.x / 32;
   const int64_t c4 = int64_t(blockIdx.x) * 32 + cx;  // float4 column index
@@ -174,6 +177,7 @@ __global__ void colreduce_final_kernel(const float* __restrict__ partial,
                                        int64_t C, int splits, float* out,
                                        float* upd, float lr,
                                        const int32_t* err_flag) {
+  pdl_entry();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= C) return;
   float s = partial[c];
@@ -187,6 +191,7 @@ __global__ void splitk_final4_kernel(const float* __restrict__ part, int64_t M,
                                      int64_t N, int splits, float* dW,
                                      int64_t lddw, float* Wu, int64_t ldw,
                                      float lr, const int32_t* err_flag) {
+  pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // float4 index
   const int64_t n4 = N / 4;
   if (e >= M * n4) return;
@@ -217,6 +222,7 @@ __global__ void splitk_final_kernel(const float* __restrict__ part, int64_t M,
                                     int64_t N, int splits, float* dW,
                                     int64_t lddw, float* Wu, int64_t ldw,
                                     float lr, const int32_t* err_flag) {
+  pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= M * N) return;
   const int64_t m = e / N, n = e - m * N;
@@ -238,7 +244,7 @@ int gemm_simt(const float* a, int64_t a_outer, int64_t a_k, const float* b,
   const int64_t z = K == 0 ? 1 : ceil_div(K, k_chunk);
   if (used_splits) *used_splits = int(z);
   dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(M, BM)), unsigned(z));
-  gemm_simt_kernel<<<grid, 256, 0, s>>>(A, B, M, N, K, k_chunk, ep);
+  launch(gemm_simt_kernel, grid, 256, 0, s, A, B, M, N, K, k_chunk, ep);
   return check_launch("gemm_simt_kernel");
 }
 
@@ -258,15 +264,12 @@ int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
   const int64_t rpc = R == 0 ? 1 : ceil_div(R, splits);
   splits = R == 0 ? 1 : ceil_div(R, rpc);
   if (vec) {
-    colreduce_partial4_kernel<<<dim3(unsigned(ceil_div(C, 128)), unsigned(splits)), 256, 0, s>>>(
-        X, ldx, scale, R, C, rpc, ws);
+    launch(colreduce_partial4_kernel, dim3(unsigned(ceil_div(C, 128)), unsigned(splits)), 256, 0, s, X, ldx, scale, R, C, rpc, ws);
   } else {
-    colreduce_partial_kernel<<<dim3(unsigned(ceil_div(C, 32)), unsigned(splits)), 256, 0, s>>>(
-        X, ldx, scale, R, C, rpc, ws);
+    launch(colreduce_partial_kernel, dim3(unsigned(ceil_div(C, 32)), unsigned(splits)), 256, 0, s, X, ldx, scale, R, C, rpc, ws);
   }
   if (int rc = check_launch("colreduce_partial_kernel")) return rc;
-  colreduce_final_kernel<<<unsigned(ceil_div(C, 256)), 256, 0, s>>>(
-      ws, C, int(splits), out, upd, lr, err_flag);
+  launch(colreduce_final_kernel, unsigned(ceil_div(C, 256)), 256, 0, s, ws, C, int(splits), out, upd, lr, err_flag);
   return check_launch("colreduce_final_kernel");
 }
 
@@ -277,11 +280,9 @@ int splitk_reduce(const float* part, int64_t M, int64_t N, int splits, float* dW
                   (reinterpret_cast<uintptr_t>(part) & 15) == 0 &&
                   (!Wu || (reinterpret_cast<uintptr_t>(Wu) & 15) == 0);
   if (v4) {
-    splitk_final4_kernel<<<unsigned(ceil_div(M * N / 4, 256)), 256, 0, s>>>(
-        part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+    launch(splitk_final4_kernel, unsigned(ceil_div(M * N / 4, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
   } else {
-    splitk_final_kernel<<<unsigned(ceil_div(M * N, 256)), 256, 0, s>>>(
-        part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+    launch(splitk_final_kernel, unsigned(ceil_div(M * N, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
   }
   return check_launch("splitk_final_kernel");
 }

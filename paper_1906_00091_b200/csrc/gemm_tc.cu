@@ -208,6 +208,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t* acc_full = bars + 2 * TSTAGES + 2 * LSTAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
+  pdl_trigger();  // prologue below touches no data of the previous kernel
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
   const int kt0 = blockIdx.z * args.k_tiles_per_split;
@@ -239,6 +240,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // operands / epilogue inputs come from earlier kernels
 
   if (warp == 0) {
     // ---- TMA producer: raw fp32 tiles (the tensor core reads them as the
@@ -466,7 +468,7 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
     configured = true;
   }
   dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)), unsigned(splits));
-  k<<<grid, THREADS, sm, s>>>(a, b, args);
+  launch(k, grid, THREADS, sm, s, a, b, args);
   return check_launch("tc_gemm_kernel");
 }
 
@@ -645,6 +647,7 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, sp));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
   if (int rc = launch<true, true>(ma, mb, a, K, bn, used, s)) return rc;
+  if (getenv("DLRM_EXP_NO_SPLITK")) return 0;
   return splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s);
 }
 

@@ -29,6 +29,7 @@ bce_head_kernel(const float* __restrict__ A, int64_t lda,
                 int64_t M, int64_t K, const float* __restrict__ y,
                 float n_total, float* logits, float* prob, float* grad_z,
                 float* per_sample, float2* part) {
+  pdl_entry();
   __shared__ float s_loss[8], s_ok[8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m = int64_t(blockIdx.x) * 8 + warp;
@@ -74,6 +75,7 @@ bce_head_kernel(const float* __restrict__ A, int64_t lda,
 
 __global__ void bce_final_kernel(const float2* __restrict__ part, int64_t nb,
                                  float* stats) {
+  pdl_entry();
   __shared__ float s_l[256], s_c[256];
   float l = 0.f, c = 0.f;
   for (int64_t i = threadIdx.x; i < nb; i += 256) { l += part[i].x; c += part[i].y; }
@@ -96,6 +98,7 @@ __global__ void head_dA_kernel(const float* __restrict__ A, int64_t lda,
                                const float* __restrict__ g, int64_t M,
                                int64_t K, float* __restrict__ dA, int64_t ldda,
                                int relu_mask) {
+  pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= M * K) return;
   const int64_t m = e / K, k = e - m * K;
@@ -107,6 +110,7 @@ __global__ void relu_grad_kernel(const float* __restrict__ g, int64_t ldg,
                                  const float* __restrict__ a, int64_t lda,
                                  float* __restrict__ out, int64_t ldo, int64_t M,
                                  int64_t N) {
+  pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= M * N) return;
   const int64_t m = e / N, n = e - m * N;
@@ -123,8 +127,7 @@ extern "C" int dlrm_relu_grad(const float* g, int64_t ldg, const float* act,
                               int64_t N, dlrm_stream_t stream) {
   DLRM_REQUIRE(M >= 0 && N >= 1, "bad relu_grad shape");
   if (M == 0) return 0;
-  relu_grad_kernel<<<unsigned(ceil_div(M * N, 256)), 256, 0, as_stream(stream)>>>(
-      g, ldg, act, lda, out, ldo, M, N);
+  launch(relu_grad_kernel, unsigned(ceil_div(M * N, 256)), 256, 0, as_stream(stream), g, ldg, act, lda, out, ldo, M, N);
   return check_launch("relu_grad_kernel");
 }
 
@@ -145,10 +148,10 @@ extern "C" int dlrm_bce_head(const float* A, int64_t lda, const float* w,
   cudaStream_t s = as_stream(stream);
   const int64_t nb = ceil_div(M, 8);
   float2* part = static_cast<float2*>(workspace);
-  bce_head_kernel<<<unsigned(nb), 256, 0, s>>>(A, lda, w, b, M, K, y, n_total,
+  launch(bce_head_kernel, unsigned(nb), 256, 0, s, A, lda, w, b, M, K, y, n_total,
                                                  logits, prob, grad_z, per_sample, part);
   if (int rc = check_launch("bce_head_kernel")) return rc;
-  bce_final_kernel<<<1, 256, 0, s>>>(part, nb, stats);
+  launch(bce_final_kernel, 1, 256, 0, s, part, nb, stats);
   return check_launch("bce_final_kernel");
 }
 
@@ -162,7 +165,7 @@ extern "C" int dlrm_head_bwd(const float* A, int64_t lda, const float* w,
   DLRM_REQUIRE(M >= 1 && K >= 1 && lda >= K, "bad head_bwd arguments");
   cudaStream_t s = as_stream(stream);
   if (dA) {
-    head_dA_kernel<<<unsigned(ceil_div(M * K, 256)), 256, 0, s>>>(A, lda, w, g, M,
+    launch(head_dA_kernel, unsigned(ceil_div(M * K, 256)), 256, 0, s, A, lda, w, g, M,
                                                                   K, dA, ldda, relu_mask);
     if (int rc = check_launch("head_dA_kernel")) return rc;
   }

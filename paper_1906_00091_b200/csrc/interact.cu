@@ -27,6 +27,7 @@ template <bool V4>
 __global__ void __launch_bounds__(256)
 interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
                     float* __restrict__ out, int64_t ld_out, int64_t pad_to) {
+  pdl_entry();
   extern __shared__ float4 smem4[];
   float* z = reinterpret_cast<float*>(smem4);
   const int pitch = int(dim) + 4;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256)
 interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
                     int64_t batch, int S, const float* __restrict__ gout,
                     int64_t ld_gout, int mask_f0) {
+  pdl_entry();
   extern __shared__ float4 smem4[];
   float* z = reinterpret_cast<float*>(smem4);
   const int pitch = int(dim) + 4;
@@ -169,10 +171,14 @@ interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
   }
 }
 
-int pick_samples(int nf, int64_t dim, size_t extra_per_sample, size_t fixed,
+// Samples per CTA: enough CTAs for >= 2 per SM (the op is latency-bound at
+// DLRM sizes: a few MB of features), capped by the shared-memory budget.
+int pick_samples(int nf, int64_t dim, int64_t batch, size_t extra_per_sample, size_t fixed,
                  size_t budget) {
   const size_t per = size_t(nf) * (dim + 4) * 4 + extra_per_sample;
   int S = int((budget - fixed) / per);
+  const int64_t want = batch / (2 * kNumSMs);
+  if (S > want) S = int(want);
   if (S > 32) S = 32;
   return S < 1 ? 1 : S;
 }
@@ -207,13 +213,13 @@ extern "C" int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf,
   if (batch == 0) return 0;
   const int npairs = nf * (nf - 1) / 2;
   const size_t fixed = align_up(size_t(npairs) * 4, 16);
-  const int S = pick_samples(nf, dim, 0, fixed, 96 * 1024);
+  const int S = pick_samples(nf, dim, batch, 0, fixed, 96 * 1024);
   const size_t smem = size_t(S) * nf * (dim + 4) * 4 + fixed;
   DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
   cudaStream_t s = as_stream(stream);
   auto k = v4 ? interact_fwd_kernel<true> : interact_fwd_kernel<false>;
   DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k<<<unsigned(ceil_div(batch, S)), 256, smem, s>>>(fs, nf, dim, batch, S, out,
+  launch(k, unsigned(ceil_div(batch, S)), 256, smem, s, fs, nf, dim, batch, S, out,
                                                      ld_out, pad_to);
   return check_launch("interact_fwd_kernel");
 }
@@ -238,13 +244,13 @@ extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
   v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
   if (batch == 0) return 0;
   const size_t extra = size_t(nf) * (nf + 1) * 4;
-  const int S = pick_samples(nf, dim, extra, 0, 96 * 1024);
+  const int S = pick_samples(nf, dim, batch, extra, 0, 96 * 1024);
   const size_t smem = size_t(S) * (nf * (dim + 4) * 4 + extra);
   DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
   cudaStream_t s = as_stream(stream);
   auto k = v4 ? interact_bwd_kernel<true> : interact_bwd_kernel<false>;
   DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  k<<<unsigned(ceil_div(batch, S)), 256, smem, s>>>(fs, gs, nf, dim, batch, S,
+  launch(k, unsigned(ceil_div(batch, S)), 256, smem, s, fs, gs, nf, dim, batch, S,
                                                      gout, ld_gout, relu_mask_f0);
   return check_launch("interact_bwd_kernel");
 }

@@ -2,6 +2,8 @@
 // data gradient (ReLU mask fused), weight/bias gradients (split-K with a
 // fixed-order reduction, SGD fused).  Shapes the tcgen05 path accepts go
 // there (gemm_tc.cu); everything else runs on the SIMT kernels.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "gemm.cuh"
 #include "gemm_tc.cuh"
@@ -97,7 +99,7 @@ extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
     if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s))
       return rc;
   }
-  if (db || b_upd) {
+  if ((db || b_upd) && !getenv("DLRM_EXP_NO_BIAS")) {
     float* cws = ws + size_t(choose_splits(M, N, K)) * N * K;
     if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K))
       cws = ws + tc_linear_bwd_weight_ws_floats(M, N, K) - colreduce_ws_floats(M, N);

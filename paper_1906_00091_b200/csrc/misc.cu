@@ -19,6 +19,13 @@ bool debug_sync() {
   }();
   return on;
 }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DLRM_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
@@ -27,6 +34,7 @@ namespace {
 // matching numpy's `param -= lr * grad` rounding.
 __global__ void sgd_dense_kernel(float* __restrict__ p, const float* __restrict__ g,
                                  int64_t n, float lr, const int32_t* err_flag) {
+  pdl_entry();
   if (err_flag && *err_flag) return;
   const int64_t n4 = n / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -64,7 +72,7 @@ extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
                    reinterpret_cast<uintptr_t>(g) % 16 == 0,
                "sgd_dense needs 16-byte aligned buffers");
   const int64_t blocks = ceil_div(ceil_div(n, 4), 256);
-  sgd_dense_kernel<<<unsigned(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256,
-                     0, as_stream(stream)>>>(p, g, n, lr, err_flag);
+  launch(sgd_dense_kernel, unsigned(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256,
+                     0, as_stream(stream), p, g, n, lr, err_flag);
   return check_launch("sgd_dense_kernel");
 }

@@ -163,8 +163,8 @@ class StepEngine:
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
         # the index-only half of the sparse backward (keys + radix sort) runs
         # on a side stream, overlapped with the dense part of the step;
-        # DLRM_EMB_PREP = "start" | "after_fwd" (default) | "inline"
-        self.prep_at = os.environ.get("DLRM_EMB_PREP", "after_fwd")
+        # DLRM_EMB_PREP = "start" (default) | "after_fwd" | "inline"
+        self.prep_at = os.environ.get("DLRM_EMB_PREP", "start")
         self.side = torch.cuda.Stream(device=dev)
 
         for v in self.input_sets:
