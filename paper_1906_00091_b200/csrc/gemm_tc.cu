@@ -37,12 +37,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-#ifndef DLRM_EXP_TSTAGES
-#define DLRM_EXP_TSTAGES 4
-#define DLRM_EXP_LSTAGES 2
-#endif
-constexpr int TSTAGES = DLRM_EXP_TSTAGES;  // TMA ring of raw fp32 tiles
-constexpr int LSTAGES = DLRM_EXP_LSTAGES;  // ring of split-off lo tiles
+constexpr int TSTAGES = 4;  // TMA ring of raw fp32 tiles
+constexpr int LSTAGES = 2;  // ring of split-off lo tiles
 constexpr int SPLIT_WARPS = 8;  // splitter + epilogue warps (2 per TMEM lane quarter)
 constexpr int THREADS = 64 + 32 * SPLIT_WARPS;
 
@@ -158,12 +154,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+struct WgradFuse {
+  int on;    // 1: fused wgrad epilogue (cluster of gridDim.z split-K CTAs)
+  int bias;  // 1: bias gradient from the row sums of A
+  float* dW;
+  int64_t lddw;
+  float* Wu;
+  int64_t ldw;
+  float* db;
+  float* bu;
+  float lr;
+  const int32_t* err_flag;
+  int vec;  // dW / W rows 16-byte aligned
+};
+
 struct TcArgs {
   int64_t M, N, K;
   int k_tiles_per_split;
   int k_tiles;
   GemmEpilogue ep;
   int a3d, b3d;  // MN-major operand described as a 3D tensor: one TMA box per tile
+  WgradFuse wf;
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -173,6 +184,115 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Fused weight-gradient epilogue (linear_bwd_weight): the split-K CTAs of one
+// output tile form a thread-block cluster along z.  Each keeps its partial
+// tile in its own shared memory; after a cluster barrier CTA z reduces rows
+// [z*R, (z+1)*R) of the tile over the cluster ranks 0..S-1 in order (DSMEM
+// loads, deterministic), writes dW and / or applies W -= lr * dW, and the
+// n-tile-0 cluster does the same for the bias gradient (row sums of the A
+// operand accumulated by the splitter warps).  No partial sums in global
+// memory, no reduction kernel, no counters.
+constexpr uint32_t kBiasScratch = 32 * 20 * 4 * 8;  // after the epilogue transpose tiles
+
+// First of the 4 consecutive tile rows (m) held by 16-byte column c16 of k-row
+// kr in A chunk r of an MN-major SWIZZLE_128B_ATOM_32B tile: 32-byte atoms are
+// XOR-permuted with (k-row % 4) inside each 128-byte row.
+__device__ __forceinline__ int bias_row0(int r, int kr, int c16) {
+  return 32 * r + 8 * ((c16 >> 1) ^ (kr & 3)) + 4 * (c16 & 1);
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ float ld_dsmem1(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
+// Executed by every thread of every CTA of the cluster (see WgradFuse).
+template <int BN>
+__device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const uint8_t* ptile,
+                                                     const uint8_t* bscratch, int64_t m0,
+                                                     int64_t n0) {
+  const WgradFuse& wf = args.wf;
+  constexpr int P = BN + 4, C4 = BN / 4;
+  const int S = int(gridDim.z), z = int(blockIdx.z);  // cluster (1, 1, S): rank == z
+  cluster_sync_all();  // every partial tile / bias scratch of the cluster is written
+  const bool upd = wf.Wu != nullptr && !(wf.err_flag && *wf.err_flag);
+  const int R = (BM + S - 1) / S, r0 = z * R, r1 = r0 + R < BM ? r0 + R : BM;
+  const float* pt = reinterpret_cast<const float*>(ptile);
+  const uint32_t base0 = dsmem_addr(pt, 0);
+  const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, 1) - base0 : 0;
+  for (int e = threadIdx.x; e < (r1 - r0) * C4; e += blockDim.x) {
+    const int r = r0 + e / C4, c = (e % C4) * 4;
+    const int64_t row = m0 + r, col = n0 + c;
+    if (row >= args.M || col >= args.N) continue;
+    const uint32_t off = uint32_t(r * P + c) * 4;
+    float4 acc = ld_dsmem4(base0 + off);
+    for (int k = 1; k < S; ++k) {
+      const float4 v = ld_dsmem4(base0 + uint32_t(k) * rank_stride + off);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (wf.vec && col + 3 < args.N) {
+      if (wf.dW) *reinterpret_cast<float4*>(wf.dW + row * wf.lddw + col) = acc;
+      if (upd) {
+        float4* w = reinterpret_cast<float4*>(wf.Wu + row * wf.ldw + col);
+        float4 o = *w;
+        o.x = __fsub_rn(o.x, __fmul_rn(wf.lr, acc.x));
+        o.y = __fsub_rn(o.y, __fmul_rn(wf.lr, acc.y));
+        o.z = __fsub_rn(o.z, __fmul_rn(wf.lr, acc.z));
+        o.w = __fsub_rn(o.w, __fmul_rn(wf.lr, acc.w));
+        *w = o;
+      }
+    } else {
+      for (int i = 0; i < 4 && col + i < args.N; ++i) {
+        if (wf.dW) wf.dW[row * wf.lddw + col + i] = a[i];
+        if (upd) {
+          float* w = wf.Wu + row * wf.ldw + col + i;
+          *w = __fsub_rn(*w, __fmul_rn(wf.lr, a[i]));
+        }
+      }
+    }
+  }
+  if (wf.bias && blockIdx.x == 0) {
+    const bool bupd = wf.bu != nullptr && !(wf.err_flag && *wf.err_flag);
+    const float* bs = reinterpret_cast<const float*>(bscratch);
+    const uint32_t bb0 = dsmem_addr(bs, 0);
+    const uint32_t bstride = S > 1 ? dsmem_addr(bs, 1) - bb0 : 0;
+    for (int r = r0 + int(threadIdx.x); r < r1; r += int(blockDim.x)) {
+      const int64_t row = m0 + r;
+      if (row >= args.M) continue;
+      float acc = 0.f;  // ranks in order, k-rows in order
+      for (int k = 0; k < S; ++k)
+        for (int kr = 0; kr < 32; ++kr)
+          acc += ld_dsmem1(bb0 + uint32_t(k) * bstride + uint32_t(kr * BM + r) * 4);
+      if (wf.db) wf.db[row] = acc;
+      if (bupd) wf.bu[row] = __fsub_rn(wf.bu[row], __fmul_rn(wf.lr, acc));
+    }
+  }
+  cluster_sync_all();  // no CTA leaves while others still read its shared memory
 }
 
 template <bool A_MN, bool B_MN, int BN>
@@ -280,24 +400,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
         const int t = it % TSTAGES, l = it % LSTAGES;
-#ifdef DLRM_EXP_PURE
-        mbar_wait(&full[t], (it / TSTAGES) & 1);
-#else
         mbar_wait(&conv[l], (it / LSTAGES) & 1);
-#endif
         tc_fence_after();
         const uint32_t a_hi = smem_u32(raw_ring + t * RAW_BYTES);
         const uint32_t b_hi = a_hi + A_BYTES;
-#ifdef DLRM_EXP_PURE
-        const uint32_t a_lo = a_hi;
-#else
         const uint32_t a_lo = smem_u32(lo_ring + l * LO_BYTES);
-#endif
         const uint32_t b_lo = a_lo + A_BYTES;
-#ifdef DLRM_EXP_TMAONLY
-        mbar_arrive(&empty_t[t]);
-        continue;
-#endif
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
@@ -314,42 +422,47 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t small = tmem + uint32_t(NBIG * BN);
           const uint32_t acc_small = (it > 0 || kk > 0) ? 1u : 0u;
           const uint32_t acc_big = (it >= NBIG || kk > 0) ? 1u : 0u;
-#ifndef DLRM_EXP_ONE_MMA
           mma_tf32(small, dal, dbh, IDESC, acc_small);
           mma_tf32(small, dah, dbl, IDESC, 1u);
-#endif
           mma_tf32(big, dah, dbh, IDESC, acc_big);
         }
         mma_commit(&empty_t[t]);
-#ifndef DLRM_EXP_PURE
         mma_commit(&empty_l[l]);
-#endif
       }
       mma_commit(acc_full);
     }
   } else {
-    // ---- splitter warps (2..5): lo = x - trunc_tf32(x) for every landed tile
+    // ---- splitter warps (2..9): lo = x - trunc_tf32(x) for every landed tile.
+    // Fused weight gradient, n-tile 0: the same pass accumulates the row sums
+    // of the (MN-major) A tile = the bias gradient.  Thread ct always sees
+    // A float4 ct + 256 r (r < 4) of a tile: chunk r (32 rows), k-row ct/8,
+    // 16-byte column ct%8 of the 128-byte row (swizzled, see bias_row0).
     const int ct = threadIdx.x - 64;  // 0 .. 32*SPLIT_WARPS-1
-#ifdef DLRM_EXP_PURE
-    for (int it = 0; it < 0; ++it) {
-#else
+    const bool do_bias = A_MN && args.wf.on && args.wf.bias && blockIdx.x == 0;
+    float4 bsum[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) bsum[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int RAW_F4 = int(RAW_BYTES / 16), A_F4 = int(A_BYTES / 16);
     for (int it = 0; it < nk; ++it) {
-#endif
       const int t = it % TSTAGES, l = it % LSTAGES;
       mbar_wait(&full[t], (it / TSTAGES) & 1);
       if (it >= LSTAGES) mbar_wait(&empty_l[l], ((it / LSTAGES) - 1) & 1);
       const float4* src = reinterpret_cast<const float4*>(raw_ring + t * RAW_BYTES);
       float4* dst = reinterpret_cast<float4*>(lo_ring + l * LO_BYTES);
-#ifndef DLRM_EXP_NOSPLIT
-#pragma unroll 4
-      for (int i = ct; i < int(RAW_BYTES / 16); i += 32 * SPLIT_WARPS) {
-        const float4 x = src[i];
-        dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
-                             x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
-                             x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
-                             x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+#pragma unroll
+      for (int j = 0; j < (RAW_F4 + 32 * SPLIT_WARPS - 1) / (32 * SPLIT_WARPS); ++j) {
+        const int i = ct + 32 * SPLIT_WARPS * j;
+        if (RAW_F4 % (32 * SPLIT_WARPS) == 0 || i < RAW_F4) {
+          const float4 x = src[i];
+          dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                               x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
+                               x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
+                               x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+          if (j < 4 && i < A_F4 && do_bias) {
+            bsum[j].x += x.x; bsum[j].y += x.y; bsum[j].z += x.z; bsum[j].w += x.w;
+          }
+        }
       }
-#endif
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[l]);
@@ -384,6 +497,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           for (int i = 0; i < 16; ++i) v[i] += __uint_as_float(ra[j][i]);
         }
       }
+      if (args.wf.on) {  // fused weight gradient: the partial tile stays in smem
+        float* prow = reinterpret_cast<float*>(raw_ring) + (32 * q + lane) * (BN + 4) + c0;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(prow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 16; i += 4)
         *reinterpret_cast<float4*>(tile + lane * 20 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -398,7 +518,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       __syncwarp();
     }
+    if (do_bias) {  // per-thread row sums -> [k-row][m] scratch in unswizzled order
+      float* bs = reinterpret_cast<float*>(lo_ring + kBiasScratch);
+      const int kr = ct >> 3, c16 = ct & 7;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        *reinterpret_cast<float4*>(bs + kr * BM + bias_row0(r, kr, c16)) = bsum[r];
+    }
   }
+  if (args.wf.on) wgrad_cluster_reduce<BN>(args, raw_ring, lo_ring + kBiasScratch, m0, n0);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -468,8 +596,58 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
     configured = true;
   }
   dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)), unsigned(splits));
-  launch(k, grid, THREADS, sm, s, a, b, args);
-  return check_launch("tc_gemm_kernel");
+  if (!args.wf.on) {
+    launch(k, grid, THREADS, sm, s, a, b, args);
+    return check_launch("tc_gemm_kernel");
+  }
+  // fused weight gradient: the split-K CTAs of a tile are one cluster
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = unsigned(splits);
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, k, a, b, args);
+  return check_launch("tc_gemm_kernel(cluster)");
+}
+
+// Concurrently resident clusters of `cz` CTAs of the BN-wide kernel (the
+// split-K clusters of the fused weight gradient); cached per (BN, cz).
+template <bool A_MN, bool B_MN, int BN>
+int max_clusters(int cz) {
+  static int cache[17] = {0};
+  if (cz < 1 || cz > 16) return 1;
+  if (cache[cz]) return cache[cz];
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
+  const size_t sm = smem_bytes(BN);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  if (cz > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, 1, unsigned(cz));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = sm;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = unsigned(cz);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = kNumSMs / cz;
+  }
+  cache[cz] = n;
+  return n;
 }
 
 // Tile planner: pick the N tile (and, where a workspace exists, the split-K
@@ -619,36 +797,56 @@ bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64
 }
 
 namespace {
+// Fused weight gradient: BN and the split-K cluster size from the same time
+// model, waves counted against the number of co-resident clusters.
 TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
-  return plan_tc(N, K, ceil_div(M, BK), true, 32, N * K);
+  constexpr double F = 9000, C0 = 600, C1 = 7.5;
+  const int64_t kt = ceil_div(M, BK), mt = ceil_div(N, BM);
+  TcPlan best{128, 1};
+  double best_t = 1e30;
+  for (int bn : {128, 64, 32}) {
+    if (bn > 32 && K <= bn / 2) continue;
+    const int64_t tiles = mt * ceil_div(K, bn);
+    int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
+    if (smax < 1) smax = 1;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int cap = bn == 128 ? max_clusters<true, true, 128>(int(sp))
+                    : bn == 64  ? max_clusters<true, true, 64>(int(sp))
+                                : max_clusters<true, true, 32>(int(sp));
+      const double waves = double(ceil_div(tiles, cap));
+      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn)) +
+                       (sp > 1 ? 400.0 * double(sp) : 0.0);
+      if (t < best_t) {
+        best_t = t;
+        best = TcPlan{bn, int(sp)};
+      }
+    }
+  }
+  return best;
 }
 }  // namespace
 
-size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K) {
-  const TcPlan p = weight_plan(M, N, K);
-  return size_t(p.splits) * N * K + size_t(ceil_div(M, 64) + 1) * N;
-}
-
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
                          int64_t N, int64_t K, float* dW, int64_t lddw, float* W_upd,
-                         int64_t ldw, float lr, const int32_t* err_flag, float* ws,
-                         cudaStream_t s) {
-  // dW (N x K) = gZ^T X: GEMM m = N (MN-major in gZ), n = K (MN-major in X), k = M
+                         int64_t ldw, float* db, float* b_upd, float lr,
+                         const int32_t* err_flag, cudaStream_t s) {
+  // dW (N x K) = gZ^T X: GEMM m = N (MN-major in gZ), n = K (MN-major in X), k = M;
+  // db (N) = row sums of the A operand; both reduced over the split-K cluster
   const TcPlan pl = weight_plan(M, N, K);
-  const int bn = pl.bn, sp = pl.splits;
+  const int bn = pl.bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
                    map_operand(&mb, X, true, K, M, ldx, bn),
                "tensor map encoding failed (linear_bwd_weight)");
-  TcArgs a{N, K, M, 0, 0, GemmEpilogue{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N,
-                                        aligned16(ws) && K % 4 == 0},
-           use3d(true, N, BM), use3d(true, K, bn)};
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{}, use3d(true, N, BM), use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(M, BK));
-  a.k_tiles_per_split = int(ceil_div(a.k_tiles, sp));
+  a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
-  if (int rc = launch<true, true>(ma, mb, a, K, bn, used, s)) return rc;
-  if (getenv("DLRM_EXP_NO_SPLITK")) return 0;
-  return splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s);
+  const bool vec = (!dW || (aligned16(dW) && lddw % 4 == 0)) &&
+                   (!W_upd || (aligned16(W_upd) && ldw % 4 == 0));
+  a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, lr, err_flag,
+                   vec ? 1 : 0};
+  return launch<true, true>(ma, mb, a, K, bn, used, s);
 }
 
 }  // namespace dlrm

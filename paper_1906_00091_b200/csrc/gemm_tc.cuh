@@ -24,11 +24,12 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W,
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X,
                              int64_t ldx, int64_t M, int64_t N, int64_t K);
-size_t tc_linear_bwd_weight_ws_floats(int64_t M, int64_t N, int64_t K);
+// dW / W update and the bias gradient / update in one launch (split-K
+// reduced inside a thread-block cluster); needs no workspace.
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X,
                          int64_t ldx, int64_t M, int64_t N, int64_t K,
                          float* dW, int64_t lddw, float* W_upd, int64_t ldw,
-                         float lr, const int32_t* err_flag, float* ws,
-                         cudaStream_t s);
+                         float* db, float* b_upd, float lr,
+                         const int32_t* err_flag, cudaStream_t s);
 
 }  // namespace dlrm

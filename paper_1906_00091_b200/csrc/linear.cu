@@ -64,10 +64,10 @@ extern "C" int dlrm_linear_bwd_data(const float* gZ, int64_t ldg,
 
 extern "C" size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N,
                                                         int64_t K) {
+  // SIMT path: split-K partials + bias column-reduce partials (the tcgen05
+  // path reduces inside a cluster and needs none)
   const int sp = choose_splits(M, N, K);
-  size_t f = size_t(sp) * N * K + colreduce_ws_floats(M, N);
-  const size_t tc = tc_linear_bwd_weight_ws_floats(M, N, K);
-  if (tc > f) f = tc;
+  const size_t f = size_t(sp) * N * K + colreduce_ws_floats(M, N);
   return f * sizeof(float) + 256;
 }
 
@@ -80,29 +80,24 @@ extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
                                       size_t ws_bytes, dlrm_stream_t stream) {
   DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldx >= K,
                "bad linear_bwd_weight shape");
+  cudaStream_t s = as_stream(stream);
+  if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K))
+    return tc_linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, W_upd, ldw, db, b_upd,
+                                lr, err_flag, s);
   DLRM_REQUIRE(ws_bytes >= dlrm_linear_bwd_weight_workspace_size(M, N, K) &&
                    workspace != nullptr,
                "linear_bwd_weight workspace too small");
-  cudaStream_t s = as_stream(stream);
   float* ws = static_cast<float*>(workspace);
-  if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K)) {
-    if (int rc = tc_linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, W_upd,
-                                      ldw, lr, err_flag, ws, s))
-      return rc;
-  } else {
-    const int sp = choose_splits(M, N, K);
-    GemmEpilogue ep{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N};
-    // dW(N x K) = gZ^T X: A(m',k') = gZ[k'*ldg + m'], B(k',n') = X[k'*ldx + n']
-    int used = 1;
-    if (int rc = gemm_simt(gZ, 1, ldg, X, 1, ldx, N, K, M, sp, ep, K, s, &used))
-      return rc;
-    if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s))
-      return rc;
-  }
-  if ((db || b_upd) && !getenv("DLRM_EXP_NO_BIAS")) {
-    float* cws = ws + size_t(choose_splits(M, N, K)) * N * K;
-    if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K))
-      cws = ws + tc_linear_bwd_weight_ws_floats(M, N, K) - colreduce_ws_floats(M, N);
+  const int sp = choose_splits(M, N, K);
+  GemmEpilogue ep{EPI_PARTIAL, 0, ws, 0, nullptr, nullptr, 0, K, N};
+  // dW(N x K) = gZ^T X: A(m',k') = gZ[k'*ldg + m'], B(k',n') = X[k'*ldx + n']
+  int used = 1;
+  if (int rc = gemm_simt(gZ, 1, ldg, X, 1, ldx, N, K, M, sp, ep, K, s, &used))
+    return rc;
+  if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s))
+    return rc;
+  if (db || b_upd) {
+    float* cws = ws + size_t(sp) * N * K;
     return colreduce(gZ, ldg, nullptr, M, N, db, b_upd, lr, err_flag, cws,
                      colreduce_ws_floats(M, N), s);
   }
