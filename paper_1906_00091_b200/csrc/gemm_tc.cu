@@ -37,8 +37,18 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-constexpr int TSTAGES = 4;  // TMA ring of raw fp32 tiles
-constexpr int LSTAGES = 2;  // ring of split-off lo tiles
+// Ring depths (raw TMA tiles, split-off lo tiles) within 227 KB of shared
+// memory.  The TMA ring must cover the L2 latency of a tile load (about
+// 1.5 us at full load = 4-5 k-steps of MMA work); a CTA pair holds half of
+// B, so its stages are smaller and the rings deeper.
+#ifndef DLRM_TC_TS
+#define DLRM_TC_TS 5
+#define DLRM_TC_LS 2
+#define DLRM_TC_TS2 6
+#define DLRM_TC_LS2 3
+#endif
+__host__ __device__ constexpr int raw_stages(bool pair) { return pair ? DLRM_TC_TS2 : DLRM_TC_TS; }
+__host__ __device__ constexpr int lo_stages(bool pair) { return pair ? DLRM_TC_LS2 : DLRM_TC_LS; }
 constexpr int SPLIT_WARPS = 8;  // splitter + epilogue warps (2 per TMEM lane quarter)
 constexpr int THREADS = 64 + 32 * SPLIT_WARPS;
 
@@ -105,9 +115,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
 }
 
 // Instruction descriptor: kind::tf32, fp32 accumulate, M = 128.
-__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn, int m = BM) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) |
-         (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+         (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -120,6 +130,37 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       "}\n" ::"r"(tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// CTA pair (cta_group::2): issued by the leader CTA; A rows 0..127 come from
+// the leader's shared memory, rows 128..255 from the peer's (same offsets),
+// and each CTA supplies half of the N columns of B.
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// completion of the pair's MMAs arrives on the barrier at the same offset in
+// every CTA of `mask`
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -140,19 +181,6 @@ __device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 struct WgradFuse {
   int on;    // 1: fused wgrad epilogue (cluster of gridDim.z split-K CTAs)
@@ -215,6 +243,23 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
   return r;
 }
 
+// Forwarded "lo ready" arrive on the pair leader's barrier.  The lo tiles it
+// covers were written by this CTA's splitter warps, made visible to the async
+// proxy (fence.proxy.async) and released to this thread at CTA scope through
+// the local barrier, i.e. they are performed in this CTA's shared memory
+// before the arrive is issued; a .release.cluster arrive would add a
+// GPU-scope fence (MEMBAR.ALL.GPU, ~1.5k cycles) per k-step on the critical
+// path of the pair.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+#ifdef DLRM_PAIR_RELEASE
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+#else
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+#endif
+}
+
 __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -231,19 +276,22 @@ __device__ __forceinline__ float ld_dsmem1(uint32_t addr) {
 }
 
 // Executed by every thread of every CTA of the cluster (see WgradFuse).
-template <int BN>
+template <int BN, bool PAIR>
 __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const uint8_t* ptile,
                                                      const uint8_t* bscratch, int64_t m0,
-                                                     int64_t n0) {
+                                                     int64_t n0, uint32_t pr) {
   const WgradFuse& wf = args.wf;
   constexpr int P = BN + 4, C4 = BN / 4;
-  const int S = int(gridDim.z), z = int(blockIdx.z);  // cluster (1, 1, S): rank == z
+  // cluster (PAIR ? 2 : 1, 1, S): split k of this CTA's row block has rank
+  // pr + (PAIR ? 2 : 1) * k
+  const int S = int(gridDim.z), z = int(blockIdx.z);
   cluster_sync_all();  // every partial tile / bias scratch of the cluster is written
   const bool upd = wf.Wu != nullptr && !(wf.err_flag && *wf.err_flag);
   const int R = (BM + S - 1) / S, r0 = z * R, r1 = r0 + R < BM ? r0 + R : BM;
   const float* pt = reinterpret_cast<const float*>(ptile);
-  const uint32_t base0 = dsmem_addr(pt, 0);
-  const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, 1) - base0 : 0;
+  constexpr uint32_t RS = PAIR ? 2 : 1;
+  const uint32_t base0 = dsmem_addr(pt, pr);
+  const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, pr + RS) - base0 : 0;
   for (int e = threadIdx.x; e < (r1 - r0) * C4; e += blockDim.x) {
     const int r = r0 + e / C4, c = (e % C4) * 4;
     const int64_t row = m0 + r, col = n0 + c;
@@ -276,11 +324,11 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
       }
     }
   }
-  if (wf.bias && blockIdx.x == 0) {
+  if (wf.bias && n0 == 0) {
     const bool bupd = wf.bu != nullptr && !(wf.err_flag && *wf.err_flag);
     const float* bs = reinterpret_cast<const float*>(bscratch);
-    const uint32_t bb0 = dsmem_addr(bs, 0);
-    const uint32_t bstride = S > 1 ? dsmem_addr(bs, 1) - bb0 : 0;
+    const uint32_t bb0 = dsmem_addr(bs, pr);
+    const uint32_t bstride = S > 1 ? dsmem_addr(bs, pr + RS) - bb0 : 0;
     for (int r = r0 + int(threadIdx.x); r < r1; r += int(blockDim.x)) {
       const int64_t row = m0 + r;
       if (row >= args.M) continue;
@@ -295,12 +343,20 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
   cluster_sync_all();  // no CTA leaves while others still read its shared memory
 }
 
-template <bool A_MN, bool B_MN, int BN>
+// PAIR: the two CTAs of a cluster pair along x compute a 256 x BN tile with
+// cta_group::2 MMAs (each loads its own 128 A rows and BN/2 B columns), which
+// cuts the shared-memory traffic per MMA by a quarter; the leader (even y)
+// issues the MMAs, both CTAs split and run their own epilogue rows.
+template <bool A_MN, bool B_MN, int BN, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                TcArgs args) {
+  constexpr int BNL = PAIR ? BN / 2 : BN;  // B columns held by this CTA
+  constexpr int LSTAGES = lo_stages(PAIR);
+  constexpr int TSTAGES = raw_stages(PAIR);
+  static_assert(!PAIR || BNL % 32 == 0 || !B_MN, "pair B half must be whole 32-column chunks");
   constexpr uint32_t A_BYTES = BM * BK * 4;  // 16 KB
-  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t B_BYTES = BNL * BK * 4;
   constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;  // one TMA stage (= the hi operands)
   constexpr uint32_t LO_BYTES = A_BYTES + B_BYTES;   // one lo slot
   // NBIG interleaved accumulators for hi*hi (k-block it -> it % NBIG) plus
@@ -313,11 +369,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr uint32_t TMEM_COLS = COLS_NEEDED <= 32 ? 32 : COLS_NEEDED <= 64 ? 64
                                : COLS_NEEDED <= 128 ? 128 : COLS_NEEDED <= 256 ? 256 : 512;
   static_assert(COLS_NEEDED <= 512, "TMEM overflow");
-  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN, PAIR ? 2 * BM : BM);
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned for the 128B swizzle; offsetting the __shared__ array
+  // (not casting through an integer) keeps every derived pointer in the
+  // shared window, so the splitter / epilogue accesses compile to LDS / STS
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* raw_ring = smem;                            // TSTAGES x RAW_BYTES
   uint8_t* lo_ring = smem + TSTAGES * RAW_BYTES;       // LSTAGES x LO_BYTES
   uint64_t* bars = reinterpret_cast<uint64_t*>(lo_ring + LSTAGES * LO_BYTES);
@@ -330,7 +388,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   pdl_trigger();  // prologue below touches no data of the previous kernel
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  // pairs run along x (cluster (2, 1, S)): grid = (m tiles, n tiles, splits);
+  // otherwise grid = (n tiles, m tiles, splits)
+  const int64_t m_tile = PAIR ? blockIdx.x : blockIdx.y, n_tile = PAIR ? blockIdx.y : blockIdx.x;
+  const int64_t m0 = m_tile * BM, n0 = n_tile * BN;
+  const uint32_t pr = PAIR ? (blockIdx.x & 1u) : 0u;          // rank inside the pair
+  const uint32_t lead = PAIR ? cluster_ctarank() - pr : 0u;   // cluster rank of the leader
+  const int64_t nb0 = n0 + int64_t(pr) * BNL;                  // this CTA's B columns
   const int kt0 = blockIdx.z * args.k_tiles_per_split;
   const int kt1 = min(args.k_tiles, kt0 + args.k_tiles_per_split);
   const int nk = kt1 - kt0;
@@ -341,7 +405,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&empty_t[s], 1);
     }
     for (int s = 0; s < LSTAGES; ++s) {
-      mbar_init(&conv[s], SPLIT_WARPS);
+      // the leader's lo-ready barrier also takes one forwarded arrive from the peer
+      mbar_init(&conv[s], PAIR && pr == 0 ? SPLIT_WARPS + 1 : SPLIT_WARPS);
       mbar_init(&empty_l[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -350,14 +415,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer arrives on the leader's barriers
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // operands / epilogue inputs come from earlier kernels
@@ -383,21 +457,31 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         uint8_t* sb = st + A_BYTES;
         if (B_MN && args.b3d) {
-          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
+          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(nb0 / 32));
         } else if (B_MN) {
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c)
-            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
-          if (BN % 32)  // BN == 16: a single 16-wide box
-            tma_load_2d(sb, &tmB, &full[s], int(n0), k0);
+          for (int c = 0; c < BNL / 32; ++c)
+            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(nb0 + 32 * c), k0);
+          if (BNL % 32)  // BN == 16: a single 16-wide box
+            tma_load_2d(sb, &tmB, &full[s], int(nb0), k0);
         } else {
-          tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
+          tma_load_2d(sb, &tmB, &full[s], k0, int(nb0));
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer
-    if (lane == 0) {
+    // ---- pair peer: forward "lo ready" to the leader, one cluster-scope
+    // release per k-step by a single thread (a release.cluster arrive costs a
+    // GPU-scope fence; the splitter warps only arrive locally)
+    if (PAIR && pr != 0 && lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int l = it % LSTAGES;
+        mbar_wait(&conv[l], (it / LSTAGES) & 1);
+        mbar_arrive_cluster(dsmem_addr(&conv[l], lead));
+      }
+    }
+    // ---- MMA issuer (the pair's leader only)
+    if (lane == 0 && pr == 0) {
       for (int it = 0; it < nk; ++it) {
         const int t = it % TSTAGES, l = it % LSTAGES;
         mbar_wait(&conv[l], (it / LSTAGES) & 1);
@@ -422,14 +506,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t small = tmem + uint32_t(NBIG * BN);
           const uint32_t acc_small = (it > 0 || kk > 0) ? 1u : 0u;
           const uint32_t acc_big = (it >= NBIG || kk > 0) ? 1u : 0u;
-          mma_tf32(small, dal, dbh, IDESC, acc_small);
-          mma_tf32(small, dah, dbl, IDESC, 1u);
-          mma_tf32(big, dah, dbh, IDESC, acc_big);
+          if (PAIR) {
+            mma_tf32_pair(small, dal, dbh, IDESC, acc_small);
+            mma_tf32_pair(small, dah, dbl, IDESC, 1u);
+            mma_tf32_pair(big, dah, dbh, IDESC, acc_big);
+          } else {
+            mma_tf32(small, dal, dbh, IDESC, acc_small);
+            mma_tf32(small, dah, dbl, IDESC, 1u);
+            mma_tf32(big, dah, dbh, IDESC, acc_big);
+          }
         }
-        mma_commit(&empty_t[t]);
-        mma_commit(&empty_l[l]);
+        if (PAIR) {
+          const uint16_t mask = uint16_t(3u << lead);
+          mma_commit_pair(&empty_t[t], mask);
+          mma_commit_pair(&empty_l[l], mask);
+        } else {
+          mma_commit(&empty_t[t]);
+          mma_commit(&empty_l[l]);
+        }
       }
-      mma_commit(acc_full);
+      if (PAIR) mma_commit_pair(acc_full, uint16_t(3u << lead));
+      else mma_commit(acc_full);
     }
   } else {
     // ---- splitter warps (2..9): lo = x - trunc_tf32(x) for every landed tile.
@@ -438,7 +535,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // A float4 ct + 256 r (r < 4) of a tile: chunk r (32 rows), k-row ct/8,
     // 16-byte column ct%8 of the 128-byte row (swizzled, see bias_row0).
     const int ct = threadIdx.x - 64;  // 0 .. 32*SPLIT_WARPS-1
-    const bool do_bias = A_MN && args.wf.on && args.wf.bias && blockIdx.x == 0;
+    const bool do_bias = A_MN && args.wf.on && args.wf.bias && n_tile == 0;
     float4 bsum[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) bsum[r] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -526,14 +623,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         *reinterpret_cast<float4*>(bs + kr * BM + bias_row0(r, kr, c16)) = bsum[r];
     }
   }
-  if (args.wf.on) wgrad_cluster_reduce<BN>(args, raw_ring, lo_ring + kBiasScratch, m0, n0);
+  if (args.wf.on)
+    wgrad_cluster_reduce<BN, PAIR>(args, raw_ring, lo_ring + kBiasScratch, m0, n0, pr);
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM / barriers
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS)
-                 : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -581,26 +685,43 @@ bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-constexpr size_t smem_bytes(int bn) {
-  return size_t(TSTAGES + LSTAGES) * (BM * BK * 4 + bn * BK * 4) + 1024 + 256;
+constexpr size_t smem_bytes(int bn, bool pair) {
+  return size_t(raw_stages(pair) + lo_stages(pair)) * (BM * BK * 4 + bn * BK * 4) + 1024 + 256;
 }
 
-template <bool A_MN, bool B_MN, int BN>
+// CTA pairs are OFF by default: measured on B200 (scripts/gemm_one.py,
+// 2048 x 1024 x K), the pair kernel matches but does not beat the single-CTA
+// kernel (K=1024: 28.7 vs 28.3 us; K=4096: 91.9 vs 91.9 us) — the steady
+// state is bound by the TMA feed + MMA shared-memory contention (1050
+// cycles / k-step without the splitter vs 830 for the MMAs alone), and the
+// pair's lock-stepped SMs give back what the halved B traffic saves.
+// DLRM_TC_PAIR=1 enables them.
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DLRM_TC_PAIR");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+template <bool A_MN, bool B_MN, int BN, bool PAIR>
 int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
               int splits, cudaStream_t s) {
-  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
-  const size_t sm = smem_bytes(BN);
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN, PAIR>;
+  const size_t sm = smem_bytes(PAIR ? BN / 2 : BN, PAIR);
   static bool configured = false;
   if (!configured) {
     DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     configured = true;
   }
-  dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)), unsigned(splits));
-  if (!args.wf.on) {
+  const unsigned nt = unsigned(ceil_div(n_grid, BN)), mt = unsigned(ceil_div(args.M, BM));
+  dim3 grid = PAIR ? dim3(mt, nt, unsigned(splits)) : dim3(nt, mt, unsigned(splits));
+  if (!args.wf.on && !PAIR) {
     launch(k, grid, THREADS, sm, s, a, b, args);
     return check_launch("tc_gemm_kernel");
   }
-  // fused weight gradient: the split-K CTAs of a tile are one cluster
+  // CTA pairs along y and / or the split-K CTAs of a weight-gradient tile
+  // along z form one cluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
@@ -608,9 +729,9 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = unsigned(splits);
+  attr[0].val.clusterDim.z = args.wf.on ? unsigned(splits) : 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
@@ -619,24 +740,25 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   return check_launch("tc_gemm_kernel(cluster)");
 }
 
-// Concurrently resident clusters of `cz` CTAs of the BN-wide kernel (the
-// split-K clusters of the fused weight gradient); cached per (BN, cz).
-template <bool A_MN, bool B_MN, int BN>
+// Concurrently resident clusters of (PAIR ? 2 : 1, 1, cz) CTAs of the
+// BN-wide kernel; cached per instantiation and cz.
+template <bool A_MN, bool B_MN, int BN, bool PAIR>
 int max_clusters(int cz) {
   static int cache[17] = {0};
   if (cz < 1 || cz > 16) return 1;
   if (cache[cz]) return cache[cz];
-  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
-  const size_t sm = smem_bytes(BN);
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN, PAIR>;
+  const size_t sm = smem_bytes(PAIR ? BN / 2 : BN, PAIR);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  if (cz > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  const int csz = cz * (PAIR ? 2 : 1);
+  if (csz > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(1, 1, unsigned(cz));
+  cfg.gridDim = dim3(PAIR ? 2 : 1, 1, unsigned(cz));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = sm;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = unsigned(cz);
   cfg.attrs = attr;
@@ -644,7 +766,7 @@ int max_clusters(int cz) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) {
     cudaGetLastError();
-    n = kNumSMs / cz;
+    n = kNumSMs / csz;
   }
   cache[cz] = n;
   return n;
@@ -687,19 +809,25 @@ TcPlan plan_tc(int64_t M, int64_t n_grid, int64_t kt, bool allow_split, int min_
   return best;
 }
 
-int pick_bn(int64_t M, int64_t n_grid) {
-  return plan_tc(M, n_grid, 8, false, 16, 0).bn;
-}
 
 template <bool A_MN, bool B_MN>
 int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
-           int bn, int splits, cudaStream_t s) {
-  switch (bn) {
-    case 16: return launch_bn<A_MN, B_MN, 16>(a, b, args, n_grid, splits, s);
-    case 32: return launch_bn<A_MN, B_MN, 32>(a, b, args, n_grid, splits, s);
-    case 64: return launch_bn<A_MN, B_MN, 64>(a, b, args, n_grid, splits, s);
-    default: return launch_bn<A_MN, B_MN, 128>(a, b, args, n_grid, splits, s);
+           int bn, int splits, bool pair, cudaStream_t s) {
+  if (pair) {
+    if (bn == 64) return launch_bn<A_MN, B_MN, 64, true>(a, b, args, n_grid, splits, s);
+    return launch_bn<A_MN, B_MN, 128, true>(a, b, args, n_grid, splits, s);
   }
+  switch (bn) {
+    case 16: return launch_bn<A_MN, B_MN, 16, false>(a, b, args, n_grid, splits, s);
+    case 32: return launch_bn<A_MN, B_MN, 32, false>(a, b, args, n_grid, splits, s);
+    case 64: return launch_bn<A_MN, B_MN, 64, false>(a, b, args, n_grid, splits, s);
+    default: return launch_bn<A_MN, B_MN, 128, false>(a, b, args, n_grid, splits, s);
+  }
+}
+
+// CTA pairs need an even number of 128-row tiles and whole 32-column B halves
+bool use_pair(int64_t M, int bn) {
+  return pair_enabled() && (bn == 64 || bn == 128) && ceil_div(M, BM) % 2 == 0;
 }
 
 // MN-major operand whose MN extent is a multiple of 32, seen as the 3D
@@ -750,16 +878,17 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
                   float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
                   int act, cudaStream_t s) {
   const int bn = plan_tc(M, n_grid, ceil_div(K, BK), false, 16, 0).bn;
+  const bool pair = use_pair(M, bn);
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
-                   map_operand(&mb, W, false, N, K, ldw, bn),
+                   map_operand(&mb, W, false, N, K, ldw, pair ? bn / 2 : bn),
                "tensor map encoding failed (linear_fwd)");
   TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M,
                                         aligned16(Y) && ldy % 4 == 0 && aligned16(b)},
            0, 0};
   a.k_tiles = int(ceil_div(K, BK));
   a.k_tiles_per_split = a.k_tiles;
-  return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
+  return launch<false, false>(ma, mb, a, n_grid, bn, 1, pair, s);
 }
 
 bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
@@ -775,17 +904,19 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
                        int64_t N, int64_t K, cudaStream_t s) {
   // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
   const int bn = plan_tc(M, K, ceil_div(N, BK), false, 32, 0).bn;
+  const bool pair = use_pair(M, bn);
+  const int bnl = pair ? bn / 2 : bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
-                   map_operand(&mb, W, true, K, N, ldw, bn),
+                   map_operand(&mb, W, true, K, N, ldw, bnl),
                "tensor map encoding failed (linear_bwd_data)");
   TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M,
                                         aligned16(dX) && ldx % 4 == 0 &&
                                             (!mask || (aligned16(mask) && ldm % 4 == 0))},
-           0, use3d(true, K, bn)};
+           0, use3d(true, K, bnl)};
   a.k_tiles = int(ceil_div(N, BK));
   a.k_tiles_per_split = a.k_tiles;
-  return launch<false, true>(ma, mb, a, K, bn, 1, s);
+  return launch<false, true>(ma, mb, a, K, bn, 1, pair, s);
 }
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
@@ -809,12 +940,19 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
     const int64_t tiles = mt * ceil_div(K, bn);
     int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
     if (smax < 1) smax = 1;
+    const bool pair = use_pair(N, bn);
+    if (pair && smax > 4) smax = 4;  // cluster (2, 1, sp) <= 8 CTAs
     for (int64_t sp = 1; sp <= smax; ++sp) {
-      const int cap = bn == 128 ? max_clusters<true, true, 128>(int(sp))
-                    : bn == 64  ? max_clusters<true, true, 64>(int(sp))
-                                : max_clusters<true, true, 32>(int(sp));
+      int cap;  // co-resident clusters, in units of 128-row tiles
+      if (pair)
+        cap = 2 * (bn == 128 ? max_clusters<true, true, 128, true>(int(sp))
+                             : max_clusters<true, true, 64, true>(int(sp)));
+      else
+        cap = bn == 128 ? max_clusters<true, true, 128, false>(int(sp))
+            : bn == 64  ? max_clusters<true, true, 64, false>(int(sp))
+                        : max_clusters<true, true, 32, false>(int(sp));
       const double waves = double(ceil_div(tiles, cap));
-      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn)) +
+      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn) * (pair ? 0.8 : 1.0)) +
                        (sp > 1 ? 400.0 * double(sp) : 0.0);
       if (t < best_t) {
         best_t = t;
@@ -834,11 +972,13 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   // db (N) = row sums of the A operand; both reduced over the split-K cluster
   const TcPlan pl = weight_plan(M, N, K);
   const int bn = pl.bn;
+  const bool pair = use_pair(N, bn);
+  const int bnl = pair ? bn / 2 : bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
-                   map_operand(&mb, X, true, K, M, ldx, bn),
+                   map_operand(&mb, X, true, K, M, ldx, bnl),
                "tensor map encoding failed (linear_bwd_weight)");
-  TcArgs a{N, K, M, 0, 0, GemmEpilogue{}, use3d(true, N, BM), use3d(true, K, bn)};
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{}, use3d(true, N, BM), use3d(true, K, bnl)};
   a.k_tiles = int(ceil_div(M, BK));
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
@@ -846,7 +986,7 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
                    (!W_upd || (aligned16(W_upd) && ldw % 4 == 0));
   a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, lr, err_flag,
                    vec ? 1 : 0};
-  return launch<true, true>(ma, mb, a, K, bn, used, s);
+  return launch<true, true>(ma, mb, a, K, bn, used, pair, s);
 }
 
 }  // namespace dlrm
