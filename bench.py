@@ -16,8 +16,14 @@
 * ``e2e``: the same step through the public engine API from PINNED HOST
   buffers — H2D of dense rows, offsets, indices and labels, the step, and a
   D2H read of the step result (loss sum, correct count) — every step.
-* ``roofline``: the dominant kernel of the step, timed alone with CUDA events
-  on its launch stream, against MEASURED_PEAKS.json.
+* ``roofline``: the dominant single kernel of the step (the embedding
+  backward apply: segmented fold + row update), its per-launch time from a
+  replay of the step graph with event-record nodes at the stage boundaries,
+  algorithmic bytes per launch, the copy-bandwidth peak of
+  MEASURED_PEAKS.json, and ``traffic`` = DRAM bytes per launch from the
+  committed ncu capture (profiles/ncu_traffic_<config>.json).
+  ``embedding_roofline`` adds the forward and the standalone full backward;
+  ``mlp_roofline`` the tcgen05 MLP GEMMs against the bf16 and 3xTF32 peaks.
 * ``cpu_baseline``: the reference algorithm (oracle/port.py, float64, the
   reference's own numpy/BLAS path) on this host's cores over a bounded
   sample of the same workload.
@@ -185,6 +191,63 @@ def run_reference(args, c, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 
+# Random-row gather ceiling on B200 (scripts/gather_bw.cu: 831k uniformly
+# random rows of a 2 GiB table, fresh indices and a flushed L2 per rep; GB/s
+# by row bytes) — the access pattern of the pooled lookup.  See
+# profiles/round1/gather_ceiling.txt.
+GATHER_CEILING = {64: 1610.0, 128: 3201.0, 256: 4223.0, 512: 4981.0}
+
+
+def ncu_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    ncu --set full capture of this config (profiles/ncu_traffic_<cfg>.json),
+    or None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except Exception:
+        return None
+
+
+def time_embedding_kernels(eng, flush, reps=5):
+    """dlrm_emb_fwd and the full sparse backward (prepare + apply, lr = 0 so
+    the tables stay unchanged) launched alone on the engine's buffers, CUDA
+    events on the launching stream, L2 flushed before each rep."""
+    import torch
+    from paper_1906_00091_b200 import _lib
+    P, call = _lib.ptr, _lib.call
+    s = torch.cuda.current_stream()
+    h = _lib.stream_handle(s)
+    d, B, nf = eng.d, eng.B, eng.nf
+
+    def fwd():
+        call("dlrm_emb_fwd", P(eng.W_all), d, eng._descs_p, eng.T, B, P(eng.Z), nf * d,
+             P(eng.err_pos), P(eng.err_flag), h)
+
+    def bwd():
+        call("dlrm_emb_bwd_prepare", d, eng._descs_p, eng.T, B, eng.total_rows,
+             P(eng.emb_ws), eng.emb_ws_bytes, h)
+        call("dlrm_emb_bwd_apply_sgd", P(eng.W_all), d, eng._descs_p, eng.T, B, P(eng.gZ),
+             nf * d, 0.0, P(eng.err_flag), eng.total_rows, P(eng.emb_ws), eng.emb_ws_bytes, h)
+
+    out = {}
+    for name, fn in (("fwd_ms", fwd), ("bwd_ms", bwd)):
+        fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for r in range(reps):
+            flush.fill_(r & 0xff)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        out[name] = tot / reps
+    return out
+
+
 def algorithmic(c, B, hbs, eng):
     """Per-step algorithmic bytes/flops of the stages."""
     d = c["d"]
@@ -310,36 +373,45 @@ def run_ours(args, c, rank, world, dist):
     e2e = world * B * K / (e2e_ms / 1e3)
     loss_last = float(res_host[K - 1, 0]) / B
 
-    # per-stage breakdown and the dominant kernel's roofline
+    # per-stage breakdown (a replay of the same step graph with event-record
+    # nodes at the stage boundaries, L2 flushed) and the rooflines
     stages = eng.profile_stages(reps=5, flush=flush)
     fwd_b, bwd_b, flops = algorithmic(c, B, hbs, eng)
-    emb_fwd_ms = stages.get("embedding_fwd", float("nan"))
-    emb_bwd_ms = stages.get("embedding_bwd_sgd", float("nan"))
+    emb_alone = time_embedding_kernels(eng, flush)
     pk, pk_kind = peaks()
     hbm = pk["hbm_gbs"]
+    emb_fwd_ms = stages.get("embedding_fwd", float("nan"))
+    emb_apply_ms = stages.get("embedding_bwd_sgd", float("nan"))
+    # embedding backward = index prepare (keys + radix sort; overlapped with
+    # the dense step on a side stream) + apply (segmented fold + row update,
+    # on the critical path); bytes: SURVEY §8(d) per lookup / per unique row
     cands = {
         "embedding_fwd": (fwd_b / (emb_fwd_ms / 1e3) / 1e9, emb_fwd_ms, fwd_b),
-        "embedding_bwd_sgd": (bwd_b / (emb_bwd_ms / 1e3) / 1e9, emb_bwd_ms, bwd_b),
+        "embedding_bwd_apply": (bwd_b / (emb_apply_ms / 1e3) / 1e9, emb_apply_ms, bwd_b),
+        "embedding_bwd_full_standalone": (bwd_b / (emb_alone["bwd_ms"] / 1e3) / 1e9,
+                                          emb_alone["bwd_ms"], bwd_b),
+        "embedding_fwd_standalone": (fwd_b / (emb_alone["fwd_ms"] / 1e3) / 1e9,
+                                     emb_alone["fwd_ms"], fwd_b),
     }
-    groups = {"embedding_fwd": stages["embedding_fwd"],
-              "embedding_bwd_sgd": stages["embedding_bwd_sgd"],
-              "mlp": stages["mlp_total"],
-              "interaction": stages["interaction_fwd"] + stages["interaction_bwd"]}
-    dom = max(groups, key=lambda k: groups[k])
-    if dom in cands:
-        gbs, kms, kb = cands[dom]
-        roofline = {"kernel": dom, "bound": "hbm", "achieved": gbs, "peak": hbm,
-                    "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
-                    "peak_kind": pk_kind, "algorithmic_bytes": kb,
-                    "ms": kms}
-    else:
-        mlp_fl = flops
-        tf = mlp_fl / (stages["mlp_total"] / 1e3) / 1e12
-        roofline = {"kernel": dom, "bound": "tensor", "achieved": tf,
-                    "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": tf / pk["bf16_tflops"], "traffic": None,
-                    "peak_kind": pk_kind + " bf16 (tf32 = 1/2, 3xTF32 = 1/6)",
-                    "ms": groups[dom]}
+    # the dominant single kernel of the step is the embedding backward apply
+    # (one fold + SGD launch; every GEMM launch is shorter, see profiles/)
+    dom = max(("embedding_fwd", "embedding_bwd_apply"), key=lambda k: cands[k][1])
+    gbs, kms, kb = cands[dom]
+    traffic = ncu_traffic(args.config, "emb_fold_kernel" if dom == "embedding_bwd_apply"
+                          else "emb_fwd_stream_kernel")
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": gbs, "peak": hbm,
+                "unit": "GB/s", "frac": gbs / hbm, "traffic": traffic,
+                "peak_kind": pk_kind + " copy bandwidth (MEASURED_PEAKS.json)",
+                "algorithmic_bytes_per_launch": kb, "ms_per_launch": kms,
+                "random_row_gather_ceiling_gbs": GATHER_CEILING.get(4 * c["d"])}
+    tf = flops / (stages["mlp_total"] / 1e3) / 1e12
+    mlp_roof = {"bound": "tensor", "achieved": tf, "unit": "TFLOP/s",
+                "peak": pk["bf16_tflops"], "frac": tf / pk["bf16_tflops"],
+                "peak_3xtf32": pk["bf16_tflops"] / 6.0,
+                "frac_of_3xtf32_peak": tf / (pk["bf16_tflops"] / 6.0),
+                "note": "fp32-accurate 3xTF32: 3 tf32 MMAs per product at half the bf16 "
+                        "rate; algorithmic flops 2*B*n_in*n_out per GEMM (fwd, dgrad, wgrad)",
+                "ms": stages["mlp_total"], "gflop_per_step": flops / 1e9}
     emb_roof = {k: {"GB/s": v[0], "ms": v[1], "bytes": v[2], "frac": v[0] / hbm}
                 for k, v in cands.items()}
 
@@ -364,7 +436,7 @@ def run_ours(args, c, rank, world, dist):
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / K},
             "gpu_launches": int(launches) * K if launches else None,
-            "roofline": roofline, "embedding_roofline": emb_roof,
+            "roofline": roofline, "embedding_roofline": emb_roof, "mlp_roofline": mlp_roof,
             "stages_ms": {k: v for k, v in stages.items() if k != "captured"},
             "stages_graph_events": stages.get("captured"), "mlp_gflop_per_step": flops / 1e9,
             "loss_last": loss_last, "clocks": clk.summary(),

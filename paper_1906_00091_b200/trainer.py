@@ -40,6 +40,21 @@ from .model import DlrmModel, ceil4
 
 __all__ = ["StepEngine", "StepResult"]
 
+
+def _adopt_flat(ws, row_base, d):
+    """The flat fp32 buffer the tables already are consecutive views of
+    (device-initialised models), or None."""
+    if not ws or any(w.dtype != torch.float32 or not w.is_contiguous() for w in ws):
+        return None
+    st = ws[0].untyped_storage()
+    base = ws[0].data_ptr()
+    for t, w in enumerate(ws):
+        if w.untyped_storage().data_ptr() != st.data_ptr() or \
+                w.data_ptr() != base + 4 * int(row_base[t]) * d:
+            return None
+    n = int(row_base[-1]) * d
+    return ws[0].reshape(-1).as_strided((n,), (1,)) if n else None
+
 INT64_MAX = np.iinfo(np.int64).max
 
 
@@ -98,12 +113,14 @@ class StepEngine:
         self.rows = [t.num_rows for t in model.tables]
         self.row_base = np.concatenate([[0], np.cumsum(self.rows)]).astype(np.int64)
         self.total_rows = int(self.row_base[-1])
-        self.W_all = torch.empty(self.total_rows * d, **f32)
-        for t, tab in enumerate(model.tables):
-            v = self.W_all[self.row_base[t] * d:self.row_base[t + 1] * d].view(
-                self.rows[t], d)
-            v.copy_(tab.weights)
-            tab.weights = v
+        self.W_all = _adopt_flat([t.weights for t in model.tables], self.row_base, d)
+        if self.W_all is None:  # copy into one buffer, releasing each table after
+            self.W_all = torch.empty(self.total_rows * d, **f32)
+            for t, tab in enumerate(model.tables):
+                v = self.W_all[self.row_base[t] * d:self.row_base[t + 1] * d].view(
+                    self.rows[t], d)
+                v.copy_(tab.weights)
+                tab.weights = v
 
         # ---- inputs: one contiguous block per input set, laid out exactly
         # like a packed host batch (pack_host_batch) so a step's inputs move

@@ -22,6 +22,7 @@ ap.add_argument("--rows", type=int, nargs="*")
 ap.add_argument("--d", type=int, nargs="*")
 ap.add_argument("--pool", type=int, nargs="*")
 ap.add_argument("--fwd-only", action="store_true")
+ap.add_argument("--nnz", type=int, default=1 << 20, help="lookups per point")
 a = ap.parse_args()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists("MEASURED_PEAKS.json") else 6553.6
@@ -53,7 +54,7 @@ for rows in rows_list:
         W = torch.empty(rows * d, device=dev)
         W.uniform_(-0.1, 0.1)
         for pool in pool_list:
-            B = max(2048, 262144 // pool)
+            B = max(2048, a.nnz // pool)
             for dist in ("uniform", "zipf"):
                 nnz = B * pool
                 if dist == "uniform":
