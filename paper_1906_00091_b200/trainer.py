@@ -182,6 +182,8 @@ class StepEngine:
         # on a side stream, overlapped with the dense part of the step;
         # DLRM_EMB_PREP = "start" (default) | "after_fwd" | "inline"
         self.prep_at = os.environ.get("DLRM_EMB_PREP", "start")
+        # DLRM_EMB_APPLY_SIDE=0 keeps the apply on the main stream
+        self.apply_side = os.environ.get("DLRM_EMB_APPLY_SIDE", "1") != "0"
         self.side = torch.cuda.Stream(device=dev)
 
         for v in self.input_sets:
@@ -308,6 +310,7 @@ class StepEngine:
     def launch(self, stream=None, mark=None):
         """Issue the whole step on ``stream`` (default: current stream).
         ``mark(stage)`` (profiling only) is called before each stage."""
+        profiling = mark is not None
         mark = mark or (lambda name: None)
         main = stream if stream is not None else torch.cuda.current_stream()
         s = _lib.stream_handle(main)
@@ -392,6 +395,20 @@ class StepEngine:
         call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
              self.gR.stride(0), C.cast(self._gfeat, C.c_void_p),
              C.cast(self._gstride, C.c_void_p), 1, s)
+        # The sparse backward apply needs only the feature gradients the
+        # interaction backward just wrote: it runs on the side stream,
+        # concurrently with the bottom MLP backward (the stage profile, which
+        # times stages on one stream, keeps them in order).
+        apply_done = None
+        if self.apply_side and prep_done is not None and profiling is False:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.side.wait_event(ev)
+            call("dlrm_emb_bwd_apply_sgd", P(self.W_all), d, self._descs_p, self.T, B,
+                 P(self.gZ), nf * d, lr, ef, self.total_rows, P(self.emb_ws),
+                 self.emb_ws_bytes, _lib.stream_handle(self.side))
+            apply_done = torch.cuda.Event()
+            apply_done.record(self.side)
         # bottom MLP backward
         mark("bottom_mlp_bwd")
         for i in range(self.Lb - 1, -1, -1):
@@ -411,6 +428,9 @@ class StepEngine:
                  P(l.bias), lr, ef, ws, wsb, s)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
+        if apply_done is not None:
+            main.wait_event(apply_done)  # join: the next step reads the tables
+            return
         if prep_done is None:
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
                  P(self.emb_ws), self.emb_ws_bytes, s)
