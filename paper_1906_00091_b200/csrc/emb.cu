@@ -274,24 +274,6 @@ emb_fwd_warp_kernel(const float* __restrict__ W, int64_t dim, TableSet ts,
   }
 }
 
-// cp.async helpers (16 B per lane, zero fill when !ok)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int n = ok ? 16 : 0;  // src-size 0 -> zero fill
-#ifndef DLRM_CP_CA
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
-               : "memory");
-#else
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
-               : "memory");
-#endif
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // ---------------------------------------------------------------------------
 // forward, streaming variant (the default for 16-byte-aligned rows).
 //

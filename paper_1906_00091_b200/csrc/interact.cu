@@ -41,13 +41,15 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
   const int64_t b0 = int64_t(blockIdx.x) * S;
   const int ns = int(batch - b0 < S ? batch - b0 : S);
   // stage features
-  if (V4) {
+  if (V4) {  // cp.async: every 16-byte piece of the tile in flight at once
     const int nv = int(dim / 4);
     for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
       const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c);
-      *reinterpret_cast<float4*>(z + (size_t(s) * nf + f) * pitch + 4 * c) = v;
+      cp_async16(z + (size_t(s) * nf + f) * pitch + 4 * c,
+                 reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c, true);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
   } else {
     for (int e = threadIdx.x; e < ns * nf * int(dim); e += blockDim.x) {
       const int s = e / (nf * int(dim)), r = e - s * nf * int(dim), f = r / int(dim),
@@ -58,6 +60,67 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
   __syncthreads();
   const int width = int(dim) + npairs;
   const int total_w = int(pad_to > width ? pad_to : width);
+  if (V4) {
+    // z0 copy and zero pad columns
+    const int extra = total_w - width;
+    for (int e = threadIdx.x; e < ns * (int(dim) + extra); e += blockDim.x) {
+      const int s = e / (int(dim) + extra), col = e - s * (int(dim) + extra);
+      out[(b0 + s) * ld_out + (col < dim ? col : width + (col - int(dim)))] =
+          col < dim ? z[size_t(s) * nf * pitch + col] : 0.f;
+    }
+    // pair dots in 4x4 feature blocks (bi <= bj): 8 float4 smem loads feed
+    // 64 FMAs, so the staged rows are re-read nf/4 instead of nf times
+    const int nbk = (nf + 3) / 4, ntile = nbk * (nbk + 1) / 2;
+    for (int e = threadIdx.x; e < ns * ntile; e += blockDim.x) {
+      const int s = e / ntile;
+      int t = e - s * ntile, bi = 0;
+      while (t >= nbk - bi) { t -= nbk - bi; ++bi; }
+      const int bj = bi + t;
+      const float* zs = z + size_t(s) * nf * pitch;
+      const float* ri[4];
+      const float* rj[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ri[k] = zs + min(4 * bi + k, nf - 1) * pitch;
+        rj[k] = zs + min(4 * bj + k, nf - 1) * pitch;
+      }
+      // four interleaved partial sums per pair (columns c % 4), combined as
+      // (p0 + p1) + (p2 + p3): the same rounding as the per-pair kernel
+      float4 acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c = 0; c < dim; c += 4) {
+        float4 x[4], y[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          x[k] = *reinterpret_cast<const float4*>(ri[k] + c);
+          y[k] = *reinterpret_cast<const float4*>(rj[k] + c);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            acc[a][b].x = fmaf(x[a].x, y[b].x, acc[a][b].x);
+            acc[a][b].y = fmaf(x[a].y, y[b].y, acc[a][b].y);
+            acc[a][b].z = fmaf(x[a].z, y[b].z, acc[a][b].z);
+            acc[a][b].w = fmaf(x[a].w, y[b].w, acc[a][b].w);
+          }
+      }
+      float* orow = out + (b0 + s) * ld_out + dim;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = 4 * bi + a, j = 4 * bj + b;
+          if (i < j && j < nf)
+            orow[i * (2 * nf - i - 1) / 2 + (j - i - 1)] =
+                (acc[a][b].x + acc[a][b].y) + (acc[a][b].z + acc[a][b].w);
+        }
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < ns * total_w; e += blockDim.x) {
     const int s = e / total_w, col = e - s * total_w;
     const float* zs = z + size_t(s) * nf * pitch;
@@ -68,22 +131,9 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
       const int pr = pairs[col - int(dim)];
       const float* zi = zs + (pr >> 16) * pitch;
       const float* zj = zs + (pr & 0xffff) * pitch;
-      if (V4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int c = 0; c < dim; c += 4) {
-          const float4 x = *reinterpret_cast<const float4*>(zi + c);
-          const float4 y = *reinterpret_cast<const float4*>(zj + c);
-          a.x = fmaf(x.x, y.x, a.x);
-          a.y = fmaf(x.y, y.y, a.y);
-          a.z = fmaf(x.z, y.z, a.z);
-          a.w = fmaf(x.w, y.w, a.w);
-        }
-        v = (a.x + a.y) + (a.z + a.w);
-      } else {
-        float a = 0.f;
-        for (int c = 0; c < dim; ++c) a = fmaf(zi[c], zj[c], a);
-        v = a;
-      }
+      float a = 0.f;
+      for (int c = 0; c < dim; ++c) a = fmaf(zi[c], zj[c], a);
+      v = a;
     } else {
       v = 0.f;
     }
@@ -100,19 +150,20 @@ interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
   extern __shared__ float4 smem4[];
   float* z = reinterpret_cast<float*>(smem4);
   const int pitch = int(dim) + 4;
-  const int gp = nf + 1;  // pitch of the symmetric gradient matrix
+  const int gp = (nf + 3) & ~3;  // pitch of the symmetric gradient matrix (float4 rows)
   float* G = z + size_t(S) * nf * pitch;
   const int npairs = nf * (nf - 1) / 2;
   const int64_t b0 = int64_t(blockIdx.x) * S;
   const int ns = int(batch - b0 < S ? batch - b0 : S);
   const int id = int(dim);
-  if (V4) {
+  if (V4) {  // cp.async staging (see forward)
     const int nv = id / 4;
     for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
       const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
-      const float4 v = __ldg(reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c);
-      *reinterpret_cast<float4*>(z + (size_t(s) * nf + f) * pitch + 4 * c) = v;
+      cp_async16(z + (size_t(s) * nf + f) * pitch + 4 * c,
+                 reinterpret_cast<const float4*>(fs.feat[f] + (b0 + s) * fs.stride[f]) + c, true);
     }
+    cp_async_commit();
   } else {
     for (int e = threadIdx.x; e < ns * nf * id; e += blockDim.x) {
       const int s = e / (nf * id), r = e - s * nf * id, f = r / id, c = r - f * id;
@@ -124,6 +175,7 @@ interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
     const int s = e / nf, f = e - s * nf;
     G[(size_t(s) * nf + f) * gp + f] = 0.f;
   }
+#pragma unroll 4
   for (int e = threadIdx.x; e < ns * npairs; e += blockDim.x) {
     const int s = e / npairs, p = e - s * npairs;
     int i, j;
@@ -132,31 +184,44 @@ interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
     G[(size_t(s) * nf + i) * gp + j] = g;
     G[(size_t(s) * nf + j) * gp + i] = g;
   }
+  if (V4) cp_async_wait<0>();
   __syncthreads();
   if (V4) {
-    const int nv = id / 4;
-    for (int e = threadIdx.x; e < ns * nf * nv; e += blockDim.x) {
-      const int s = e / (nf * nv), r = e - s * nf * nv, f = r / nv, c = r - f * nv;
+    // 4 features x 4 columns per thread: one float4 of G (symmetric, so row j
+    // holds G[f0..f3][j]) and one float4 of Z feed 16 FMAs
+    const int nv = id / 4, nbk = (nf + 3) / 4;
+    for (int e = threadIdx.x; e < ns * nbk * nv; e += blockDim.x) {
+      const int s = e / (nbk * nv), r = e - s * nbk * nv, fb = r / nv, c = r - fb * nv;
       const float* zs = z + size_t(s) * nf * pitch + 4 * c;
-      const float* gr = G + (size_t(s) * nf + f) * gp;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (f == 0) a = __ldg(reinterpret_cast<const float4*>(gout + (b0 + s) * ld_gout) + c);
+      const float* gs0 = G + size_t(s) * nf * gp + 4 * fb;
+      float4 a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fb == 0) a[0] = __ldg(reinterpret_cast<const float4*>(gout + (b0 + s) * ld_gout) + c);
       for (int j = 0; j < nf; ++j) {
-        const float g = gr[j];
+        const float4 g = *reinterpret_cast<const float4*>(gs0 + j * gp);
         const float4 x = *reinterpret_cast<const float4*>(zs + j * pitch);
-        a.x = fmaf(g, x.x, a.x);
-        a.y = fmaf(g, x.y, a.y);
-        a.z = fmaf(g, x.z, a.z);
-        a.w = fmaf(g, x.w, a.w);
+        const float gk[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          a[k].x = fmaf(gk[k], x.x, a[k].x);
+          a[k].y = fmaf(gk[k], x.y, a[k].y);
+          a[k].z = fmaf(gk[k], x.z, a[k].z);
+          a[k].w = fmaf(gk[k], x.w, a[k].w);
+        }
       }
-      if (f == 0 && mask_f0) {
+      if (fb == 0 && mask_f0) {
         const float4 z0 = *reinterpret_cast<const float4*>(zs);
-        a.x *= z0.x > 0.f ? 1.f : 0.f;
-        a.y *= z0.y > 0.f ? 1.f : 0.f;
-        a.z *= z0.z > 0.f ? 1.f : 0.f;
-        a.w *= z0.w > 0.f ? 1.f : 0.f;
+        a[0].x *= z0.x > 0.f ? 1.f : 0.f;
+        a[0].y *= z0.y > 0.f ? 1.f : 0.f;
+        a[0].z *= z0.z > 0.f ? 1.f : 0.f;
+        a[0].w *= z0.w > 0.f ? 1.f : 0.f;
       }
-      reinterpret_cast<float4*>(gs.feat[f] + (b0 + s) * gs.stride[f])[c] = a;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int f = 4 * fb + k;
+        if (f < nf) reinterpret_cast<float4*>(gs.feat[f] + (b0 + s) * gs.stride[f])[c] = a[k];
+      }
     }
   } else {
     for (int e = threadIdx.x; e < ns * nf * id; e += blockDim.x) {
@@ -243,7 +308,7 @@ extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
   }
   v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
   if (batch == 0) return 0;
-  const size_t extra = size_t(nf) * (nf + 1) * 4;
+  const size_t extra = size_t(nf) * ((nf + 3) & ~3) * 4;
   const int S = pick_samples(nf, dim, batch, extra, 0, 96 * 1024);
   const size_t smem = size_t(S) * (nf * (dim + 4) * 4 + extra);
   DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
