@@ -488,30 +488,21 @@ def run_hybrid(args, c, rank, world, dist):
     P = args.pool
     hbs = rank_batches(c, plan, rank, P, seed=1)
 
-    def to_dev(b):
-        return (torch.as_tensor(b[0].astype(np.float32), device=dev),
-                torch.as_tensor(b[1].astype(np.float32), device=dev),
-                [torch.as_tensor(o, device=dev) for o in b[2]],
-                [torch.as_tensor(i, device=dev) for i in b[3]])
-
-    def to_pin(b):
-        return (torch.as_tensor(b[0].astype(np.float32)).pin_memory(),
-                torch.as_tensor(b[1].astype(np.float32)).pin_memory(),
-                [torch.as_tensor(o).pin_memory() for o in b[2]],
-                [torch.as_tensor(i).pin_memory() for i in b[3]])
-
-    dpool = [to_dev(b) for b in hbs]
-    hpool = [to_pin(b) for b in hbs]
-    h2d = int(np.mean([hp[0].nbytes + hp[1].nbytes + sum(o.nbytes for o in hp[2])
-                       + sum(i.nbytes for i in hp[3]) for hp in hpool]))
+    # the data pipeline packs each batch once into the rank's input-block
+    # layout (pinned host); the device pool holds the same blocks in HBM
+    hpool = [tr.pack(*b) for b in hbs]
+    dpool = [hp.to(dev) for hp in hpool]
+    h2d = int(tr.engine.block_bytes)
     n0 = _lib.launch_count()
-    tr.load(*dpool[0])
+    tr.stage(dpool[0])
     tr.step()
     launches = _lib.launch_count() - n0
+    captured = tr.capture()       # NCCL collectives inside the step graph
     for w in range(args.warmup):
-        tr.load(*dpool[w % P])
-        tr.step()
+        tr.stage(dpool[w % P])
+        tr.step(sync=False)
     torch.cuda.synchronize()
+    tr.check_errors()
     stream = torch.cuda.current_stream()
     K = args.steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -523,10 +514,11 @@ def run_hybrid(args, c, rank, world, dist):
     for s in range(K):
         flush.fill_(s & 0xff)
         starts[s].record(stream)
-        tr.load(*dpool[s % P])
-        tr.step()
+        tr.stage(dpool[s % P])
+        tr.step(sync=False)     # no host sync inside the step
         ends[s].record(stream)
     torch.cuda.synchronize()
+    tr.check_errors()
     dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
     t = torch.tensor([ms], device=dev)
@@ -536,12 +528,15 @@ def run_hybrid(args, c, rank, world, dist):
     # e2e from pinned host buffers
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
+    res_host = torch.zeros((K, 3), dtype=torch.float32).pin_memory()
     e0.record(stream)
     for s in range(K):
-        tr.load(*hpool[s % P])
-        r = tr.step()
+        tr.stage(hpool[s % P])        # one H2D copy of the packed batch
+        tr.step(sync=False)
+        res_host[s].copy_(tr.engine.stats, non_blocking=True)   # D2H of the step result
     e1.record(stream)
     torch.cuda.synchronize()
+    r = tr.result()
     clk.__exit__()
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -556,7 +551,8 @@ def run_hybrid(args, c, rank, world, dist):
             "config": {"workload": c["name"], "global_batch": Bg, "per_gpu_batch": B,
                        "parallelism": f"hybrid: tables model-parallel {plan.table_assignment}, "
                                       f"MLP data-parallel x{world}",
-                       "l2": "flushed (256 MiB write) between timed steps"},
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "graph": captured},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 12},
             "gpu_launches": launches * K, "loss_last": r.loss,
@@ -574,6 +570,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--hybrid", action="store_true",
+                    help="run the multi-process hybrid path even at N=1 (under torchrun)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-batch", type=int, default=256)
     args = ap.parse_args()
@@ -585,12 +583,12 @@ def main():
     if args.impl == "reference":
         run_reference(args, c, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.hybrid:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl")
-    if world > 1:
+    if world > 1 or args.hybrid:
         run_hybrid(args, c, rank, world, dist)
     else:
         run_ours(args, c, rank, world, dist)

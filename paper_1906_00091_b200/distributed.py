@@ -206,11 +206,21 @@ class RankEngine:
         self.caps = [max(1, int(c)) for c in caps]
         self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
 
-        # inputs
-        self.x = torch.zeros((Bl, ceil4(cfg.dense_dim)), **f32)
-        self.labels = torch.zeros(Bl, **f32)
-        self.offsets = torch.zeros((max(To, 1), Bg + 1), dtype=torch.int64, device=dev)
-        self.indices = torch.zeros(max(int(self.cap_base[-1]), 1), dtype=torch.int64, device=dev)
+        # inputs: ONE contiguous block [x | labels | offsets | indices] so a
+        # step's inputs move with one copy (pack() builds the same layout in
+        # pinned host memory); x / labels / offsets / indices are views
+        a16 = lambda n: (n + 15) // 16 * 16
+        lay, o = {}, 0
+        for name, nbytes in (("x", Bl * ceil4(cfg.dense_dim) * 4), ("labels", Bl * 4),
+                             ("offsets", max(To, 1) * (Bg + 1) * 8),
+                             ("indices", max(int(self.cap_base[-1]), 1) * 8)):
+            lay[name] = (o, nbytes)
+            o = a16(o + nbytes)
+        self.block_layout, self.block_bytes = lay, o
+        self.block = torch.zeros(o, dtype=torch.uint8, device=dev)
+        v = self._views(self.block)
+        self.x, self.labels = v["x"], v["labels"]
+        self.offsets, self.indices = v["offsets"], v["indices"]
 
         # exchange buffers
         self.send = torch.zeros(max(layout.send_numel, 1), **f32)
@@ -264,22 +274,60 @@ class RankEngine:
         self._gfeat = (C.c_void_p * self.nf)(*[p for p, _ in gfeats])
         self._gstride = (C.c_int64 * self.nf)(*[s for _, s in gfeats])
 
+    def _views(self, blk):
+        lay, To = self.block_layout, max(len(self.own), 1)
+
+        def view(name, dtype, shape):
+            o, n = lay[name]
+            return blk[o:o + n].view(dtype).view(*shape)
+        return {"x": view("x", torch.float32, (self.Bl, ceil4(self.cfg.dense_dim))),
+                "labels": view("labels", torch.float32, (self.Bl,)),
+                "offsets": view("offsets", torch.int64, (To, self.Bg + 1)),
+                "indices": view("indices", torch.int64, (max(int(self.cap_base[-1]), 1),))}
+
+    def pack(self, dense_local, labels_local, offsets_owned, indices_owned):
+        """This rank's batch in the input-block layout, in pinned host memory
+        (done once per batch by the data pipeline)."""
+        blk = torch.zeros(self.block_bytes, dtype=torch.uint8).pin_memory()
+        v = self._views(blk)
+        v["x"][:, :self.cfg.dense_dim].copy_(torch.as_tensor(np.asarray(dense_local, np.float32)))
+        v["labels"].copy_(torch.as_tensor(np.asarray(labels_local, np.float32)))
+        for j in range(len(self.own)):
+            i = np.asarray(indices_owned[j], np.int64)
+            if i.size > self.caps[j]:
+                raise OverflowError(f"table {self.own[j]}: {i.size} indices exceed "
+                                    f"capacity {self.caps[j]}")
+            v["offsets"][j].copy_(torch.as_tensor(np.asarray(offsets_owned[j], np.int64)))
+            cb = int(self.cap_base[j])
+            v["indices"][cb:cb + i.size].copy_(torch.as_tensor(i))
+        self._host_indices = indices_owned
+        return blk
+
+    def stage(self, packed: torch.Tensor):
+        """One copy of a packed block (pinned host or device) into the inputs."""
+        self.block.copy_(packed, non_blocking=True)
+
     # ------------------------------------------------------------------
     def load(self, dense_local, labels_local, offsets_owned, indices_owned):
         """dense/labels: this rank's shard; offsets/indices: one global-batch
         bag set per OWNED table (host arrays or device tensors)."""
-        from .trainer import _to_dev, _to_dev_f32
-        self.x[:, :self.cfg.dense_dim].copy_(_to_dev_f32(dense_local, self.dev))
-        self.labels.copy_(_to_dev_f32(labels_local, self.dev))
+        # copy_ straight from the source: pinned host tensors move with an
+        # async H2D copy on the current stream (no host synchronisation)
+        def src(a, dtype):
+            if isinstance(a, torch.Tensor):
+                return a if a.dtype == dtype else a.to(dtype)
+            return torch.as_tensor(np.asarray(a)).to(dtype)
+        self.x[:, :self.cfg.dense_dim].copy_(src(dense_local, torch.float32), non_blocking=True)
+        self.labels.copy_(src(labels_local, torch.float32), non_blocking=True)
         for j in range(len(self.own)):
             i = indices_owned[j]
             n = int(i.shape[0])
             if n > self.caps[j]:
                 raise OverflowError(f"table {self.own[j]}: {n} indices exceed "
                                     f"capacity {self.caps[j]}")
-            self.offsets[j].copy_(_to_dev(offsets_owned[j], torch.int64, self.dev))
+            self.offsets[j].copy_(src(offsets_owned[j], torch.int64), non_blocking=True)
             cb = int(self.cap_base[j])
-            self.indices[cb:cb + n].copy_(_to_dev(i, torch.int64, self.dev))
+            self.indices[cb:cb + n].copy_(src(i, torch.int64), non_blocking=True)
         self._host_indices = indices_owned
 
     # ------------------------------------------------------------------
@@ -378,12 +426,40 @@ class RankEngine:
         """err_flag <- any rank raised (after the stats allreduce)."""
         self.err_flag.copy_((self.stats[2:3] > 0).to(torch.int32))
 
-    def phase_c(self, stream=None):
+    def prepare_sparse_backward(self, stream=None):
+        """Index-only half of the sparse backward (keys + radix sort of the
+        owned tables' lookups); valid as soon as the indices are loaded, so
+        the trainer runs it on a side stream under the dense work."""
+        To = len(self.own)
+        if To:
+            _lib.call("dlrm_emb_bwd_prepare", self.d, C.cast(self._descs, C.c_void_p), To,
+                      self.Bg, self.total_rows, _lib.ptr(self.emb_ws), self.emb_ws_bytes,
+                      _lib.stream_handle(stream))
+
+    def apply_sparse(self, stream=None):
+        """Owned tables: segmented fold of the received gradients + row SGD
+        (skipped on device when err_flag is set)."""
+        To = len(self.own)
+        if To:
+            P = _lib.ptr
+            _lib.call("dlrm_emb_bwd_apply_sgd", P(self.W_own), self.d,
+                      C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.grecv),
+                      To * self.d, self.lr, P(self.err_flag), self.total_rows,
+                      P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(stream))
+
+    def sgd_dense(self, stream=None):
+        P = _lib.ptr
+        _lib.call("dlrm_sgd_dense", P(self.params), P(self.grads),
+                  self.params.numel(), self.lr, P(self.err_flag), _lib.stream_handle(stream))
+
+    def phase_c(self, stream=None, prepared=False):
         s = _lib.stream_handle(stream)
         P = _lib.ptr
         To = len(self.own)
+        if To and not prepared:
+            self.prepare_sparse_backward(stream)
         if To:
-            _lib.call("dlrm_emb_bwd_sgd", P(self.W_own), self.d,
+            _lib.call("dlrm_emb_bwd_apply_sgd", P(self.W_own), self.d,
                       C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.grecv),
                       To * self.d, self.lr, P(self.err_flag), self.total_rows,
                       P(self.emb_ws), self.emb_ws_bytes, s)
@@ -417,35 +493,100 @@ class HybridTrainer:
         self.ex = NcclExchange(self.layout, group, ar_group)
         self.rank = rank
         self.comm_stream = torch.cuda.Stream()
+        self.side = torch.cuda.Stream()
+        self.graph = None
 
     def load(self, *args):
         self.engine.load(*args)
 
-    def step(self) -> StepResult:
+    def pack(self, *args):
+        return self.engine.pack(*args)
+
+    def stage(self, packed):
+        self.engine.stage(packed)
+
+    def capture(self):
+        """Record the step (both all-to-alls and the allreduces included:
+        NCCL collectives are graph-capturable) into a CUDA graph; later
+        ``step()`` calls replay it.  Every rank must capture, and then replay
+        in lockstep.  Returns False (and keeps eager steps) if capture fails."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                self._issue()
+        except Exception:
+            self.graph = None
+            torch.cuda.synchronize()
+            return False
+        self.graph = g
+        return True
+
+    def step(self, sync: bool = True):
+        """One hybrid training step.  ``sync=False`` issues the whole step
+        without any host synchronisation (ranks skip their updates on device
+        if any rank saw a bad index) and returns None; call
+        ``check_errors()`` / ``result()`` later to raise / read it."""
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._issue()
+        if not sync:
+            return None
+        self.check_errors()
+        return self.result()
+
+    def _issue(self):
         e, ex = self.engine, self.ex
         cur = torch.cuda.current_stream()
+        # sort the owned lookups on the side stream while the step runs
+        fork = torch.cuda.Event()
+        fork.record(cur)
+        self.side.wait_event(fork)
+        e.prepare_sparse_backward(self.side)
         e.phase_a()
         ex.forward(e.send, e.recv)
         e.phase_b_forward()
-        e.phase_b_top_backward()
-        # top-MLP gradients reduce on the second communicator while the
-        # interaction / bottom backward and the reverse exchange run
-        top = e.grads[e.split_at:]
-        h_top = ex.allreduce_async(top)
-        e.phase_b_interaction_backward()
-        ex.backward(e.gsend, e.grecv)
-        e.phase_b_bottom_backward()
-        h_bot = ex.allreduce_async(e.grads[:e.split_at])
+        # loss, correct count and this rank's index-error flag are all known
+        # after the head: reduce them now, so every rank can skip its updates
+        # (on device) before any update is issued
         e.publish_error()
         ex.allreduce(e.stats)
         e.adopt_global_error()
+        e.phase_b_top_backward()
+        # top-MLP gradients reduce on the second communicator while the
+        # interaction / bottom backward and the reverse exchange run
+        h_top = ex.allreduce_async(e.grads[e.split_at:])
+        e.phase_b_interaction_backward()
+        ex.backward(e.gsend, e.grecv)
+        # owned-table fold + row update on the side stream, concurrently
+        # with the bottom MLP backward
+        got = torch.cuda.Event()
+        got.record(cur)
+        self.side.wait_event(got)
+        e.apply_sparse(self.side)
+        applied = torch.cuda.Event()
+        applied.record(self.side)
+        e.phase_b_bottom_backward()
+        h_bot = ex.allreduce_async(e.grads[:e.split_at])
         h_top.wait()
         h_bot.wait()
-        e.phase_c()
+        e.sgd_dense()
+        cur.wait_event(applied)
+
+    def check_errors(self):
+        """Raise for the last step if any rank saw an out-of-range index
+        (synchronises with the device)."""
+        e = self.engine
         if float(e.stats[2].item()) > 0:
             err = e.local_error()
             if err is not None:
                 raise LookupIndexError(*err)
             raise RuntimeError("a peer rank reported an out-of-range index")
+
+    def result(self) -> StepResult:
+        """StepResult of the last step (loss / accuracy over the global
+        batch; synchronises with the device)."""
+        e = self.engine
         st = e.stats.cpu()
         return StepResult(float(st[0]) / e.Bg, float(st[1]) / e.Bg, e.prob.clone())

@@ -93,3 +93,55 @@ def test_bad_index_raises_with_device_and_mutates_nothing(golden):
         tr.step(hb.dense.astype(np.float32), sparse, hb.labels.astype(np.float32))
     for x, y in zip(before, arrays_of(b, t, tr.tables)):
         assert np.array_equal(x, y)
+
+
+def test_hybrid_trainer_nccl_one_process(golden):
+    """HybridTrainer over a real NCCL communicator (one process, one GPU):
+    the all-to-alls, the overlapped allreduces, the no-sync step and the
+    deferred error check run through the multi-process code path and give
+    the same losses as the fused single-device step."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1906_00091_b200.distributed import HybridTrainer
+
+    fx = golden("traj_c1s.npz")
+    c, batches = traj_inputs(fx)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        model = build(c)
+        plan = make_plan(model.config, c["batch"], 1)
+        caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
+        tr = HybridTrainer(model, plan, 0, caps, lr=c["lr"],
+                           ar_group=dist.new_group([0]))
+        ref_model = build(c)
+        opt = Sgd(c["lr"])
+        for k, hb in enumerate(batches):
+            if k < 2:   # eager steps through load()
+                tr.load(hb.dense.astype(np.float32), hb.labels.astype(np.float32),
+                        hb.offsets, hb.indices)
+            else:       # packed input block + the captured step graph
+                tr.stage(tr.pack(hb.dense, hb.labels, hb.offsets, hb.indices))
+            if k == 2:
+                assert tr.capture()
+            if k % 2:
+                r = tr.step()
+            else:
+                assert tr.step(sync=False) is None
+                tr.check_errors()
+                r = tr.result()
+            sparse = [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)]
+            s = train_step(ref_model, hb.dense.astype(np.float32), sparse, hb.labels, opt)
+            assert abs(r.loss - s.loss) <= 1e-6 * abs(s.loss), (k, r.loss, s.loss)
+        # a graph holding NCCL work must be released before the communicator
+        tr.graph = None
+        del tr
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
