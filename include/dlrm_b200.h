@@ -51,6 +51,25 @@ typedef struct {
   int64_t table_id;        /* reported in LookupIndexError                  */
 } dlrm_table_desc;
 
+/* Parameter update rule applied by the fused *_upd / *_apply entry points
+ * (ref optim.py).  For every updated fp32 parameter p with gradient g:
+ *   DLRM_UPD_SGD      p -= fl(lr*g)                                (31-46)
+ *   DLRM_UPD_ADAGRAD  G += fl(g*g);  p -= fl(fl(lr*g) / fl(sqrt(G) + eps))
+ *                                                                 (49-73)
+ * with G the accumulator at address &p + accum_delta (floats): the caller
+ * keeps one accumulator buffer with the SAME layout as each parameter buffer
+ * (the tables' W_all, the flat MLP buffer) and passes the pointer distance.
+ * Products / quotients are rounded before the subtraction exactly like numpy
+ * (no FMA contraction). */
+#define DLRM_UPD_SGD 0
+#define DLRM_UPD_ADAGRAD 1
+typedef struct {
+  int32_t kind;        /* DLRM_UPD_SGD or DLRM_UPD_ADAGRAD */
+  float lr;
+  float eps;           /* Adagrad only */
+  int64_t accum_delta; /* Adagrad only: accumulator = parameter + delta */
+} dlrm_update;
+
 /* ---- embedding bags (north_star subsystem 1) --------------------------- */
 
 /* Reset the error records: err_pos[0..nt) = INT64_MAX, *err_flag = 0. */
@@ -102,6 +121,14 @@ int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tab
                            int64_t grad_stride, float lr, const int32_t* err_flag,
                            int64_t total_rows, void* workspace, size_t ws_bytes,
                            dlrm_stream_t stream);
+/* apply with any update rule (SGD or Adagrad; ref adagrad_step_rows,
+ * optim.py:62-73): the rule is applied once per touched row to its folded
+ * gradient; the row accumulators live at W_all + upd->accum_delta. */
+int dlrm_emb_bwd_apply(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                       int32_t nt, int64_t num_bags, const float* grad,
+                       int64_t grad_stride, const dlrm_update* upd,
+                       const int32_t* err_flag, int64_t total_rows, void* workspace,
+                       size_t ws_bytes, dlrm_stream_t stream);
 
 /* lookup_backward parity path for ONE table: coalesced SparseRowGrad.
  * rows_out[u] ascending unique local rows, values_out[u*dim..] their folded
@@ -120,6 +147,9 @@ int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
 int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
                   const float* values, int64_t n, float lr,
                   dlrm_stream_t stream);
+/* rows update with any rule (ref sgd_step_rows / adagrad_step_rows). */
+int dlrm_update_rows(float* W, int64_t dim, const int64_t* rows, const float* values,
+                     int64_t n, const dlrm_update* upd, dlrm_stream_t stream);
 
 /* ---- dot interaction (north_star subsystem 2) -------------------------- */
 
@@ -180,6 +210,14 @@ int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X,
                            float* W_upd, int64_t ldw, float* b_upd, float lr,
                            const int32_t* err_flag, void* workspace,
                            size_t ws_bytes, dlrm_stream_t stream);
+/* the same with any update rule for W_upd / b_upd (accumulators at
+ * parameter + upd->accum_delta). */
+int dlrm_linear_bwd_weight_upd(const float* gZ, int64_t ldg, const float* X,
+                               int64_t ldx, int64_t M, int64_t N, int64_t K,
+                               float* dW, int64_t lddw, float* db, float* W_upd,
+                               int64_t ldw, float* b_upd, const dlrm_update* upd,
+                               const int32_t* err_flag, void* workspace,
+                               size_t ws_bytes, dlrm_stream_t stream);
 
 /* ---- loss head (last top layer, N = 1) --------------------------------- */
 
@@ -204,6 +242,12 @@ int dlrm_head_bwd(const float* A, int64_t lda, const float* w, const float* g,
                   float* b_upd, float lr,
                   const int32_t* err_flag, void* workspace, size_t ws_bytes,
                   dlrm_stream_t stream);
+int dlrm_head_bwd_upd(const float* A, int64_t lda, const float* w, const float* g,
+                      int64_t M, int64_t K, float* dA, int64_t ldda,
+                      int32_t relu_mask, float* dw, float* db, float* w_upd,
+                      float* b_upd, const dlrm_update* upd,
+                      const int32_t* err_flag, void* workspace, size_t ws_bytes,
+                      dlrm_stream_t stream);
 
 /* out[m, n] = g[m, n] * (act[m, n] > 0)   (ref activation_grad relu,
  * dense.py:110-120, applied as in model.py:177). */
@@ -217,6 +261,10 @@ int dlrm_relu_grad(const float* g, int64_t ldg, const float* act, int64_t lda,
  * skipped when err_flag != NULL and *err_flag != 0. */
 int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
                    const int32_t* err_flag, dlrm_stream_t stream);
+/* dense update with any rule (ref sgd_step / adagrad_step, optim.py:31-59);
+ * skipped when *err_flag. */
+int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* upd,
+                      const int32_t* err_flag, dlrm_stream_t stream);
 
 /* ---- misc --------------------------------------------------------------- */
 

@@ -67,3 +67,22 @@ def sgd_rows(W, rows, vals, lr):
 
 def sgd_dense(p, g, lr):
     return np.asarray(p, f32) - f32(lr) * np.asarray(g, f32)
+
+
+def adagrad_dense(p, g, accum, lr, eps):
+    """float32 restatement of ref adagrad_step (optim.py:49-59), op for op:
+    G = G + g*g; p = p - (lr*g) / (sqrt(G) + eps).  Returns (p, G)."""
+    g = np.asarray(g, f32)
+    G = (np.asarray(accum, f32) + g * g).astype(f32)
+    upd = (f32(lr) * g) / (np.sqrt(G) + f32(eps))
+    return (np.asarray(p, f32) - upd).astype(f32), G
+
+
+def adagrad_rows(W, rows, vals, accum, lr, eps):
+    """float32 restatement of ref adagrad_step_rows (optim.py:62-73)."""
+    W = np.array(W, f32, copy=True)
+    A = np.array(accum, f32, copy=True)
+    if rows.size:
+        W[rows], A[rows] = adagrad_dense(W[rows], vals, A[rows], lr, eps)
+    return W, A
+

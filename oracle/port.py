@@ -245,8 +245,31 @@ def bce_from_logits(z, y):
 # --------------------------------------------------------------------------
 # the training step  (ref parallel.py:250-287, optim.py:31-46)
 
-def train_step(model, dense, offsets, indices, labels, lr, weights=None):
-    """One SGD step in place on ``model``; returns (loss, accuracy, probs)."""
+def adagrad_update(param, grad, accum, lr, eps):
+    """ref adagrad_step (optim.py:49-59): G += g*g; p -= lr*g / (sqrt(G)+eps)."""
+    accum += grad * grad
+    param -= lr * grad / (np.sqrt(accum) + eps)
+
+
+def adagrad_update_rows(W, rows, vals, accum, lr, eps):
+    """ref adagrad_step_rows (optim.py:62-73)."""
+    accum[rows] += vals * vals
+    W[rows] -= lr * vals / (np.sqrt(accum[rows]) + eps)
+
+
+def adagrad_state(model):
+    """Zero accumulators with the shapes of every parameter (ref
+    AdagradState.for_mlp + the lazily created per-table accumulators)."""
+    return {"bottom": [(np.zeros_like(w), np.zeros_like(b)) for w, b, _ in model["bottom"]],
+            "top": [(np.zeros_like(w), np.zeros_like(b)) for w, b, _ in model["top"]],
+            "tables": [np.zeros_like(W) for W in model["tables"]]}
+
+
+def train_step(model, dense, offsets, indices, labels, lr, weights=None,
+               adagrad=None, eps=1e-10):
+    """One training step in place on ``model``; returns (loss, accuracy,
+    probs).  SGD, or Adagrad when ``adagrad`` is a state from
+    ``adagrad_state`` (ref Adagrad.apply, optim.py:135-140)."""
     weights = weights or [None] * len(model["tables"])
     z0, b_in, b_pre = mlp_forward(model["bottom"], dense)
     embs = [lookup(W, o, i, w, t) for t, (W, o, i, w) in
@@ -264,13 +287,23 @@ def train_step(model, dense, offsets, indices, labels, lr, weights=None):
     sparse = [lookup_backward(W, o, i, g, w, t) for t, (W, o, i, g, w) in
               enumerate(zip(model["tables"], offsets, indices, g_embs,
                             weights))]
-    for layers, dws, dbs in ((model["bottom"], b_dw, b_db),
-                             (model["top"], t_dw, t_db)):
-        for (w, b, _), dw, db in zip(layers, dws, dbs):
-            w -= lr * dw
-            b -= lr * db
-    for W, (rows, vals) in zip(model["tables"], sparse):
-        if rows.size:
-            W[rows] -= lr * vals
+    if adagrad is not None:
+        for which, layers, dws, dbs in (("bottom", model["bottom"], b_dw, b_db),
+                                        ("top", model["top"], t_dw, t_db)):
+            for (w, b, _), dw, db, (aw, ab) in zip(layers, dws, dbs, adagrad[which]):
+                adagrad_update(w, dw, aw, lr, eps)
+                adagrad_update(b, db, ab, lr, eps)
+        for W, (rows, vals), acc in zip(model["tables"], sparse, adagrad["tables"]):
+            if rows.size:
+                adagrad_update_rows(W, rows, vals, acc, lr, eps)
+    else:
+        for layers, dws, dbs in ((model["bottom"], b_dw, b_db),
+                                 (model["top"], t_dw, t_db)):
+            for (w, b, _), dw, db in zip(layers, dws, dbs):
+                w -= lr * dw
+                b -= lr * db
+        for W, (rows, vals) in zip(model["tables"], sparse):
+            if rows.size:
+                W[rows] -= lr * vals
     acc = float(np.mean((prob > 0.5) == (labels > 0.5)))
     return loss, acc, prob

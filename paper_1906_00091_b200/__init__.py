@@ -17,7 +17,8 @@ from .model import (DlrmCache, DlrmConfig, DlrmGradients, DlrmModel, MlpCache,
                     embedding_param_count, init_mlp, init_model, interact,
                     interact_backward, interaction_width, mlp_backward,
                     mlp_forward, mlp_param_count, param_count)
-from .optim import Sgd, make_optimizer, sgd_step, sgd_step_rows
+from .optim import (Adagrad, AdagradState, Sgd, adagrad_step, adagrad_step_rows,
+                    make_optimizer, sgd_step, sgd_step_rows)
 from .trainer import StepEngine, StepResult
 from .parallel import (CommLog, DevicePlan, ParallelTrainer, ShuffleSlice,
                        allreduce,

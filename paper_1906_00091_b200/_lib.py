@@ -27,6 +27,14 @@ class TableDesc(C.Structure):
                 ("capacity", _i64), ("table_id", _i64)]
 
 
+class Update(C.Structure):
+    """dlrm_update: SGD / Adagrad rule; accumulator = parameter + accum_delta."""
+    _fields_ = [("kind", _i32), ("lr", _f32), ("eps", _f32), ("accum_delta", _i64)]
+
+
+UPD_SGD, UPD_ADAGRAD = 0, 1
+
+
 class Features(C.Structure):
     _fields_ = [("feat", _vp * MAX_FEATURES),
                 ("feat_stride", _i64 * MAX_FEATURES)]
@@ -40,6 +48,15 @@ _SIGS = {
     "dlrm_emb_bwd_prepare": [_i64, _vp, _i32, _i64, _i64, _vp, _sz, _vp],
     "dlrm_emb_bwd_apply_sgd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _f32,
                                _vp, _i64, _vp, _sz, _vp],
+    "dlrm_emb_bwd_apply": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _i64,
+                           _vp, _sz, _vp],
+    "dlrm_update_rows": [_vp, _i64, _vp, _vp, _i64, _vp, _vp],
+    "dlrm_linear_bwd_weight_upd": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp,
+                                   _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                                   _sz, _vp],
+    "dlrm_head_bwd_upd": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp,
+                          _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+    "dlrm_update_dense": [_vp, _vp, _i64, _vp, _vp, _vp],
     "dlrm_emb_bwd_coalesce": [_i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _sz, _vp],
     "dlrm_sgd_rows": [_vp, _i64, _vp, _vp, _i64, _f32, _vp],

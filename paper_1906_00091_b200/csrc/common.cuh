@@ -77,6 +77,48 @@ __device__ __forceinline__ void pdl_entry() {
 
 bool pdl_enabled();
 
+// ---- parameter updates (dlrm_update, see the header) ----------------------
+struct Upd {
+  int32_t kind;
+  float lr;
+  float eps;
+  int64_t delta;  // accumulator = parameter + delta (floats), Adagrad only
+};
+
+inline Upd sgd_rule(float lr) { return Upd{DLRM_UPD_SGD, lr, 0.f, 0}; }
+inline Upd upd_rule(const dlrm_update* u) { return Upd{u->kind, u->lr, u->eps, u->accum_delta}; }
+
+// new value of parameter w (stored at p) for gradient g; Adagrad also
+// updates the accumulator at p + delta
+__device__ __forceinline__ float upd_apply(const Upd& u, float* p, float w, float g) {
+  if (u.kind == DLRM_UPD_ADAGRAD) {
+    float* a = p + u.delta;
+    const float G = __fadd_rn(*a, __fmul_rn(g, g));
+    *a = G;
+    return __fsub_rn(w, __fdiv_rn(__fmul_rn(u.lr, g), __fadd_rn(__fsqrt_rn(G), u.eps)));
+  }
+  return __fsub_rn(w, __fmul_rn(u.lr, g));
+}
+
+__device__ __forceinline__ float4 upd_apply4(const Upd& u, float* p, float4 w, float4 g) {
+  if (u.kind == DLRM_UPD_ADAGRAD) {
+    float4* ap = reinterpret_cast<float4*>(p + u.delta);
+    float4 a = *ap;
+    a.x = __fadd_rn(a.x, __fmul_rn(g.x, g.x));
+    a.y = __fadd_rn(a.y, __fmul_rn(g.y, g.y));
+    a.z = __fadd_rn(a.z, __fmul_rn(g.z, g.z));
+    a.w = __fadd_rn(a.w, __fmul_rn(g.w, g.w));
+    *ap = a;
+    return make_float4(
+        __fsub_rn(w.x, __fdiv_rn(__fmul_rn(u.lr, g.x), __fadd_rn(__fsqrt_rn(a.x), u.eps))),
+        __fsub_rn(w.y, __fdiv_rn(__fmul_rn(u.lr, g.y), __fadd_rn(__fsqrt_rn(a.y), u.eps))),
+        __fsub_rn(w.z, __fdiv_rn(__fmul_rn(u.lr, g.z), __fadd_rn(__fsqrt_rn(a.z), u.eps))),
+        __fsub_rn(w.w, __fdiv_rn(__fmul_rn(u.lr, g.w), __fadd_rn(__fsqrt_rn(a.w), u.eps))));
+  }
+  return make_float4(__fsub_rn(w.x, __fmul_rn(u.lr, g.x)), __fsub_rn(w.y, __fmul_rn(u.lr, g.y)),
+                     __fsub_rn(w.z, __fmul_rn(u.lr, g.z)), __fsub_rn(w.w, __fmul_rn(u.lr, g.w)));
+}
+
 // cp.async helpers (16 B per lane, zero fill when !ok)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));

@@ -50,14 +50,13 @@ __device__ __forceinline__ float4 vadd(float4 a, float4 b) {
                      __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
 __device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float4 vsgd(float4 w, float lr, float4 g) {
-  return make_float4(__fsub_rn(w.x, __fmul_rn(lr, g.x)),
-                     __fsub_rn(w.y, __fmul_rn(lr, g.y)),
-                     __fsub_rn(w.z, __fmul_rn(lr, g.z)),
-                     __fsub_rn(w.w, __fmul_rn(lr, g.w)));
+// row update (SGD / Adagrad, see dlrm_update): new value of the parameter
+// vector stored at p whose current value is w
+__device__ __forceinline__ float4 vupd(const Upd& u, float4* p, float4 w, float4 g) {
+  return upd_apply4(u, reinterpret_cast<float*>(p), w, g);
 }
-__device__ __forceinline__ float vsgd(float w, float lr, float g) {
-  return __fsub_rn(w, __fmul_rn(lr, g));
+__device__ __forceinline__ float vupd(const Upd& u, float* p, float w, float g) {
+  return upd_apply(u, p, w, g);
 }
 template <typename V>
 __device__ __forceinline__ V vzero();
@@ -590,8 +589,8 @@ struct FoldArgs {
   uint32_t sentinel;
   const float* grad;
   int64_t grad_stride;
-  float* W;  // SGD mode
-  float lr;
+  float* W;  // update mode
+  Upd upd;
   const int32_t* err_flag;
   const uint32_t* uid;  // coalesce mode
   int64_t* rows_out;
@@ -692,7 +691,7 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const int64_t c = lane + int64_t(v) * LPB;
-        if (c < nvec) wrow[c] = vsgd(wcur[v], fa.lr, acc[v]);
+        if (c < nvec) wrow[c] = vupd(fa.upd, wrow + c, wcur[v], acc[v]);
       }
     }
   };
@@ -827,7 +826,7 @@ emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
       if (c == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
     } else {
       float* w = fa.W + int64_t(row) * dim + c;
-      *w = __fsub_rn(*w, __fmul_rn(fa.lr, acc));
+      *w = upd_apply(fa.upd, w, *w, acc);
     }
   }
   }  // runs (grid-stride)
@@ -844,7 +843,7 @@ template <int VEC>
 __global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
                                 const int64_t* __restrict__ rows,
                                 const float* __restrict__ values, int64_t n,
-                                float lr) {
+                                Upd u) {
   pdl_entry();
   using V = typename VecT<VEC>::T;
   const int64_t nvec = dim / VEC;
@@ -853,7 +852,7 @@ __global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
   const int64_t i = e / nvec, c = e - i * nvec;
   V* w = reinterpret_cast<V*>(W + rows[i] * dim) + c;
   const V g = reinterpret_cast<const V*>(values + i * dim)[c];
-  *w = vsgd(*w, lr, g);
+  *w = vupd(u, w, *w, g);
 }
 
 // Hot rows (deferred long runs) are reduced in three steps so that a single
@@ -998,7 +997,7 @@ seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
       if (c == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
     } else {
       float* w = fa.W + int64_t(row) * dim + c;
-      *w = __fsub_rn(*w, __fmul_rn(fa.lr, v));
+      *w = upd_apply(fa.upd, w, *w, v);
     }
   }
   }  // runs (grid-stride)
@@ -1356,11 +1355,12 @@ extern "C" int dlrm_emb_bwd_prepare(int64_t dim, const dlrm_table_desc* tables, 
                     p.end_bit, as_stream(stream));
 }
 
-extern "C" int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
-                                      int32_t nt, int64_t num_bags, const float* grad,
-                                      int64_t grad_stride, float lr, const int32_t* err_flag,
-                                      int64_t total_rows, void* workspace, size_t ws_bytes,
-                                      dlrm_stream_t stream) {
+namespace dlrm {
+namespace {
+int emb_apply(float* W_all, int64_t dim, const dlrm_table_desc* tables, int32_t nt,
+              int64_t num_bags, const float* grad, int64_t grad_stride, const Upd& u,
+              const int32_t* err_flag, int64_t total_rows, void* workspace, size_t ws_bytes,
+              dlrm_stream_t stream) {
   static thread_local TableSet ts;
   BwdPlan p;
   if (int rc = bwd_plan(ts, tables, nt, dim, total_rows, workspace, ws_bytes, &p)) return rc;
@@ -1375,12 +1375,36 @@ extern "C" int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_tabl
   fa.grad = grad;
   fa.grad_stride = grad_stride;
   fa.W = W_all;
-  fa.lr = lr;
+  fa.upd = u;
   fa.err_flag = err_flag;
   bool v4 = vec4_ok(dim, W_all, grad_stride, 0) &&
-            (reinterpret_cast<uintptr_t>(grad) % 16) == 0;
+            (reinterpret_cast<uintptr_t>(grad) % 16) == 0 &&
+            (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0);
   for (int i = 0; i < nt && v4; ++i) v4 = tables[i].out_offset % 4 == 0;
   return run_fold<false>(fa, ts, dim, v4, ws, p.L, as_stream(stream));
+}
+}  // namespace
+}  // namespace dlrm
+
+extern "C" int dlrm_emb_bwd_apply_sgd(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                                      int32_t nt, int64_t num_bags, const float* grad,
+                                      int64_t grad_stride, float lr, const int32_t* err_flag,
+                                      int64_t total_rows, void* workspace, size_t ws_bytes,
+                                      dlrm_stream_t stream) {
+  return emb_apply(W_all, dim, tables, nt, num_bags, grad, grad_stride, sgd_rule(lr), err_flag,
+                   total_rows, workspace, ws_bytes, stream);
+}
+
+extern "C" int dlrm_emb_bwd_apply(float* W_all, int64_t dim, const dlrm_table_desc* tables,
+                                  int32_t nt, int64_t num_bags, const float* grad,
+                                  int64_t grad_stride, const dlrm_update* upd,
+                                  const int32_t* err_flag, int64_t total_rows, void* workspace,
+                                  size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(upd->eps >= 0.f, "eps must be nonnegative");
+  return emb_apply(W_all, dim, tables, nt, num_bags, grad, grad_stride, upd_rule(upd), err_flag,
+                   total_rows, workspace, ws_bytes, stream);
 }
 
 extern "C" int dlrm_emb_bwd_sgd(float* W_all, int64_t dim,
@@ -1454,20 +1478,38 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
   return run_fold<true>(fa, ts, dim, v4, ws, L, s);
 }
 
-extern "C" int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
-                             const float* values, int64_t n, float lr,
-                             dlrm_stream_t stream) {
-  DLRM_REQUIRE(dim >= 1 && n >= 0, "bad sgd_rows arguments");
+namespace dlrm {
+namespace {
+int update_rows(float* W, int64_t dim, const int64_t* rows, const float* values, int64_t n,
+                const Upd& u, dlrm_stream_t stream) {
+  DLRM_REQUIRE(dim >= 1 && n >= 0, "bad row-update arguments");
   if (n == 0) return 0;
   cudaStream_t s = as_stream(stream);
   const bool v4 = vec4_ok(dim, W, dim, 0) &&
-                  (reinterpret_cast<uintptr_t>(values) % 16) == 0;
+                  (reinterpret_cast<uintptr_t>(values) % 16) == 0 &&
+                  (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0);
   if (v4) {
     const int64_t e = n * (dim / 4);
-    launch(sgd_rows_kernel<4>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, lr);
+    launch(sgd_rows_kernel<4>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, u);
   } else {
     const int64_t e = n * dim;
-    launch(sgd_rows_kernel<1>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, lr);
+    launch(sgd_rows_kernel<1>, unsigned(ceil_div(e, 256)), 256, 0, s, W, dim, rows, values, n, u);
   }
   return check_launch("sgd_rows_kernel");
+}
+}  // namespace
+}  // namespace dlrm
+
+extern "C" int dlrm_sgd_rows(float* W, int64_t dim, const int64_t* rows,
+                             const float* values, int64_t n, float lr,
+                             dlrm_stream_t stream) {
+  return update_rows(W, dim, rows, values, n, sgd_rule(lr), stream);
+}
+
+extern "C" int dlrm_update_rows(float* W, int64_t dim, const int64_t* rows, const float* values,
+                                int64_t n, const dlrm_update* upd, dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(upd->eps >= 0.f, "eps must be nonnegative");
+  return update_rows(W, dim, rows, values, n, upd_rule(upd), stream);
 }

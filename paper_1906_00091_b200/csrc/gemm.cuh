@@ -83,12 +83,12 @@ int gemm_simt(const float* a, int64_t a_outer, int64_t a_k, const float* b,
               cudaStream_t s, int* used_splits = nullptr);
 
 int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
-              int64_t C, float* out, float* upd, float lr,
+              int64_t C, float* out, float* upd, const Upd& u,
               const int32_t* err_flag, float* ws, size_t ws_floats,
               cudaStream_t s);
 
 int splitk_reduce(const float* part, int64_t M, int64_t N, int splits,
-                  float* dW, int64_t lddw, float* Wu, int64_t ldw, float lr,
+                  float* dW, int64_t lddw, float* Wu, int64_t ldw, const Upd& u,
                   const int32_t* err_flag, cudaStream_t s);
 
 }  // namespace dlrm

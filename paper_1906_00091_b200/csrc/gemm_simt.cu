@@ -172,10 +172,10 @@ colreduce_partial4_kernel(const float* __restrict__ X, int64_t ldx,
 }
 
 // stage 2: out[c] = sum_z partial[z][c] (ascending z); optional store and
-// fused SGD (p -= fl(lr*g)), skipped when *err_flag.
+// fused update (SGD / Adagrad), skipped when *err_flag.
 __global__ void colreduce_final_kernel(const float* __restrict__ partial,
                                        int64_t C, int splits, float* out,
-                                       float* upd, float lr,
+                                       float* upd, Upd u,
                                        const int32_t* err_flag) {
   pdl_entry();
   const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -183,14 +183,14 @@ __global__ void colreduce_final_kernel(const float* __restrict__ partial,
   float s = partial[c];
   for (int z = 1; z < splits; ++z) s += partial[int64_t(z) * C + c];
   if (out) out[c] = s;
-  if (upd && !(err_flag && *err_flag)) upd[c] = __fsub_rn(upd[c], __fmul_rn(lr, s));
+  if (upd && !(err_flag && *err_flag)) upd[c] = upd_apply(u, upd + c, upd[c], s);
 }
 
 // dW split-K reduction, 4 consecutive columns per thread (N % 4 == 0).
 __global__ void splitk_final4_kernel(const float* __restrict__ part, int64_t M,
                                      int64_t N, int splits, float* dW,
                                      int64_t lddw, float* Wu, int64_t ldw,
-                                     float lr, const int32_t* err_flag) {
+                                     Upd u, const int32_t* err_flag) {
   pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // float4 index
   const int64_t n4 = N / 4;
@@ -208,12 +208,7 @@ __global__ void splitk_final4_kernel(const float* __restrict__ part, int64_t M,
   }
   if (Wu && !(err_flag && *err_flag)) {
     float4* w = reinterpret_cast<float4*>(Wu + m * ldw + c);
-    float4 o = *w;
-    o.x = __fsub_rn(o.x, __fmul_rn(lr, s.x));
-    o.y = __fsub_rn(o.y, __fmul_rn(lr, s.y));
-    o.z = __fsub_rn(o.z, __fmul_rn(lr, s.z));
-    o.w = __fsub_rn(o.w, __fmul_rn(lr, s.w));
-    *w = o;
+    *w = upd_apply4(u, reinterpret_cast<float*>(w), *w, s);
   }
 }
 
@@ -221,7 +216,7 @@ __global__ void splitk_final4_kernel(const float* __restrict__ part, int64_t M,
 __global__ void splitk_final_kernel(const float* __restrict__ part, int64_t M,
                                     int64_t N, int splits, float* dW,
                                     int64_t lddw, float* Wu, int64_t ldw,
-                                    float lr, const int32_t* err_flag) {
+                                    Upd u, const int32_t* err_flag) {
   pdl_entry();
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= M * N) return;
@@ -230,7 +225,7 @@ __global__ void splitk_final_kernel(const float* __restrict__ part, int64_t M,
   for (int z = 1; z < splits; ++z) s += part[int64_t(z) * M * N + e];
   if (dW) dW[m * lddw + n] = s;
   if (Wu && !(err_flag && *err_flag))
-    Wu[m * ldw + n] = __fsub_rn(Wu[m * ldw + n], __fmul_rn(lr, s));
+    Wu[m * ldw + n] = upd_apply(u, Wu + m * ldw + n, Wu[m * ldw + n], s);
 }
 
 }  // namespace
@@ -249,7 +244,7 @@ int gemm_simt(const float* a, int64_t a_outer, int64_t a_k, const float* b,
 }
 
 int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
-              int64_t C, float* out, float* upd, float lr,
+              int64_t C, float* out, float* upd, const Upd& u,
               const int32_t* err_flag, float* ws, size_t ws_floats,
               cudaStream_t s) {
   const bool vec = C % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
@@ -269,20 +264,21 @@ int colreduce(const float* X, int64_t ldx, const float* scale, int64_t R,
     launch(colreduce_partial_kernel, dim3(unsigned(ceil_div(C, 32)), unsigned(splits)), 256, 0, s, X, ldx, scale, R, C, rpc, ws);
   }
   if (int rc = check_launch("colreduce_partial_kernel")) return rc;
-  launch(colreduce_final_kernel, unsigned(ceil_div(C, 256)), 256, 0, s, ws, C, int(splits), out, upd, lr, err_flag);
+  launch(colreduce_final_kernel, unsigned(ceil_div(C, 256)), 256, 0, s, ws, C, int(splits), out, upd, u, err_flag);
   return check_launch("colreduce_final_kernel");
 }
 
 int splitk_reduce(const float* part, int64_t M, int64_t N, int splits, float* dW,
-                  int64_t lddw, float* Wu, int64_t ldw, float lr,
+                  int64_t lddw, float* Wu, int64_t ldw, const Upd& u,
                   const int32_t* err_flag, cudaStream_t s) {
   const bool v4 = N % 4 == 0 && (ldw % 4 == 0 || !Wu) &&
+                  (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0) &&
                   (reinterpret_cast<uintptr_t>(part) & 15) == 0 &&
                   (!Wu || (reinterpret_cast<uintptr_t>(Wu) & 15) == 0);
   if (v4) {
-    launch(splitk_final4_kernel, unsigned(ceil_div(M * N / 4, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+    launch(splitk_final4_kernel, unsigned(ceil_div(M * N / 4, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, u, err_flag);
   } else {
-    launch(splitk_final_kernel, unsigned(ceil_div(M * N, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, lr, err_flag);
+    launch(splitk_final_kernel, unsigned(ceil_div(M * N, 256)), 256, 0, s, part, M, N, splits, dW, lddw, Wu, ldw, u, err_flag);
   }
   return check_launch("splitk_final_kernel");
 }

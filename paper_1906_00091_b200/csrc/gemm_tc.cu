@@ -191,7 +191,7 @@ struct WgradFuse {
   int64_t ldw;
   float* db;
   float* bu;
-  float lr;
+  Upd upd;  // SGD / Adagrad rule for W and b
   const int32_t* err_flag;
   int vec;  // dW / W rows 16-byte aligned
 };
@@ -307,19 +307,14 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
       if (wf.dW) *reinterpret_cast<float4*>(wf.dW + row * wf.lddw + col) = acc;
       if (upd) {
         float4* w = reinterpret_cast<float4*>(wf.Wu + row * wf.ldw + col);
-        float4 o = *w;
-        o.x = __fsub_rn(o.x, __fmul_rn(wf.lr, acc.x));
-        o.y = __fsub_rn(o.y, __fmul_rn(wf.lr, acc.y));
-        o.z = __fsub_rn(o.z, __fmul_rn(wf.lr, acc.z));
-        o.w = __fsub_rn(o.w, __fmul_rn(wf.lr, acc.w));
-        *w = o;
+        *w = upd_apply4(wf.upd, reinterpret_cast<float*>(w), *w, acc);
       }
     } else {
       for (int i = 0; i < 4 && col + i < args.N; ++i) {
         if (wf.dW) wf.dW[row * wf.lddw + col + i] = a[i];
         if (upd) {
           float* w = wf.Wu + row * wf.ldw + col + i;
-          *w = __fsub_rn(*w, __fmul_rn(wf.lr, a[i]));
+          *w = upd_apply(wf.upd, w, *w, a[i]);
         }
       }
     }
@@ -337,7 +332,7 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
         for (int kr = 0; kr < 32; ++kr)
           acc += ld_dsmem1(bb0 + uint32_t(k) * bstride + uint32_t(kr * BM + r) * 4);
       if (wf.db) wf.db[row] = acc;
-      if (bupd) wf.bu[row] = __fsub_rn(wf.bu[row], __fmul_rn(wf.lr, acc));
+      if (bupd) wf.bu[row] = upd_apply(wf.upd, wf.bu + row, wf.bu[row], acc);
     }
   }
   cluster_sync_all();  // no CTA leaves while others still read its shared memory
@@ -966,7 +961,7 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
 
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
                          int64_t N, int64_t K, float* dW, int64_t lddw, float* W_upd,
-                         int64_t ldw, float* db, float* b_upd, float lr,
+                         int64_t ldw, float* db, float* b_upd, const Upd& u,
                          const int32_t* err_flag, cudaStream_t s) {
   // dW (N x K) = gZ^T X: GEMM m = N (MN-major in gZ), n = K (MN-major in X), k = M;
   // db (N) = row sums of the A operand; both reduced over the split-K cluster
@@ -983,8 +978,9 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
   const bool vec = (!dW || (aligned16(dW) && lddw % 4 == 0)) &&
-                   (!W_upd || (aligned16(W_upd) && ldw % 4 == 0));
-  a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, lr, err_flag,
+                   (!W_upd || (aligned16(W_upd) && ldw % 4 == 0)) &&
+                   (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0);
+  a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, u, err_flag,
                    vec ? 1 : 0};
   return launch<true, true>(ma, mb, a, K, bn, used, pair, s);
 }

@@ -29,7 +29,7 @@ bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X,
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X,
                          int64_t ldx, int64_t M, int64_t N, int64_t K,
                          float* dW, int64_t lddw, float* W_upd, int64_t ldw,
-                         float* db, float* b_upd, float lr,
+                         float* db, float* b_upd, const Upd& u,
                          const int32_t* err_flag, cudaStream_t s);
 
 }  // namespace dlrm

@@ -155,6 +155,28 @@ extern "C" int dlrm_bce_head(const float* A, int64_t lda, const float* w,
   return check_launch("bce_final_kernel");
 }
 
+static int head_bwd(const float* A, int64_t lda, const float* w, const float* g, int64_t M,
+                    int64_t K, float* dA, int64_t ldda, int32_t relu_mask, float* dw, float* db,
+                    float* w_upd, float* b_upd, const Upd& u, const int32_t* err_flag,
+                    void* workspace, size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 1 && K >= 1 && lda >= K, "bad head_bwd arguments");
+  cudaStream_t s = as_stream(stream);
+  if (dA) {
+    launch(head_dA_kernel, unsigned(ceil_div(M * K, 256)), 256, 0, s, A, lda, w, g, M, K, dA,
+           ldda, relu_mask);
+    if (int rc = check_launch("head_dA_kernel")) return rc;
+  }
+  float* ws = static_cast<float*>(workspace);
+  const size_t wf = ws_bytes / sizeof(float);
+  if (dw || w_upd) {
+    if (int rc = colreduce(A, lda, g, M, K, dw, w_upd, u, err_flag, ws, wf, s)) return rc;
+  }
+  if (db || b_upd) {
+    if (int rc = colreduce(g, 1, nullptr, M, 1, db, b_upd, u, err_flag, ws, wf, s)) return rc;
+  }
+  return 0;
+}
+
 extern "C" int dlrm_head_bwd(const float* A, int64_t lda, const float* w,
                              const float* g, int64_t M, int64_t K, float* dA,
                              int64_t ldda, int32_t relu_mask, float* dw,
@@ -162,24 +184,21 @@ extern "C" int dlrm_head_bwd(const float* A, int64_t lda, const float* w,
                              float* b_upd, float lr, const int32_t* err_flag,
                              void* workspace, size_t ws_bytes,
                              dlrm_stream_t stream) {
-  DLRM_REQUIRE(M >= 1 && K >= 1 && lda >= K, "bad head_bwd arguments");
-  cudaStream_t s = as_stream(stream);
-  if (dA) {
-    launch(head_dA_kernel, unsigned(ceil_div(M * K, 256)), 256, 0, s, A, lda, w, g, M,
-                                                                  K, dA, ldda, relu_mask);
-    if (int rc = check_launch("head_dA_kernel")) return rc;
-  }
-  float* ws = static_cast<float*>(workspace);
-  const size_t wf = ws_bytes / sizeof(float);
-  if (dw || w_upd) {
-    if (int rc = colreduce(A, lda, g, M, K, dw, w_upd, lr, err_flag, ws, wf, s))
-      return rc;
-  }
-  if (db || b_upd) {
-    if (int rc = colreduce(g, 1, nullptr, M, 1, db, b_upd, lr, err_flag, ws, wf, s))
-      return rc;
-  }
-  return 0;
+  return head_bwd(A, lda, w, g, M, K, dA, ldda, relu_mask, dw, db, w_upd, b_upd, sgd_rule(lr),
+                  err_flag, workspace, ws_bytes, stream);
+}
+
+extern "C" int dlrm_head_bwd_upd(const float* A, int64_t lda, const float* w, const float* g,
+                                 int64_t M, int64_t K, float* dA, int64_t ldda,
+                                 int32_t relu_mask, float* dw, float* db, float* w_upd,
+                                 float* b_upd, const dlrm_update* upd,
+                                 const int32_t* err_flag, void* workspace, size_t ws_bytes,
+                                 dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(upd->eps >= 0.f, "eps must be nonnegative");
+  return head_bwd(A, lda, w, g, M, K, dA, ldda, relu_mask, dw, db, w_upd, b_upd, upd_rule(upd),
+                  err_flag, workspace, ws_bytes, stream);
 }
 
 extern "C" size_t dlrm_head_bwd_workspace_size(int64_t M, int64_t K) {

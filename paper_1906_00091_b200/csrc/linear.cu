@@ -71,19 +71,18 @@ extern "C" size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N,
   return f * sizeof(float) + 256;
 }
 
-extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
-                                      const float* X, int64_t ldx, int64_t M,
-                                      int64_t N, int64_t K, float* dW,
-                                      int64_t lddw, float* db, float* W_upd,
-                                      int64_t ldw, float* b_upd, float lr,
-                                      const int32_t* err_flag, void* workspace,
-                                      size_t ws_bytes, dlrm_stream_t stream) {
+namespace dlrm {
+namespace {
+int linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
+                      int64_t N, int64_t K, float* dW, int64_t lddw, float* db, float* W_upd,
+                      int64_t ldw, float* b_upd, const Upd& u, const int32_t* err_flag,
+                      void* workspace, size_t ws_bytes, dlrm_stream_t stream) {
   DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldx >= K,
                "bad linear_bwd_weight shape");
   cudaStream_t s = as_stream(stream);
   if (tc_linear_bwd_weight_ok(gZ, ldg, X, ldx, M, N, K))
     return tc_linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, W_upd, ldw, db, b_upd,
-                                lr, err_flag, s);
+                                u, err_flag, s);
   DLRM_REQUIRE(ws_bytes >= dlrm_linear_bwd_weight_workspace_size(M, N, K) &&
                    workspace != nullptr,
                "linear_bwd_weight workspace too small");
@@ -94,12 +93,38 @@ extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
   int used = 1;
   if (int rc = gemm_simt(gZ, 1, ldg, X, 1, ldx, N, K, M, sp, ep, K, s, &used))
     return rc;
-  if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, lr, err_flag, s))
+  if (int rc = splitk_reduce(ws, N, K, used, dW, lddw, W_upd, ldw, u, err_flag, s))
     return rc;
   if (db || b_upd) {
     float* cws = ws + size_t(sp) * N * K;
-    return colreduce(gZ, ldg, nullptr, M, N, db, b_upd, lr, err_flag, cws,
+    return colreduce(gZ, ldg, nullptr, M, N, db, b_upd, u, err_flag, cws,
                      colreduce_ws_floats(M, N), s);
   }
   return 0;
+}
+}  // namespace
+}  // namespace dlrm
+
+extern "C" int dlrm_linear_bwd_weight(const float* gZ, int64_t ldg,
+                                      const float* X, int64_t ldx, int64_t M,
+                                      int64_t N, int64_t K, float* dW,
+                                      int64_t lddw, float* db, float* W_upd,
+                                      int64_t ldw, float* b_upd, float lr,
+                                      const int32_t* err_flag, void* workspace,
+                                      size_t ws_bytes, dlrm_stream_t stream) {
+  return linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, db, W_upd, ldw, b_upd,
+                           sgd_rule(lr), err_flag, workspace, ws_bytes, stream);
+}
+
+extern "C" int dlrm_linear_bwd_weight_upd(const float* gZ, int64_t ldg, const float* X,
+                                          int64_t ldx, int64_t M, int64_t N, int64_t K,
+                                          float* dW, int64_t lddw, float* db, float* W_upd,
+                                          int64_t ldw, float* b_upd, const dlrm_update* upd,
+                                          const int32_t* err_flag, void* workspace,
+                                          size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(upd->eps >= 0.f, "eps must be nonnegative");
+  return linear_bwd_weight(gZ, ldg, X, ldx, M, N, K, dW, lddw, db, W_upd, ldw, b_upd,
+                           upd_rule(upd), err_flag, workspace, ws_bytes, stream);
 }

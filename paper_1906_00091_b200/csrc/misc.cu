@@ -30,25 +30,21 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 
-// p -= fl(lr * g): __fmul_rn/__fsub_rn keep nvcc from contracting to an FMA,
-// matching numpy's `param -= lr * grad` rounding.
-__global__ void sgd_dense_kernel(float* __restrict__ p, const float* __restrict__ g,
-                                 int64_t n, float lr, const int32_t* err_flag) {
+// p -= fl(lr * g) (SGD) or the Adagrad rule (upd_apply*): __fmul_rn /
+// __fsub_rn keep nvcc from contracting to an FMA, matching numpy's rounding.
+__global__ void update_dense_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                    int64_t n, Upd u, const int32_t* err_flag) {
   pdl_entry();
   if (err_flag && *err_flag) return;
   const int64_t n4 = n / 4;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 w = reinterpret_cast<float4*>(p)[i];
-    const float4 d = reinterpret_cast<const float4*>(g)[i];
-    w.x = __fsub_rn(w.x, __fmul_rn(lr, d.x));
-    w.y = __fsub_rn(w.y, __fmul_rn(lr, d.y));
-    w.z = __fsub_rn(w.z, __fmul_rn(lr, d.z));
-    w.w = __fsub_rn(w.w, __fmul_rn(lr, d.w));
-    reinterpret_cast<float4*>(p)[i] = w;
+    float4* pw = reinterpret_cast<float4*>(p) + i;
+    *pw = upd_apply4(u, reinterpret_cast<float*>(pw), *pw,
+                     reinterpret_cast<const float4*>(g)[i]);
   }
   for (int64_t i = n4 * 4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    p[i] = __fsub_rn(p[i], __fmul_rn(lr, g[i]));
+    p[i] = upd_apply(u, p + i, p[i], g[i]);
 }
 
 }  // namespace
@@ -64,15 +60,29 @@ extern "C" const char* dlrm_build_info(void) {
   return "libdlrmb200 sm_100a";
 }
 
-extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
-                              const int32_t* err_flag, dlrm_stream_t stream) {
+static int update_dense(float* p, const float* g, int64_t n, const Upd& u,
+                        const int32_t* err_flag, dlrm_stream_t stream) {
   DLRM_REQUIRE(n >= 0, "negative length");
   if (n == 0) return 0;
   DLRM_REQUIRE(reinterpret_cast<uintptr_t>(p) % 16 == 0 &&
-                   reinterpret_cast<uintptr_t>(g) % 16 == 0,
-               "sgd_dense needs 16-byte aligned buffers");
+                   reinterpret_cast<uintptr_t>(g) % 16 == 0 &&
+                   (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0),
+               "dense update needs 16-byte aligned buffers");
   const int64_t blocks = ceil_div(ceil_div(n, 4), 256);
-  launch(sgd_dense_kernel, unsigned(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256,
-                     0, as_stream(stream), p, g, n, lr, err_flag);
-  return check_launch("sgd_dense_kernel");
+  launch(update_dense_kernel, unsigned(blocks < 4 * kNumSMs ? blocks : 4 * kNumSMs), 256, 0,
+         as_stream(stream), p, g, n, u, err_flag);
+  return check_launch("update_dense_kernel");
+}
+
+extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
+                              const int32_t* err_flag, dlrm_stream_t stream) {
+  return update_dense(p, g, n, sgd_rule(lr), err_flag, stream);
+}
+
+extern "C" int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* upd,
+                                 const int32_t* err_flag, dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(upd->eps >= 0.f, "eps must be nonnegative");
+  return update_dense(p, g, n, upd_rule(upd), err_flag, stream);
 }

@@ -157,7 +157,8 @@ class RankEngine:
     """
 
     def __init__(self, model: DlrmModel, layout: ExchangeLayout,
-                 capacities=None, lr: float = 0.1):
+                 capacities=None, lr: float = 0.1, optimizer: str = "sgd",
+                 eps: float = 1e-10):
         _lib.require_cuda()
         cfg = model.config
         self.model, self.cfg, self.L = model, cfg, layout
@@ -254,6 +255,18 @@ class RankEngine:
         self.stats = torch.zeros(3, **f32)
         self.err_pos = torch.empty(max(To, 1), dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # update rule (SGD / Adagrad with same-layout accumulators)
+        from .optim import update_rule
+        self.optimizer = optimizer
+        if optimizer == "adagrad":
+            self.params_acc = torch.zeros_like(self.params)
+            self.W_acc = torch.zeros_like(self.W_own)
+            self.upd_mlp = update_rule("adagrad", self.lr, eps, self.params, self.params_acc)
+            self.upd_emb = update_rule("adagrad", self.lr, eps, self.W_own, self.W_acc)
+        elif optimizer == "sgd":
+            self.upd_mlp = self.upd_emb = update_rule("sgd", self.lr)
+        else:
+            raise ValueError(f"unknown optimizer: {optimizer!r}")
         self._build_descs()
 
     def _build_descs(self):
@@ -442,29 +455,24 @@ class RankEngine:
         To = len(self.own)
         if To:
             P = _lib.ptr
-            _lib.call("dlrm_emb_bwd_apply_sgd", P(self.W_own), self.d,
+            _lib.call("dlrm_emb_bwd_apply", P(self.W_own), self.d,
                       C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.grecv),
-                      To * self.d, self.lr, P(self.err_flag), self.total_rows,
+                      To * self.d, C.byref(self.upd_emb), P(self.err_flag), self.total_rows,
                       P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(stream))
 
     def sgd_dense(self, stream=None):
+        """Dense update of the MLP replica from the allreduced gradients."""
         P = _lib.ptr
-        _lib.call("dlrm_sgd_dense", P(self.params), P(self.grads),
-                  self.params.numel(), self.lr, P(self.err_flag), _lib.stream_handle(stream))
+        _lib.call("dlrm_update_dense", P(self.params), P(self.grads),
+                  self.params.numel(), C.byref(self.upd_mlp), P(self.err_flag),
+                  _lib.stream_handle(stream))
 
     def phase_c(self, stream=None, prepared=False):
-        s = _lib.stream_handle(stream)
-        P = _lib.ptr
         To = len(self.own)
         if To and not prepared:
             self.prepare_sparse_backward(stream)
-        if To:
-            _lib.call("dlrm_emb_bwd_apply_sgd", P(self.W_own), self.d,
-                      C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.grecv),
-                      To * self.d, self.lr, P(self.err_flag), self.total_rows,
-                      P(self.emb_ws), self.emb_ws_bytes, s)
-        _lib.call("dlrm_sgd_dense", P(self.params), P(self.grads),
-                  self.params.numel(), self.lr, P(self.err_flag), s)
+        self.apply_sparse(stream)
+        self.sgd_dense(stream)
 
     def local_error(self):
         """(table_id, position, index, rows) of this rank's first bad index."""
@@ -487,9 +495,10 @@ class HybridTrainer:
     plan assigns to it and an MLP replica."""
 
     def __init__(self, model: DlrmModel, plan: DevicePlan, rank: int,
-                 capacities=None, lr: float = 0.1, group=None, ar_group=None):
+                 capacities=None, lr: float = 0.1, group=None, ar_group=None,
+                 optimizer: str = "sgd", eps: float = 1e-10):
         self.layout = ExchangeLayout(plan, rank, model.config.sparse_dim)
-        self.engine = RankEngine(model, self.layout, capacities, lr)
+        self.engine = RankEngine(model, self.layout, capacities, lr, optimizer, eps)
         self.ex = NcclExchange(self.layout, group, ar_group)
         self.rank = rank
         self.comm_stream = torch.cuda.Stream()

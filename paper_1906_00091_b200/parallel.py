@@ -198,18 +198,30 @@ def format_comm_report(comm: CommLog) -> str:
 # --------------------------------------------------------------------------
 # single-device training step  (ref parallel.py:250-287)
 
-def _engine_for(model: DlrmModel, batch: int, batches, lr: float,
+def _engine_for(model: DlrmModel, batch: int, batches, optimizer,
                 weighted: bool) -> StepEngine:
     eng = getattr(model, "_engine", None)
     nnz = [sb.nnz for sb in batches]
-    if (eng is not None and eng.B == batch and eng.lr == float(lr)
+    kind = optimizer.name
+    eps = float(getattr(optimizer, "eps", 1e-10))
+    if (eng is not None and eng.B == batch and eng.lr == float(optimizer.lr)
+            and eng.optimizer == kind and (kind != "adagrad" or eng.eps == eps)
             and eng.weighted == weighted
             and all(n <= c for n, c in zip(nnz, eng.caps))):
         return eng
     caps = [max(n, batch) for n in nnz]
     if eng is not None:  # grow geometrically so graphs are rarely rebuilt
         caps = [max(c, int(1.25 * old)) for c, old in zip(caps, eng.caps)]
-    eng = StepEngine(model, batch, caps, lr=lr, weighted=weighted)
+    if eng is not None and kind == "adagrad" and eng.optimizer == "adagrad":
+        # a rebuilt engine keeps the Adagrad accumulators
+        acc_p, acc_w = eng.params_acc, eng.W_acc
+    else:
+        acc_p = acc_w = None
+    eng = StepEngine(model, batch, caps, lr=optimizer.lr, weighted=weighted,
+                     optimizer=kind, eps=eps)
+    if acc_p is not None:
+        eng.params_acc.copy_(acc_p)
+        eng.W_acc.copy_(acc_w)
     eng.eager_runs = 0
     model._engine = eng
     return eng
@@ -222,8 +234,8 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
     Same contract as the reference: updates ``model`` in place and returns
     (loss, accuracy, probs); an out-of-range index raises LookupIndexError
     and leaves every parameter untouched."""
-    if not isinstance(optimizer, Sgd):
-        raise NotImplementedError("the fused step implements SGD only")
+    if getattr(optimizer, "name", None) not in ("sgd", "adagrad"):
+        raise ValueError(f"unsupported optimizer {optimizer!r}")
     cfg = model.config
     if len(batches) != cfg.num_tables:
         raise ValueError(
@@ -234,7 +246,7 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
             raise ValueError(
                 f"sparse batch {t} has {sb.num_segments} segments, batch is {b}")
     weighted = any(sb.weights is not None for sb in batches)
-    eng = _engine_for(model, b, batches, optimizer.lr, weighted)
+    eng = _engine_for(model, b, batches, optimizer, weighted)
     eng.load(dense_x, [sb.offsets for sb in batches],
              [sb.indices for sb in batches], labels,
              [sb.weights for sb in batches] if weighted else None)
@@ -269,8 +281,8 @@ class ParallelTrainer:
                  eps: float = 1e-10, concurrent: bool = False,
                  capacities=None):
         from .distributed import ExchangeLayout, LocalExchange, RankEngine
-        if optimizer_name != "sgd":
-            raise NotImplementedError("the fused step implements SGD only")
+        if optimizer_name not in ("sgd", "adagrad"):
+            raise ValueError(f"unknown optimizer: {optimizer_name!r}")
         plan.validate()
         if len(plan.table_assignment) != model.config.num_tables:
             raise ValueError("plan does not cover the model's tables")
@@ -285,7 +297,8 @@ class ParallelTrainer:
                                 model.top.copy(), self.tables)
             own = self.layouts[r].owned[r]
             caps = None if capacities is None else [capacities[t] for t in own]
-            self.engines.append(RankEngine(replica, self.layouts[r], caps, lr))
+            self.engines.append(RankEngine(replica, self.layouts[r], caps, lr,
+                                           optimizer_name, eps))
         self.ex = LocalExchange(self.layouts)
         self.comm = CommLog()
         self.step_count = 0

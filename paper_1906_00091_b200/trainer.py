@@ -78,7 +78,8 @@ class StepEngine:
 
     def __init__(self, model: DlrmModel, batch_size: int, capacities=None,
                  lr: float = 0.1, weighted: bool = False,
-                 n_total: int | None = None, input_sets: int = 1):
+                 n_total: int | None = None, input_sets: int = 1,
+                 optimizer: str = "sgd", eps: float = 1e-10):
         _lib.require_cuda()
         cfg = model.config
         self.model, self.cfg = model, cfg
@@ -178,6 +179,19 @@ class StepEngine:
         self.stats = torch.zeros(2, **f32)
         self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # update rule fused into the step's kernels (ref optim.py): SGD, or
+        # Adagrad with accumulators laid out exactly like the parameters
+        from .optim import update_rule
+        self.optimizer, self.eps = optimizer, float(eps)
+        if optimizer == "adagrad":
+            self.params_acc = torch.zeros_like(self.params)
+            self.W_acc = torch.zeros_like(self.W_all)
+            self.upd_mlp = update_rule("adagrad", self.lr, eps, self.params, self.params_acc)
+            self.upd_emb = update_rule("adagrad", self.lr, eps, self.W_all, self.W_acc)
+        elif optimizer == "sgd":
+            self.upd_mlp = self.upd_emb = update_rule("sgd", self.lr)
+        else:
+            raise ValueError(f"unknown optimizer: {optimizer!r}")
         # the index-only half of the sparse backward (keys + radix sort) runs
         # on a side stream, overlapped with the dense part of the step;
         # DLRM_EMB_PREP = "start" (default) | "after_fwd" | "inline"
@@ -373,9 +387,10 @@ class StepEngine:
              P(self.prob), P(self.glogit), None, P(self.stats), ws, wsb, s)
         # head backward (dA masked by the ReLU below it) + fused SGD
         ga = self.gtop[-1] if self.Lt > 1 else self.gR
-        call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), B,
+        um, ue = C.byref(self.upd_mlp), C.byref(self.upd_emb)
+        call("dlrm_head_bwd_upd", P(a), lda, P(head.storage), P(self.glogit), B,
              head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None,
-             None, P(head.storage), P(head.bias), lr, ef, ws, wsb, s)
+             None, P(head.storage), P(head.bias), um, ef, ws, wsb, s)
         # top MLP backward
         mark("top_mlp_bwd")
         for i in range(self.Lt - 2, -1, -1):
@@ -387,9 +402,9 @@ class StepEngine:
             call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
                  l.ldw, P(mask), mask.stride(0) if mask is not None else 0,
                  P(dx), dx.stride(0), B, l.n_out, l.n_in, s)
-            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin),
+            call("dlrm_linear_bwd_weight_upd", P(gz), gz.stride(0), P(xin),
                  xin.stride(0), B, l.n_out, l.n_in, None, 0, None,
-                 P(l.storage), l.ldw, P(l.bias), lr, ef, ws, wsb, s)
+                 P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb, s)
         # interaction backward (bottom's last ReLU folded in for feature 0)
         mark("interaction_bwd")
         call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
@@ -404,8 +419,8 @@ class StepEngine:
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
-            call("dlrm_emb_bwd_apply_sgd", P(self.W_all), d, self._descs_p, self.T, B,
-                 P(self.gZ), nf * d, lr, ef, self.total_rows, P(self.emb_ws),
+            call("dlrm_emb_bwd_apply", P(self.W_all), d, self._descs_p, self.T, B,
+                 P(self.gZ), nf * d, ue, ef, self.total_rows, P(self.emb_ws),
                  self.emb_ws_bytes, _lib.stream_handle(self.side))
             apply_done = torch.cuda.Event()
             apply_done.record(self.side)
@@ -423,9 +438,9 @@ class StepEngine:
                 call("dlrm_linear_bwd_data", P(gz), ldg, P(l.storage), l.ldw,
                      P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), B, l.n_out, l.n_in, s)
-            call("dlrm_linear_bwd_weight", P(gz), ldg, P(xin), xin.stride(0),
+            call("dlrm_linear_bwd_weight_upd", P(gz), ldg, P(xin), xin.stride(0),
                  B, l.n_out, l.n_in, None, 0, None, P(l.storage), l.ldw,
-                 P(l.bias), lr, ef, ws, wsb, s)
+                 P(l.bias), um, ef, ws, wsb, s)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
         if apply_done is not None:
@@ -436,8 +451,8 @@ class StepEngine:
                  P(self.emb_ws), self.emb_ws_bytes, s)
         else:
             main.wait_event(prep_done)
-        call("dlrm_emb_bwd_apply_sgd", P(self.W_all), d, self._descs_p, self.T, B,
-             P(self.gZ), nf * d, lr, ef, self.total_rows, P(self.emb_ws),
+        call("dlrm_emb_bwd_apply", P(self.W_all), d, self._descs_p, self.T, B,
+             P(self.gZ), nf * d, ue, ef, self.total_rows, P(self.emb_ws),
              self.emb_ws_bytes, s)
 
     # ------------------------------------------------------------------

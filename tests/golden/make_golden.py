@@ -55,6 +55,17 @@ TRAJ = {
                 batch=64, k=1, fixed=True, steps=2, lr=0.1),
     "c3s": dict(tables=[800] * 4, d=64, bot=[32, 64, 64], top=[64, 32, 1],
                 seed=1, batch=96, k=12, fixed=False, steps=3, lr=0.1),
+    # Adagrad: the reference's make_optimizer("adagrad").
+    # eps well above fp32 rounding noise: with eps ~ 0 the first Adagrad step
+    # is lr*sign(g), so a gradient that is 1e-12 in float64 and 1e-9 of the
+    # other sign in float32 moves a weight by 2*lr — no fp32 implementation
+    # can match float64 elementwise there.
+    "c1a": dict(tables=[600] * 8, d=16, bot=[13, 512, 256, 64, 16],
+                top=[512, 256, 1], seed=0, batch=128, k=1, fixed=True,
+                steps=4, lr=0.01, opt="adagrad", eps=1e-2),
+    "c3a": dict(tables=[800] * 4, d=64, bot=[32, 64, 64], top=[64, 32, 1],
+                seed=1, batch=96, k=12, fixed=False, steps=3, lr=0.01,
+                opt="adagrad", eps=1e-4),
 }
 
 
@@ -120,7 +131,7 @@ def make_traj(name, c):
     for w, t in zip(start["tables"], ref_model.tables):
         t.weights[...] = w
 
-    opt = dlrmkit.make_optimizer("sgd", c["lr"])
+    opt = dlrmkit.make_optimizer(c.get("opt", "sgd"), c["lr"], c.get("eps", 1e-10))
     losses, accs, probs = [], [], []
     for hb in batches:
         dense32 = hb.dense.astype(np.float32).astype(np.float64)
@@ -133,10 +144,12 @@ def make_traj(name, c):
 
     # the oracle pin: our float64 port must reproduce dlrmkit bit for bit
     pm = start
+    ada = port.adagrad_state(pm) if c.get("opt") == "adagrad" else None
     for s, hb in enumerate(batches):
         dense32 = hb.dense.astype(np.float32).astype(np.float64)
         loss, acc, prob = port.train_step(pm, dense32, hb.offsets,
-                                          hb.indices, hb.labels, c["lr"])
+                                          hb.indices, hb.labels, c["lr"],
+                                          adagrad=ada, eps=c.get("eps", 1e-10))
         assert loss == losses[s] and acc == accs[s], (name, s, loss, losses[s])
         assert np.array_equal(prob, probs[s])
     final_ref = port_arrays(ref_model_to_port(ref_model))
@@ -197,6 +210,9 @@ def make_bags():
 
 
 if __name__ == "__main__":
-    make_bags()
+    only = sys.argv[1:]
+    if not only:
+        make_bags()
     for name, c in TRAJ.items():
-        make_traj(name, c)
+        if not only or name in only:
+            make_traj(name, c)

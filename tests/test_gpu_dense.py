@@ -109,3 +109,38 @@ def test_sgd_dense_rounding():
     sgd_step(t, torch.tensor(g, device="cuda"), 0.1)
     exp = w - np.float32(0.1) * g
     assert np.array_equal(t.cpu().numpy().view(np.uint32), exp.view(np.uint32))
+
+
+# ---- Adagrad: kernels vs the float32 restatement, bit for bit
+
+def test_adagrad_dense_bit_exact():
+    from oracle import fp32
+    from paper_1906_00091_b200 import adagrad_step
+    rng = np.random.default_rng(3)
+    for n in (1, 7, 1000, 4099):
+        p = rng.standard_normal(n).astype(np.float32)
+        g = rng.standard_normal(n).astype(np.float32)
+        a = np.abs(rng.standard_normal(n)).astype(np.float32)
+        tp, tg, ta = (torch.as_tensor(x, device="cuda") for x in (p, g, a))
+        adagrad_step(tp, tg, ta, 0.05, 1e-8)
+        ep, ea = fp32.adagrad_dense(p, g, a, 0.05, 1e-8)
+        assert np.array_equal(tp.cpu().numpy().view(np.uint32), ep.view(np.uint32))
+        assert np.array_equal(ta.cpu().numpy().view(np.uint32), ea.view(np.uint32))
+
+
+def test_adagrad_rows_bit_exact_and_untouched_rows_keep_bits():
+    from oracle import fp32
+    from paper_1906_00091_b200 import SparseRowGrad, adagrad_step_rows
+    rng = np.random.default_rng(4)
+    for m, d in ((50, 16), (300, 20), (64, 256)):
+        W = rng.standard_normal((m, d)).astype(np.float32)
+        A = np.abs(rng.standard_normal((m, d))).astype(np.float32)
+        rows = np.sort(rng.choice(m, m // 3, replace=False)).astype(np.int64)
+        vals = rng.standard_normal((rows.size, d)).astype(np.float32)
+        tW, tA = torch.as_tensor(W, device="cuda"), torch.as_tensor(A, device="cuda")
+        g = SparseRowGrad(torch.as_tensor(rows, device="cuda"),
+                          torch.as_tensor(vals, device="cuda"))
+        adagrad_step_rows(tW, g, tA, 0.1, 1e-10)
+        eW, eA = fp32.adagrad_rows(W, rows, vals, A, 0.1, 1e-10)
+        assert np.array_equal(tW.cpu().numpy().view(np.uint32), eW.view(np.uint32))
+        assert np.array_equal(tA.cpu().numpy().view(np.uint32), eA.view(np.uint32))

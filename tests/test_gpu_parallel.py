@@ -33,8 +33,9 @@ def arrays_of(bottom, top, tables):
 def run_parallel(c, batches, G):
     model = build(c)
     caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
-    tr = ParallelTrainer(model, make_plan(model.config, c["batch"], G), "sgd",
-                         c["lr"], capacities=caps)
+    tr = ParallelTrainer(model, make_plan(model.config, c["batch"], G),
+                         c.get("opt", "sgd"), c["lr"], eps=c.get("eps", 1e-10),
+                         capacities=caps)
     res = []
     for hb in batches:
         sparse = [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)]
@@ -60,7 +61,7 @@ def test_one_rank_is_bitwise_the_fused_step(golden):
 
 
 @pytest.mark.parametrize("name,G", [("toy", 2), ("toy", 3), ("c1s", 2), ("c1s", 4),
-                                    ("c2s", 4), ("c3s", 3)])
+                                    ("c2s", 4), ("c3s", 3), ("c1a", 2), ("c3a", 3)])
 def test_matches_reference_trajectory(golden, name, G):
     fx = golden(f"traj_{name}.npz")
     c, batches = traj_inputs(fx)

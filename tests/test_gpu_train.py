@@ -14,11 +14,12 @@ import pytest
 import torch
 
 from paper_1906_00091_b200 import (DlrmConfig, LookupIndexError, Sgd,
-                                   SparseBatch, init_model, train_step)
+                                   SparseBatch, init_model, make_optimizer,
+                                   train_step)
 from tests._util import rel_err, traj_inputs
 
 pytestmark = pytest.mark.gpu
-TRAJS = ["toy", "c1s", "c2s", "c3s"]
+TRAJS = ["toy", "c1s", "c2s", "c3s", "c1a", "c3a"]   # *a: Adagrad
 
 
 def model_arrays(model):
@@ -36,7 +37,7 @@ def build(c):
 
 def run_traj(c, batches, use_graph=True):
     model = build(c)
-    opt = Sgd(c["lr"])
+    opt = make_optimizer(c.get("opt", "sgd"), c["lr"], c.get("eps", 1e-10))
     res = []
     for hb in batches:
         sparse = [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)]
