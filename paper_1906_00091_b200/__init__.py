@@ -14,7 +14,8 @@ from .embedding import (EmbeddingTable, LookupIndexError, SparseBatch,
 from .model import (DlrmCache, DlrmConfig, DlrmGradients, DlrmModel, MlpCache,
                     MlpGrads, MlpLayer, MlpParams, StageError, bce_from_logits,
                     bce_loss, dlrm_backward, dlrm_forward,
-                    embedding_param_count, init_mlp, init_model, interact,
+                    embedding_param_count, from_reference, init_mlp, init_model,
+                    interact, to_reference,
                     interact_backward, interaction_width, mlp_backward,
                     mlp_forward, mlp_param_count, param_count)
 from .optim import (Adagrad, AdagradState, Sgd, adagrad_step, adagrad_step_rows,

@@ -144,3 +144,35 @@ def test_adagrad_rows_bit_exact_and_untouched_rows_keep_bits():
         eW, eA = fp32.adagrad_rows(W, rows, vals, A, 0.1, 1e-10)
         assert np.array_equal(tW.cpu().numpy().view(np.uint32), eW.view(np.uint32))
         assert np.array_equal(tA.cpu().numpy().view(np.uint32), eA.view(np.uint32))
+
+
+def test_reference_model_round_trip():
+    """from_reference / to_reference: a dlrmkit-shaped model
+    (duck-typed here; dlrmkit is not installed on the GPU box) converts to
+    CUDA fp32 and back with values rounded to fp32 and structure kept."""
+    from types import SimpleNamespace as NS
+    from paper_1906_00091_b200 import DlrmConfig, from_reference, init_model, to_reference
+    rng = np.random.default_rng(5)
+    cfg = NS(embedding_sizes=[7, 11], sparse_dim=4, bottom_mlp_dims=[3, 5, 4],
+             top_mlp_dims=[6, 1], interaction="dot", seed=9)
+    lay = lambda o, i, a: NS(weight=rng.standard_normal((o, i)), bias=rng.standard_normal(o),
+                             activation=a)
+    ref = NS(config=cfg, bottom=NS(layers=[lay(5, 3, "relu"), lay(4, 5, "relu")]),
+             top=NS(layers=[lay(6, 7, "relu"), lay(1, 6, "identity")]),
+             tables=[NS(weights=rng.standard_normal((7, 4)), table_id=0),
+                     NS(weights=rng.standard_normal((11, 4)), table_id=1)])
+    m = from_reference(ref)
+    assert m.config.top_mlp_dims == [6, 1] and m.config.seed == 9
+    assert np.array_equal(m.bottom.layers[1].weight.cpu().numpy(),
+                          ref.bottom.layers[1].weight.astype(np.float32))
+    assert np.array_equal(m.tables[1].weights.cpu().numpy(),
+                          ref.tables[1].weights.astype(np.float32))
+    fake = NS(DlrmConfig=lambda *a: NS(args=a), MlpParams=lambda ls: NS(layers=ls),
+              MlpLayer=lambda w, b, a: NS(weight=w, bias=b, activation=a),
+              EmbeddingTable=lambda w, t: NS(weights=w, table_id=t),
+              DlrmModel=lambda c, b, t, tab: NS(config=c, bottom=b, top=t, tables=tab))
+    back = to_reference(m, fake)
+    assert back.top.layers[1].activation == "identity"
+    assert back.tables[0].weights.dtype == np.float64
+    assert np.array_equal(back.top.layers[0].weight,
+                          ref.top.layers[0].weight.astype(np.float32).astype(np.float64))
