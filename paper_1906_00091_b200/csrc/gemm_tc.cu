@@ -37,19 +37,18 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-// Ring depths (raw TMA tiles, split-off lo tiles) within 227 KB of shared
-// memory.  The TMA ring must cover the L2 latency of a tile load (about
-// 1.5 us at full load = 4-5 k-steps of MMA work); a CTA pair holds half of
-// B, so its stages are smaller and the rings deeper.
-#ifndef DLRM_TC_TS
-#define DLRM_TC_TS 5
-#define DLRM_TC_LS 2
-#define DLRM_TC_TS2 6
-#define DLRM_TC_LS2 3
+// Ring depths within 227 KB of shared memory: TSTAGES stages of
+// [A_hi | B_hi | B_lo] (TMA covers the L2 latency of a tile load) and
+// LSTAGES A_lo slots.
+constexpr int TSTAGES = 4;
+constexpr int LSTAGES = 2;
+#ifndef DLRM_TC_SPLIT_WARPS
+#define DLRM_TC_SPLIT_WARPS 8
 #endif
-__host__ __device__ constexpr int raw_stages(bool pair) { return pair ? DLRM_TC_TS2 : DLRM_TC_TS; }
-__host__ __device__ constexpr int lo_stages(bool pair) { return pair ? DLRM_TC_LS2 : DLRM_TC_LS; }
-constexpr int SPLIT_WARPS = 8;  // splitter + epilogue warps (2 per TMEM lane quarter)
+// splitter warps; the first 8 of them are also the epilogue (2 per TMEM lane
+// quarter)
+constexpr int SPLIT_WARPS = DLRM_TC_SPLIT_WARPS;
+constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + 32 * SPLIT_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -132,37 +131,6 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       : "memory");
 }
 
-// CTA pair (cta_group::2): issued by the leader CTA; A rows 0..127 come from
-// the leader's shared memory, rows 128..255 from the peer's (same offsets),
-// and each CTA supplies half of the N columns of B.
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem, uint64_t a, uint64_t b,
-                                              uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// completion of the pair's MMAs arrives on the barrier at the same offset in
-// every CTA of `mask`
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -223,7 +191,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // n-tile-0 cluster does the same for the bias gradient (row sums of the A
 // operand accumulated by the splitter warps).  No partial sums in global
 // memory, no reduction kernel, no counters.
-constexpr uint32_t kBiasScratch = 32 * 20 * 4 * 8;  // after the epilogue transpose tiles
+constexpr uint32_t kBiasScratch = 32 * 20 * 4 * 8;  // bias sums after the transpose tiles
 
 // First of the 4 consecutive tile rows (m) held by 16-byte column c16 of k-row
 // kr in A chunk r of an MN-major SWIZZLE_128B_ATOM_32B tile: 32-byte atoms are
@@ -243,23 +211,6 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
   return r;
 }
 
-// Forwarded "lo ready" arrive on the pair leader's barrier.  The lo tiles it
-// covers were written by this CTA's splitter warps, made visible to the async
-// proxy (fence.proxy.async) and released to this thread at CTA scope through
-// the local barrier, i.e. they are performed in this CTA's shared memory
-// before the arrive is issued; a .release.cluster arrive would add a
-// GPU-scope fence (MEMBAR.ALL.GPU, ~1.5k cycles) per k-step on the critical
-// path of the pair.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-#ifdef DLRM_PAIR_RELEASE
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-#else
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-#endif
-}
-
 __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -276,22 +227,20 @@ __device__ __forceinline__ float ld_dsmem1(uint32_t addr) {
 }
 
 // Executed by every thread of every CTA of the cluster (see WgradFuse).
-template <int BN, bool PAIR>
+template <int BN>
 __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const uint8_t* ptile,
                                                      const uint8_t* bscratch, int64_t m0,
-                                                     int64_t n0, uint32_t pr) {
+                                                     int64_t n0) {
   const WgradFuse& wf = args.wf;
   constexpr int P = BN + 4, C4 = BN / 4;
-  // cluster (PAIR ? 2 : 1, 1, S): split k of this CTA's row block has rank
-  // pr + (PAIR ? 2 : 1) * k
+  // cluster (1, 1, S): the split k of this tile has cluster rank k
   const int S = int(gridDim.z), z = int(blockIdx.z);
   cluster_sync_all();  // every partial tile / bias scratch of the cluster is written
   const bool upd = wf.Wu != nullptr && !(wf.err_flag && *wf.err_flag);
   const int R = (BM + S - 1) / S, r0 = z * R, r1 = r0 + R < BM ? r0 + R : BM;
   const float* pt = reinterpret_cast<const float*>(ptile);
-  constexpr uint32_t RS = PAIR ? 2 : 1;
-  const uint32_t base0 = dsmem_addr(pt, pr);
-  const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, pr + RS) - base0 : 0;
+  const uint32_t base0 = dsmem_addr(pt, 0);
+  const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, 1) - base0 : 0;
   for (int e = threadIdx.x; e < (r1 - r0) * C4; e += blockDim.x) {
     const int r = r0 + e / C4, c = (e % C4) * 4;
     const int64_t row = m0 + r, col = n0 + c;
@@ -322,8 +271,8 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
   if (wf.bias && n0 == 0) {
     const bool bupd = wf.bu != nullptr && !(wf.err_flag && *wf.err_flag);
     const float* bs = reinterpret_cast<const float*>(bscratch);
-    const uint32_t bb0 = dsmem_addr(bs, pr);
-    const uint32_t bstride = S > 1 ? dsmem_addr(bs, pr + RS) - bb0 : 0;
+    const uint32_t bb0 = dsmem_addr(bs, 0);
+    const uint32_t bstride = S > 1 ? dsmem_addr(bs, 1) - bb0 : 0;
     for (int r = r0 + int(threadIdx.x); r < r1; r += int(blockDim.x)) {
       const int64_t row = m0 + r;
       if (row >= args.M) continue;
@@ -338,58 +287,57 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
   cluster_sync_all();  // no CTA leaves while others still read its shared memory
 }
 
-// PAIR: the two CTAs of a cluster pair along x compute a 256 x BN tile with
-// cta_group::2 MMAs (each loads its own 128 A rows and BN/2 B columns), which
-// cuts the shared-memory traffic per MMA by a quarter; the leader (even y)
-// issues the MMAs, both CTAs split and run their own epilogue rows.
-template <bool A_MN, bool B_MN, int BN, bool PAIR>
+// One CTA computes a BM x BN tile of the fp32-accurate product with 3xTF32
+// tcgen05 MMAs.  Shared memory per k-step: a TMA stage [A_hi | B_hi | B_lo]
+// (the raw fp32 tiles are the hi operands; the splitter writes B_lo right
+// behind B_hi) and an A_lo slot.  With B_lo adjacent to B_hi, the two
+// products that share A_hi are ONE MMA of N = 2*BN (A_hi x [B_hi | B_lo]),
+// which reads A_hi from shared memory once instead of twice; the third
+// product A_lo x B_hi is an N = BN MMA.  Accumulators in TMEM:
+// [big0 | sm0 | big1 | sm1] (BN columns each): k-block it goes to pair
+// it % 2, so each truncating TMEM accumulation chain is half as long
+// (tensor-core fp32 accumulation truncates; the error grows with the chain).
+template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                TcArgs args) {
-  constexpr int BNL = PAIR ? BN / 2 : BN;  // B columns held by this CTA
-  constexpr int LSTAGES = lo_stages(PAIR);
-  constexpr int TSTAGES = raw_stages(PAIR);
-  static_assert(!PAIR || BNL % 32 == 0 || !B_MN, "pair B half must be whole 32-column chunks");
+  constexpr bool FUSE = BN >= 32;            // BN = 16 (MN-major 64-byte boxes): 3 MMAs
   constexpr uint32_t A_BYTES = BM * BK * 4;  // 16 KB
-  constexpr uint32_t B_BYTES = BNL * BK * 4;
-  constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;  // one TMA stage (= the hi operands)
-  constexpr uint32_t LO_BYTES = A_BYTES + B_BYTES;   // one lo slot
-  // NBIG interleaved accumulators for hi*hi (k-block it -> it % NBIG) plus
-  // one for the small cross terms; summed in fp32 in the epilogue.  The
-  // tensor core's fp32 accumulation truncates, so its error grows with the
-  // number of accumulate steps per chain: splitting cuts it ~3*NBIG-fold
-  // (measured: 8.5e-6 -> fp32-FFMA level at K = 1024).
-  constexpr int NBIG = 3;
-  constexpr uint32_t COLS_NEEDED = (NBIG + 1) * BN;
+  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t TMA_BYTES = A_BYTES + B_BYTES;
+  constexpr int NACC = 2;
+  constexpr uint32_t COLS_NEEDED = 2 * NACC * BN;
   constexpr uint32_t TMEM_COLS = COLS_NEEDED <= 32 ? 32 : COLS_NEEDED <= 64 ? 64
                                : COLS_NEEDED <= 128 ? 128 : COLS_NEEDED <= 256 ? 256 : 512;
   static_assert(COLS_NEEDED <= 512, "TMEM overflow");
-  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN, PAIR ? 2 * BM : BM);
+  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN);
+  constexpr uint32_t IDESC2 = instr_desc(FUSE ? 2 * BN : BN, A_MN, B_MN);
+  // epilogue scratch (transpose tiles, bias row sums) behind the dW partial
+  // tile, inside the (by then idle) stage ring
+  constexpr uint32_t PTILE_BYTES = (BM * (BN + 4) * 4 + 1023) / 1024 * 1024;
+  static_assert(PTILE_BYTES + kBiasScratch + 32 * BM * 4 <= TSTAGES * STAGE_BYTES,
+                "epilogue scratch exceeds the stage ring");
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned for the 128B swizzle; offsetting the __shared__ array
   // (not casting through an integer) keeps every derived pointer in the
   // shared window, so the splitter / epilogue accesses compile to LDS / STS
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* raw_ring = smem;                            // TSTAGES x RAW_BYTES
-  uint8_t* lo_ring = smem + TSTAGES * RAW_BYTES;       // LSTAGES x LO_BYTES
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_ring + LSTAGES * LO_BYTES);
+  uint8_t* ring = smem;                                // TSTAGES x STAGE_BYTES
+  uint8_t* alo_ring = smem + TSTAGES * STAGE_BYTES;    // LSTAGES x A_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(alo_ring + LSTAGES * A_BYTES);
   uint64_t* full = bars;                               // TMA landed      [T]
-  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, raw   [T]
+  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, stage [T]
   uint64_t* conv = bars + 2 * TSTAGES;                 // lo ready        [L]
-  uint64_t* empty_l = bars + 2 * TSTAGES + LSTAGES;    // MMA done, lo    [L]
+  uint64_t* empty_l = bars + 2 * TSTAGES + LSTAGES;    // MMA done, A_lo  [L]
   uint64_t* acc_full = bars + 2 * TSTAGES + 2 * LSTAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint8_t* epi = ring + PTILE_BYTES;                   // epilogue scratch
 
   pdl_trigger();  // prologue below touches no data of the previous kernel
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // pairs run along x (cluster (2, 1, S)): grid = (m tiles, n tiles, splits);
-  // otherwise grid = (n tiles, m tiles, splits)
-  const int64_t m_tile = PAIR ? blockIdx.x : blockIdx.y, n_tile = PAIR ? blockIdx.y : blockIdx.x;
-  const int64_t m0 = m_tile * BM, n0 = n_tile * BN;
-  const uint32_t pr = PAIR ? (blockIdx.x & 1u) : 0u;          // rank inside the pair
-  const uint32_t lead = PAIR ? cluster_ctarank() - pr : 0u;   // cluster rank of the leader
-  const int64_t nb0 = n0 + int64_t(pr) * BNL;                  // this CTA's B columns
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
   const int kt0 = blockIdx.z * args.k_tiles_per_split;
   const int kt1 = min(args.k_tiles, kt0 + args.k_tiles_per_split);
   const int nk = kt1 - kt0;
@@ -400,8 +348,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&empty_t[s], 1);
     }
     for (int s = 0; s < LSTAGES; ++s) {
-      // the leader's lo-ready barrier also takes one forwarded arrive from the peer
-      mbar_init(&conv[s], PAIR && pr == 0 ? SPLIT_WARPS + 1 : SPLIT_WARPS);
+      mbar_init(&conv[s], SPLIT_WARPS);
       mbar_init(&empty_l[s], 1);
     }
     mbar_init(acc_full, 1);
@@ -410,23 +357,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    if (PAIR) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "r"(TMEM_COLS)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(tmem_slot)),
-                   "r"(TMEM_COLS)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  if (PAIR) cluster_sync_all();  // the peer arrives on the leader's barriers
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // operands / epilogue inputs come from earlier kernels
@@ -438,9 +376,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       for (int it = 0; it < nk; ++it) {
         const int s = it % TSTAGES;
         if (it >= TSTAGES) mbar_wait(&empty_t[s], ((it / TSTAGES) - 1) & 1);
-        uint8_t* st = raw_ring + s * RAW_BYTES;
+        uint8_t* st = ring + s * STAGE_BYTES;
         const int k0 = (kt0 + it) * BK;
-        mbar_expect_tx(&full[s], RAW_BYTES);
+        mbar_expect_tx(&full[s], TMA_BYTES);
         if (A_MN && args.a3d) {
           tma_load_3d(st, &tmA, &full[s], 0, k0, int(m0 / 32));
         } else if (A_MN) {
@@ -452,39 +390,31 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         uint8_t* sb = st + A_BYTES;
         if (B_MN && args.b3d) {
-          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(nb0 / 32));
+          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
         } else if (B_MN) {
 #pragma unroll
-          for (int c = 0; c < BNL / 32; ++c)
-            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(nb0 + 32 * c), k0);
-          if (BNL % 32)  // BN == 16: a single 16-wide box
-            tma_load_2d(sb, &tmB, &full[s], int(nb0), k0);
+          for (int c = 0; c < BN / 32; ++c)
+            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
+          if (BN % 32)  // BN == 16: a single 16-wide box
+            tma_load_2d(sb, &tmB, &full[s], int(n0), k0);
         } else {
-          tma_load_2d(sb, &tmB, &full[s], k0, int(nb0));
+          tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
         }
       }
     }
   } else if (warp == 1) {
-    // ---- pair peer: forward "lo ready" to the leader, one cluster-scope
-    // release per k-step by a single thread (a release.cluster arrive costs a
-    // GPU-scope fence; the splitter warps only arrive locally)
-    if (PAIR && pr != 0 && lane == 0) {
-      for (int it = 0; it < nk; ++it) {
-        const int l = it % LSTAGES;
-        mbar_wait(&conv[l], (it / LSTAGES) & 1);
-        mbar_arrive_cluster(dsmem_addr(&conv[l], lead));
-      }
-    }
-    // ---- MMA issuer (the pair's leader only)
-    if (lane == 0 && pr == 0) {
+    // ---- MMA issuer
+    if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
         const int t = it % TSTAGES, l = it % LSTAGES;
         mbar_wait(&conv[l], (it / LSTAGES) & 1);
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(raw_ring + t * RAW_BYTES);
+        const uint32_t a_hi = smem_u32(ring + t * STAGE_BYTES);
         const uint32_t b_hi = a_hi + A_BYTES;
-        const uint32_t a_lo = smem_u32(lo_ring + l * LO_BYTES);
-        const uint32_t b_lo = a_lo + A_BYTES;
+        const uint32_t b_lo = b_hi + B_BYTES;
+        const uint32_t a_lo = smem_u32(alo_ring + l * A_BYTES);
+        const uint32_t big = tmem + uint32_t((it % NACC) * 2 * BN);
+        const uint32_t small = big + uint32_t(BN);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
@@ -496,62 +426,60 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint64_t dah = smem_desc(a_hi + ao, a_lbo, a_sbo, a_lay);
           const uint64_t dal = smem_desc(a_lo + ao, a_lbo, a_sbo, a_lay);
           const uint64_t dbh = smem_desc(b_hi + bo, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = smem_desc(b_lo + bo, b_lbo, b_sbo, b_lay);
-          const uint32_t big = tmem + uint32_t((it % NBIG) * BN);
-          const uint32_t small = tmem + uint32_t(NBIG * BN);
-          const uint32_t acc_small = (it > 0 || kk > 0) ? 1u : 0u;
-          const uint32_t acc_big = (it >= NBIG || kk > 0) ? 1u : 0u;
-          if (PAIR) {
-            mma_tf32_pair(small, dal, dbh, IDESC, acc_small);
-            mma_tf32_pair(small, dah, dbl, IDESC, 1u);
-            mma_tf32_pair(big, dah, dbh, IDESC, acc_big);
+          const uint32_t first = (it >= NACC || kk > 0) ? 1u : 0u;
+          if (FUSE) {
+            mma_tf32(big, dah, dbh, IDESC2, first);      // [big | small] = A_hi x [B_hi | B_lo]
           } else {
-            mma_tf32(small, dal, dbh, IDESC, acc_small);
-            mma_tf32(small, dah, dbl, IDESC, 1u);
-            mma_tf32(big, dah, dbh, IDESC, acc_big);
+            const uint64_t dbl = smem_desc(b_lo + bo, b_lbo, b_sbo, b_lay);
+            mma_tf32(big, dah, dbh, IDESC, first);
+            mma_tf32(small, dah, dbl, IDESC, first);
           }
+          mma_tf32(small, dal, dbh, IDESC, 1u);          // small += A_lo x B_hi
         }
-        if (PAIR) {
-          const uint16_t mask = uint16_t(3u << lead);
-          mma_commit_pair(&empty_t[t], mask);
-          mma_commit_pair(&empty_l[l], mask);
-        } else {
-          mma_commit(&empty_t[t]);
-          mma_commit(&empty_l[l]);
-        }
+        mma_commit(&empty_t[t]);
+        mma_commit(&empty_l[l]);
       }
-      if (PAIR) mma_commit_pair(acc_full, uint16_t(3u << lead));
-      else mma_commit(acc_full);
+      mma_commit(acc_full);
     }
   } else {
-    // ---- splitter warps (2..9): lo = x - trunc_tf32(x) for every landed tile.
+    // ---- splitter warps (2..9): lo = x - trunc_tf32(x) of the landed tiles:
+    // A_lo into the A_lo slot, B_lo into the stage right behind B_hi.
     // Fused weight gradient, n-tile 0: the same pass accumulates the row sums
     // of the (MN-major) A tile = the bias gradient.  Thread ct always sees
     // A float4 ct + 256 r (r < 4) of a tile: chunk r (32 rows), k-row ct/8,
     // 16-byte column ct%8 of the 128-byte row (swizzled, see bias_row0).
     const int ct = threadIdx.x - 64;  // 0 .. 32*SPLIT_WARPS-1
-    const bool do_bias = A_MN && args.wf.on && args.wf.bias && n_tile == 0;
-    float4 bsum[4];
+    const bool do_bias = A_MN && args.wf.on && args.wf.bias && blockIdx.x == 0;
+    constexpr int RAW_F4 = int(TMA_BYTES / 16), A_F4 = int(A_BYTES / 16);
+    constexpr int NSPLIT = 32 * SPLIT_WARPS;
+    constexpr int NB = (A_F4 + NSPLIT - 1) / NSPLIT;  // A float4s per thread per tile
+    float4 bsum[NB];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) bsum[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    constexpr int RAW_F4 = int(RAW_BYTES / 16), A_F4 = int(A_BYTES / 16);
+    for (int r = 0; r < NB; ++r) bsum[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int NJ = (RAW_F4 + NSPLIT - 1) / NSPLIT;
     for (int it = 0; it < nk; ++it) {
       const int t = it % TSTAGES, l = it % LSTAGES;
       mbar_wait(&full[t], (it / TSTAGES) & 1);
       if (it >= LSTAGES) mbar_wait(&empty_l[l], ((it / LSTAGES) - 1) & 1);
-      const float4* src = reinterpret_cast<const float4*>(raw_ring + t * RAW_BYTES);
-      float4* dst = reinterpret_cast<float4*>(lo_ring + l * LO_BYTES);
+      const float4* src = reinterpret_cast<const float4*>(ring + t * STAGE_BYTES);
+      float4* dst_a = reinterpret_cast<float4*>(alo_ring + l * A_BYTES);
+      float4* dst_b = reinterpret_cast<float4*>(ring + t * STAGE_BYTES + A_BYTES + B_BYTES) - A_F4;
 #pragma unroll
-      for (int j = 0; j < (RAW_F4 + 32 * SPLIT_WARPS - 1) / (32 * SPLIT_WARPS); ++j) {
-        const int i = ct + 32 * SPLIT_WARPS * j;
-        if (RAW_F4 % (32 * SPLIT_WARPS) == 0 || i < RAW_F4) {
+      for (int j = 0; j < NJ; ++j) {
+        const int i = ct + NSPLIT * j;
+        if (RAW_F4 % NSPLIT == 0 || i < RAW_F4) {
           const float4 x = src[i];
-          dst[i] = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
-                               x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
-                               x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
-                               x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
-          if (j < 4 && i < A_F4 && do_bias) {
-            bsum[j].x += x.x; bsum[j].y += x.y; bsum[j].z += x.z; bsum[j].w += x.w;
+          const float4 lo = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
+                                        x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
+                                        x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
+                                        x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+          if (i < A_F4) {
+            dst_a[i] = lo;
+            if (j < NB && do_bias) {
+              bsum[j].x += x.x; bsum[j].y += x.y; bsum[j].z += x.z; bsum[j].w += x.w;
+            }
+          } else {
+            dst_b[i] = lo;
           }
         }
       }
@@ -567,30 +495,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     mbar_wait(acc_full, 0);
     tc_fence_after();
     const int q = warp & 3;
-    const int half = (warp - 2) / 4;
-    float* tile = reinterpret_cast<float*>(lo_ring) + (warp - 2) * (32 * 20);
+    const int half = warp - 2 < EPI_WARPS ? (warp - 2) / 4 : 2;  // extra splitter warps: none
+    float* tile = reinterpret_cast<float*>(epi) + (warp - 2) * (32 * 20);
     const GemmEpilogue& ep = args.ep;
-    const int used = nk < NBIG ? nk : NBIG;
+    const int used = nk < NACC ? nk : NACC;
     constexpr int CW = BN / 2 < 16 ? 16 : BN / 2;  // columns per warp
 #pragma unroll 1
     for (int c0 = half * CW; c0 < BN && c0 < (half + 1) * CW; c0 += 16) {
-      uint32_t ra[NBIG + 1][16];
+      uint32_t ra[2 * NACC][16];
       const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(c0);
 #pragma unroll
-      for (int j = 0; j <= NBIG; ++j) tmem_ld16_issue(lane_base + uint32_t(j * BN), ra[j]);
+      for (int j = 0; j < 2 * NACC; ++j) tmem_ld16_issue(lane_base + uint32_t(j * BN), ra[j]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       float v[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(ra[NBIG][i]);  // cross terms
+      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(ra[0][i]) + __uint_as_float(ra[1][i]);
+      if (used > 1) {
 #pragma unroll
-      for (int j = 0; j < NBIG; ++j) {
-        if (j < used) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += __uint_as_float(ra[j][i]);
-        }
+        for (int i = 0; i < 16; ++i)
+          v[i] += __uint_as_float(ra[2][i]) + __uint_as_float(ra[3][i]);
       }
       if (args.wf.on) {  // fused weight gradient: the partial tile stays in smem
-        float* prow = reinterpret_cast<float*>(raw_ring) + (32 * q + lane) * (BN + 4) + c0;
+        float* prow = reinterpret_cast<float*>(ring) + (32 * q + lane) * (BN + 4) + c0;
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
           *reinterpret_cast<float4*>(prow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -611,28 +537,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       __syncwarp();
     }
     if (do_bias) {  // per-thread row sums -> [k-row][m] scratch in unswizzled order
-      float* bs = reinterpret_cast<float*>(lo_ring + kBiasScratch);
-      const int kr = ct >> 3, c16 = ct & 7;
+      float* bs = reinterpret_cast<float*>(epi + kBiasScratch);
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        *reinterpret_cast<float4*>(bs + kr * BM + bias_row0(r, kr, c16)) = bsum[r];
+      for (int j = 0; j < NB; ++j) {
+        const int i = ct + NSPLIT * j;  // A float4: chunk i/256, k-row (i/8)%32, column i%8
+        if (i < A_F4) {
+          const int kr = (i >> 3) & 31;
+          *reinterpret_cast<float4*>(bs + kr * BM + bias_row0(i >> 8, kr, i & 7)) = bsum[j];
+        }
+      }
     }
   }
-  if (args.wf.on)
-    wgrad_cluster_reduce<BN, PAIR>(args, raw_ring, lo_ring + kBiasScratch, m0, n0, pr);
+  if (args.wf.on) wgrad_cluster_reduce<BN>(args, ring, epi + kBiasScratch, m0, n0);
   tc_fence_before();
-  if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM / barriers
-  else __syncthreads();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    if (PAIR)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                   "r"(TMEM_COLS)
-                   : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                   "r"(TMEM_COLS)
-                   : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
   }
 }
 
@@ -680,43 +603,28 @@ bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-constexpr size_t smem_bytes(int bn, bool pair) {
-  return size_t(raw_stages(pair) + lo_stages(pair)) * (BM * BK * 4 + bn * BK * 4) + 1024 + 256;
+constexpr size_t smem_bytes(int bn) {
+  return size_t(TSTAGES) * (BM * BK * 4 + 2 * bn * BK * 4) + size_t(LSTAGES) * BM * BK * 4 +
+         1024 + 256;
 }
 
-// CTA pairs are OFF by default: measured on B200 (scripts/gemm_one.py,
-// 2048 x 1024 x K), the pair kernel matches but does not beat the single-CTA
-// kernel (K=1024: 28.7 vs 28.3 us; K=4096: 91.9 vs 91.9 us) — the steady
-// state is bound by the TMA feed + MMA shared-memory contention (1050
-// cycles / k-step without the splitter vs 830 for the MMAs alone), and the
-// pair's lock-stepped SMs give back what the halved B traffic saves.
-// DLRM_TC_PAIR=1 enables them.
-bool pair_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("DLRM_TC_PAIR");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
-template <bool A_MN, bool B_MN, int BN, bool PAIR>
+template <bool A_MN, bool B_MN, int BN>
 int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
               int splits, cudaStream_t s) {
-  auto k = tc_gemm_kernel<A_MN, B_MN, BN, PAIR>;
-  const size_t sm = smem_bytes(PAIR ? BN / 2 : BN, PAIR);
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
+  const size_t sm = smem_bytes(BN);
   static bool configured = false;
   if (!configured) {
     DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     configured = true;
   }
-  const unsigned nt = unsigned(ceil_div(n_grid, BN)), mt = unsigned(ceil_div(args.M, BM));
-  dim3 grid = PAIR ? dim3(mt, nt, unsigned(splits)) : dim3(nt, mt, unsigned(splits));
-  if (!args.wf.on && !PAIR) {
+  const dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)),
+                  unsigned(splits));
+  if (!args.wf.on) {
     launch(k, grid, THREADS, sm, s, a, b, args);
     return check_launch("tc_gemm_kernel");
   }
-  // CTA pairs along y and / or the split-K CTAs of a weight-gradient tile
-  // along z form one cluster
+  // fused weight gradient: the split-K CTAs of a tile are one cluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
@@ -724,9 +632,9 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = args.wf.on ? unsigned(splits) : 1;
+  attr[0].val.clusterDim.z = unsigned(splits);
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
@@ -735,25 +643,24 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   return check_launch("tc_gemm_kernel(cluster)");
 }
 
-// Concurrently resident clusters of (PAIR ? 2 : 1, 1, cz) CTAs of the
-// BN-wide kernel; cached per instantiation and cz.
-template <bool A_MN, bool B_MN, int BN, bool PAIR>
+// Concurrently resident clusters of (1, 1, cz) CTAs of the BN-wide kernel
+// (the split-K clusters of the fused weight gradient); cached per (BN, cz).
+template <bool A_MN, bool B_MN, int BN>
 int max_clusters(int cz) {
   static int cache[17] = {0};
   if (cz < 1 || cz > 16) return 1;
   if (cache[cz]) return cache[cz];
-  auto k = tc_gemm_kernel<A_MN, B_MN, BN, PAIR>;
-  const size_t sm = smem_bytes(PAIR ? BN / 2 : BN, PAIR);
+  auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
+  const size_t sm = smem_bytes(BN);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  const int csz = cz * (PAIR ? 2 : 1);
-  if (csz > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (cz > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(PAIR ? 2 : 1, 1, unsigned(cz));
+  cfg.gridDim = dim3(1, 1, unsigned(cz));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = sm;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = unsigned(cz);
   cfg.attrs = attr;
@@ -761,7 +668,7 @@ int max_clusters(int cz) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) {
     cudaGetLastError();
-    n = kNumSMs / csz;
+    n = kNumSMs / cz;
   }
   cache[cz] = n;
   return n;
@@ -807,22 +714,13 @@ TcPlan plan_tc(int64_t M, int64_t n_grid, int64_t kt, bool allow_split, int min_
 
 template <bool A_MN, bool B_MN>
 int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
-           int bn, int splits, bool pair, cudaStream_t s) {
-  if (pair) {
-    if (bn == 64) return launch_bn<A_MN, B_MN, 64, true>(a, b, args, n_grid, splits, s);
-    return launch_bn<A_MN, B_MN, 128, true>(a, b, args, n_grid, splits, s);
-  }
+           int bn, int splits, cudaStream_t s) {
   switch (bn) {
-    case 16: return launch_bn<A_MN, B_MN, 16, false>(a, b, args, n_grid, splits, s);
-    case 32: return launch_bn<A_MN, B_MN, 32, false>(a, b, args, n_grid, splits, s);
-    case 64: return launch_bn<A_MN, B_MN, 64, false>(a, b, args, n_grid, splits, s);
-    default: return launch_bn<A_MN, B_MN, 128, false>(a, b, args, n_grid, splits, s);
+    case 16: return launch_bn<A_MN, B_MN, 16>(a, b, args, n_grid, splits, s);
+    case 32: return launch_bn<A_MN, B_MN, 32>(a, b, args, n_grid, splits, s);
+    case 64: return launch_bn<A_MN, B_MN, 64>(a, b, args, n_grid, splits, s);
+    default: return launch_bn<A_MN, B_MN, 128>(a, b, args, n_grid, splits, s);
   }
-}
-
-// CTA pairs need an even number of 128-row tiles and whole 32-column B halves
-bool use_pair(int64_t M, int bn) {
-  return pair_enabled() && (bn == 64 || bn == 128) && ceil_div(M, BM) % 2 == 0;
 }
 
 // MN-major operand whose MN extent is a multiple of 32, seen as the 3D
@@ -873,17 +771,16 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
                   float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
                   int act, cudaStream_t s) {
   const int bn = plan_tc(M, n_grid, ceil_div(K, BK), false, 16, 0).bn;
-  const bool pair = use_pair(M, bn);
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
-                   map_operand(&mb, W, false, N, K, ldw, pair ? bn / 2 : bn),
+                   map_operand(&mb, W, false, N, K, ldw, bn),
                "tensor map encoding failed (linear_fwd)");
   TcArgs a{M, N, K, 0, 0, GemmEpilogue{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, n_grid, M,
                                         aligned16(Y) && ldy % 4 == 0 && aligned16(b)},
            0, 0};
   a.k_tiles = int(ceil_div(K, BK));
   a.k_tiles_per_split = a.k_tiles;
-  return launch<false, false>(ma, mb, a, n_grid, bn, 1, pair, s);
+  return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
 }
 
 bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
@@ -899,19 +796,17 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
                        int64_t N, int64_t K, cudaStream_t s) {
   // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
   const int bn = plan_tc(M, K, ceil_div(N, BK), false, 32, 0).bn;
-  const bool pair = use_pair(M, bn);
-  const int bnl = pair ? bn / 2 : bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
-                   map_operand(&mb, W, true, K, N, ldw, bnl),
+                   map_operand(&mb, W, true, K, N, ldw, bn),
                "tensor map encoding failed (linear_bwd_data)");
   TcArgs a{M, K, N, 0, 0, GemmEpilogue{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M,
                                         aligned16(dX) && ldx % 4 == 0 &&
                                             (!mask || (aligned16(mask) && ldm % 4 == 0))},
-           0, use3d(true, K, bnl)};
+           0, use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(N, BK));
   a.k_tiles_per_split = a.k_tiles;
-  return launch<false, true>(ma, mb, a, K, bn, 1, pair, s);
+  return launch<false, true>(ma, mb, a, K, bn, 1, s);
 }
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
@@ -935,19 +830,12 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
     const int64_t tiles = mt * ceil_div(K, bn);
     int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
     if (smax < 1) smax = 1;
-    const bool pair = use_pair(N, bn);
-    if (pair && smax > 4) smax = 4;  // cluster (2, 1, sp) <= 8 CTAs
     for (int64_t sp = 1; sp <= smax; ++sp) {
-      int cap;  // co-resident clusters, in units of 128-row tiles
-      if (pair)
-        cap = 2 * (bn == 128 ? max_clusters<true, true, 128, true>(int(sp))
-                             : max_clusters<true, true, 64, true>(int(sp)));
-      else
-        cap = bn == 128 ? max_clusters<true, true, 128, false>(int(sp))
-            : bn == 64  ? max_clusters<true, true, 64, false>(int(sp))
-                        : max_clusters<true, true, 32, false>(int(sp));
+      const int cap = bn == 128 ? max_clusters<true, true, 128>(int(sp))
+                    : bn == 64  ? max_clusters<true, true, 64>(int(sp))
+                                : max_clusters<true, true, 32>(int(sp));
       const double waves = double(ceil_div(tiles, cap));
-      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn) * (pair ? 0.8 : 1.0)) +
+      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn)) +
                        (sp > 1 ? 400.0 * double(sp) : 0.0);
       if (t < best_t) {
         best_t = t;
@@ -967,13 +855,11 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   // db (N) = row sums of the A operand; both reduced over the split-K cluster
   const TcPlan pl = weight_plan(M, N, K);
   const int bn = pl.bn;
-  const bool pair = use_pair(N, bn);
-  const int bnl = pair ? bn / 2 : bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, true, N, M, ldg, BM) &&
-                   map_operand(&mb, X, true, K, M, ldx, bnl),
+                   map_operand(&mb, X, true, K, M, ldx, bn),
                "tensor map encoding failed (linear_bwd_weight)");
-  TcArgs a{N, K, M, 0, 0, GemmEpilogue{}, use3d(true, N, BM), use3d(true, K, bnl)};
+  TcArgs a{N, K, M, 0, 0, GemmEpilogue{}, use3d(true, N, BM), use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(M, BK));
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
@@ -982,7 +868,8 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
                    (u.kind != DLRM_UPD_ADAGRAD || u.delta % 4 == 0);
   a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, u, err_flag,
                    vec ? 1 : 0};
-  return launch<true, true>(ma, mb, a, K, bn, used, pair, s);
+
+  return launch<true, true>(ma, mb, a, K, bn, used, s);
 }
 
 }  // namespace dlrm
