@@ -232,6 +232,20 @@ int dlrm_bce_head(const float* A, int64_t lda, const float* w, const float* b,
                   float* stats, void* workspace, size_t ws_bytes,
                   dlrm_stream_t stream);
 
+/* The whole loss head in two launches (forward of the N = 1 layer, BCE,
+ * logit gradient, and its backward + update; one pass over A): what
+ * dlrm_bce_head followed by dlrm_head_bwd_upd compute, with dw / db / the
+ * loss statistics reduced in a fixed CTA order.  Needs K % 4 == 0,
+ * K <= 1024, 16-byte aligned A / w / dA rows.  Optional outputs may be NULL:
+ * prob, grad_z, dA, dw, db, w_upd, b_upd. */
+size_t dlrm_head_step_workspace_size(int64_t M, int64_t K);
+int dlrm_head_step(const float* A, int64_t lda, const float* w, const float* b,
+                   int64_t M, int64_t K, const float* y, float n_total, float* prob,
+                   float* grad_z, float* stats, float* dA, int64_t ldda,
+                   int32_t relu_mask, float* dw, float* db, float* w_upd, float* b_upd,
+                   const dlrm_update* upd, const int32_t* err_flag, void* workspace,
+                   size_t ws_bytes, dlrm_stream_t stream);
+
 /* Backward through the N = 1 head: dA[m,k] = g[m]*w[k] (* (A[m,k] > 0) when
  * relu_mask, i.e. A is a ReLU output); dw[k] = sum_m g[m]*A[m,k];
  * db = sum_m g[m]; optional fused SGD (w -= lr*dw, b -= lr*db). */

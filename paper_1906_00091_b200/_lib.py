@@ -57,6 +57,8 @@ _SIGS = {
     "dlrm_head_bwd_upd": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _i32, _vp,
                           _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
     "dlrm_update_dense": [_vp, _vp, _i64, _vp, _vp, _vp],
+    "dlrm_head_step": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp,
+                       _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
     "dlrm_emb_bwd_coalesce": [_i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _sz, _vp],
     "dlrm_sgd_rows": [_vp, _i64, _vp, _vp, _i64, _f32, _vp],
@@ -83,6 +85,7 @@ _SIZE_FNS = {
     "dlrm_linear_bwd_weight_workspace_size": [_i64, _i64, _i64],
     "dlrm_bce_head_workspace_size": [_i64],
     "dlrm_head_bwd_workspace_size": [_i64, _i64],
+    "dlrm_head_step_workspace_size": [_i64, _i64],
 }
 
 # every symbol include/dlrm_b200.h declares (checked by tests/test_abi.py)

@@ -117,10 +117,170 @@ __global__ void relu_grad_kernel(const float* __restrict__ g, int64_t ldg,
   out[m * ldo + n] = g[m * ldg + n] * (a[m * lda + n] > 0.f ? 1.f : 0.f);
 }
 
+// ---------------------------------------------------------------------------
+// Fused head step: forward of the N = 1 layer + BCE + logit gradient + the
+// layer's backward in one pass over A.  A CTA owns HR rows; each warp takes
+// HR/8 of them: z = A[m].w + b (warp reduction), sigma / loss / correct /
+// g = (p - y)/n by lane 0, then dA[m] = g w (* ReLU mask) and the row's
+// contribution g A[m] to dw, all while A[m] is in registers (K <= 32*4*KV).
+// Per-CTA partials (dw [K], sum g, sum loss, #correct) go to the workspace in
+// a fixed order; head_final reduces them in CTA order and applies the update.
+constexpr int HR = 16;  // rows per CTA
+
+template <int KV>  // float4 per lane per row: K <= 128 * KV
+__global__ void __launch_bounds__(256)
+head_fused_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ w,
+                  const float* __restrict__ b, int64_t M, int64_t K,
+                  const float* __restrict__ y, float n_total, float* prob, float* grad_z,
+                  float* __restrict__ dA, int64_t ldda, int relu_mask,
+                  float* __restrict__ part) {
+  pdl_entry();
+  __shared__ float4 s_dw[8][32 * KV];
+  __shared__ float s_sc[8][3];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t kv = K / 4;
+  float4 wv[KV], dw[KV];
+#pragma unroll
+  for (int j = 0; j < KV; ++j) {
+    const int64_t c = lane + 32 * j;
+    wv[j] = c < kv ? __ldg(reinterpret_cast<const float4*>(w) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    dw[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float sg = 0.f, sl = 0.f, sok = 0.f;
+  for (int r = warp; r < HR; r += 8) {
+    const int64_t m = int64_t(blockIdx.x) * HR + r;
+    if (m >= M) break;
+    const float4* a = reinterpret_cast<const float4*>(A + m * lda);
+    float4 av[KV];
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const int64_t c = lane + 32 * j;
+      av[j] = c < kv ? __ldg(a + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      acc = fmaf(av[j].x, wv[j].x, acc);
+      acc = fmaf(av[j].y, wv[j].y, acc);
+      acc = fmaf(av[j].z, wv[j].z, acc);
+      acc = fmaf(av[j].w, wv[j].w, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    float g = 0.f;
+    if (lane == 0) {
+      const float z = acc + b[0];
+      const float yy = y[m];
+      const float per = fmaxf(z, 0.f) - z * yy + log1pf(expf(-fabsf(z)));
+      const float p = stable_sigmoid(z);
+      if (prob) prob[m] = p;
+      g = __fdiv_rn(p - yy, n_total);
+      if (grad_z) grad_z[m] = g;
+      sl += per;
+      sok += ((p > 0.5f) == (yy > 0.5f)) ? 1.f : 0.f;
+      sg += g;
+    }
+    g = __shfl_sync(0xffffffffu, g, 0);
+    float4* da = reinterpret_cast<float4*>(dA + m * ldda);
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const int64_t c = lane + 32 * j;
+      if (c < kv) {
+        float4 v = make_float4(g * wv[j].x, g * wv[j].y, g * wv[j].z, g * wv[j].w);
+        if (relu_mask) {
+          v.x *= av[j].x > 0.f ? 1.f : 0.f; v.y *= av[j].y > 0.f ? 1.f : 0.f;
+          v.z *= av[j].z > 0.f ? 1.f : 0.f; v.w *= av[j].w > 0.f ? 1.f : 0.f;
+        }
+        if (dA) da[c] = v;
+        dw[j].x = fmaf(g, av[j].x, dw[j].x);
+        dw[j].y = fmaf(g, av[j].y, dw[j].y);
+        dw[j].z = fmaf(g, av[j].z, dw[j].z);
+        dw[j].w = fmaf(g, av[j].w, dw[j].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KV; ++j) s_dw[warp][lane + 32 * j] = dw[j];
+  if (lane == 0) { s_sc[warp][0] = sg; s_sc[warp][1] = sl; s_sc[warp][2] = sok; }
+  __syncthreads();
+  // CTA partial, warps summed in order: part[cta] = [dw (K) | sum g | loss | ok]
+  float* pc = part + int64_t(blockIdx.x) * (K + 3);
+  for (int64_t c = threadIdx.x; c < kv; c += blockDim.x) {
+    float4 t = s_dw[0][c];
+    for (int q = 1; q < 8; ++q) {
+      const float4 u = s_dw[q][c];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    pc[4 * c] = t.x; pc[4 * c + 1] = t.y; pc[4 * c + 2] = t.z; pc[4 * c + 3] = t.w;
+  }
+  if (threadIdx.x < 3) {
+    float t = 0.f;
+    for (int q = 0; q < 8; ++q) t += s_sc[q][threadIdx.x];
+    pc[K + threadIdx.x] = t;
+  }
+}
+
+// dw[k] / db / stats reduced over the CTA partials in CTA order; optional
+// outputs and the fused update (skipped when *err_flag).
+__global__ void __launch_bounds__(256)
+head_final_kernel(const float* __restrict__ part, int64_t nparts, int64_t K, float* dw,
+                  float* db, float* stats, float* w_upd, float* b_upd, Upd u,
+                  const int32_t* err_flag) {
+  pdl_entry();
+  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // 0..K+2
+  if (c >= K + 3) return;
+  float t = part[c];
+  for (int64_t i = 1; i < nparts; ++i) t += part[i * (K + 3) + c];
+  const bool upd = !(err_flag && *err_flag);
+  if (c < K) {
+    if (dw) dw[c] = t;
+    if (w_upd && upd) w_upd[c] = upd_apply(u, w_upd + c, w_upd[c], t);
+  } else if (c == K) {
+    if (db) db[0] = t;
+    if (b_upd && upd) b_upd[0] = upd_apply(u, b_upd, b_upd[0], t);
+  } else if (stats) {
+    stats[c - K - 1] = t;  // [0] loss sum, [1] correct count
+  }
+}
+
 }  // namespace
 }  // namespace dlrm
 
 using namespace dlrm;
+
+extern "C" size_t dlrm_head_step_workspace_size(int64_t M, int64_t K) {
+  return size_t(ceil_div(M > 0 ? M : 1, HR)) * size_t(K + 3) * sizeof(float) + 256;
+}
+
+extern "C" int dlrm_head_step(const float* A, int64_t lda, const float* w, const float* b,
+                              int64_t M, int64_t K, const float* y, float n_total, float* prob,
+                              float* grad_z, float* stats, float* dA, int64_t ldda,
+                              int32_t relu_mask, float* dw, float* db, float* w_upd,
+                              float* b_upd, const dlrm_update* upd, const int32_t* err_flag,
+                              void* workspace, size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 1 && K >= 4 && K % 4 == 0 && K <= 128 * 8 && lda % 4 == 0 &&
+                   (!dA || ldda % 4 == 0),
+               "head_step needs K in [4, 1024], K % 4 == 0 and 16-byte rows");
+  DLRM_REQUIRE(reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0 &&
+                   (!dA || reinterpret_cast<uintptr_t>(dA) % 16 == 0),
+               "head_step needs 16-byte aligned A / w / dA");
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(workspace && ws_bytes >= dlrm_head_step_workspace_size(M, K),
+               "head_step workspace too small");
+  cudaStream_t s = as_stream(stream);
+  float* part = static_cast<float*>(workspace);
+  const int64_t nb = ceil_div(M, HR);
+  const int kvl = int(ceil_div(K / 4, 32));
+  auto go = [&](auto kern) {
+    launch(kern, unsigned(nb), 256, 0, s, A, lda, w, b, M, K, y, n_total, prob, grad_z, dA,
+           ldda, relu_mask, part);
+  };
+  if (kvl <= 2) go(head_fused_kernel<2>);
+  else if (kvl <= 4) go(head_fused_kernel<4>);
+  else go(head_fused_kernel<8>);
+  if (int rc = check_launch("head_fused_kernel")) return rc;
+  launch(head_final_kernel, unsigned(ceil_div(K + 3, 256)), 256, 0, s, part, nb, K, dw, db, stats,
+         w_upd, b_upd, upd_rule(upd), err_flag);
+  return check_launch("head_final_kernel");
+}
 
 extern "C" int dlrm_relu_grad(const float* g, int64_t ldg, const float* act,
                               int64_t lda, float* out, int64_t ldo, int64_t M,

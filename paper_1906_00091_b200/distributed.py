@@ -31,6 +31,7 @@ CPU (tests/test_distributed_cpu.py, world_size 2); the kernels need the GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -249,7 +250,10 @@ class RankEngine:
         lin = max(_lib.size("dlrm_linear_bwd_weight_workspace_size", Bl,
                             l.n_out, l.n_in) for l in self.layers)
         lin = max(lin, _lib.size("dlrm_head_bwd_workspace_size", Bl, tl[-1].n_in),
-                  _lib.size("dlrm_bce_head_workspace_size", Bl))
+                  _lib.size("dlrm_bce_head_workspace_size", Bl),
+                  _lib.size("dlrm_head_step_workspace_size", Bl, tl[-1].n_in))
+        self.head_fused = tl[-1].n_in % 4 == 0 and tl[-1].n_in <= 1024 and \
+            os.environ.get("DLRM_HEAD_FUSED", "1") != "0"
         self.lin_ws_bytes = lin
         self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
         self.stats = torch.zeros(3, **f32)
@@ -374,10 +378,22 @@ class RankEngine:
                  P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
             a, lda = out, out.stride(0)
         head = L[-1]
-        call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), Bl,
-             head.n_in, P(self.labels), float(self.Bg), None, P(self.prob),
-             P(self.glogit), None, P(self.stats), P(self.lin_ws),
-             self.lin_ws_bytes, s)
+        if self.head_fused:
+            # the loss head's forward AND backward in one pass (same kernels
+            # as the fused single-device step): prob, the logit gradient, the
+            # loss statistics, dA for the top backward and the head's dw / db
+            gw, gb = self.gslots[-1]
+            ga = self.gtop[-1] if self.Lt > 1 else self.gR
+            call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), Bl,
+                 head.n_in, P(self.labels), float(self.Bg), P(self.prob), P(self.glogit),
+                 P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw), P(gb),
+                 None, None, C.byref(self.upd_mlp), None, P(self.lin_ws),
+                 self.lin_ws_bytes, s)
+        else:
+            call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), Bl,
+                 head.n_in, P(self.labels), float(self.Bg), None, P(self.prob),
+                 P(self.glogit), None, P(self.stats), P(self.lin_ws),
+                 self.lin_ws_bytes, s)
         self._head_in = (a, lda)
 
     def phase_b_top_backward(self, stream=None):
@@ -388,9 +404,10 @@ class RankEngine:
         head = L[-1]
         gw, gb = self.gslots[-1]
         ga = self.gtop[-1] if self.Lt > 1 else self.gR
-        call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), Bl,
-             head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw),
-             P(gb), None, None, 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+        if not self.head_fused:
+            call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), Bl,
+                 head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw),
+                 P(gb), None, None, 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
         for i in range(self.Lt - 2, -1, -1):
             li = self.Lb + i
             l = L[li]

@@ -173,7 +173,12 @@ class StepEngine:
                             l.n_out, l.n_in) for l in self.layers)
         lin = max(lin, _lib.size("dlrm_head_bwd_workspace_size", B,
                                  tl[-1].n_in),
-                  _lib.size("dlrm_bce_head_workspace_size", B))
+                  _lib.size("dlrm_bce_head_workspace_size", B),
+                  _lib.size("dlrm_head_step_workspace_size", B, tl[-1].n_in))
+        # the fused loss head takes K % 4 == 0, K <= 1024 (ldw / ld of the
+        # input are multiples of 4 by construction)
+        self.head_fused = tl[-1].n_in % 4 == 0 and tl[-1].n_in <= 1024 and \
+            os.environ.get("DLRM_HEAD_FUSED", "1") != "0"
         self.lin_ws_bytes = lin
         self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
         self.stats = torch.zeros(2, **f32)
@@ -382,15 +387,23 @@ class StepEngine:
         mark("loss_head")
         head = L[-1]
         ws, wsb = P(self.lin_ws), self.lin_ws_bytes
-        call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), B,
-             head.n_in, P(self.labels), self.n_total, P(self.logits),
-             P(self.prob), P(self.glogit), None, P(self.stats), ws, wsb, s)
-        # head backward (dA masked by the ReLU below it) + fused SGD
         ga = self.gtop[-1] if self.Lt > 1 else self.gR
         um, ue = C.byref(self.upd_mlp), C.byref(self.upd_emb)
-        call("dlrm_head_bwd_upd", P(a), lda, P(head.storage), P(self.glogit), B,
-             head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None,
-             None, P(head.storage), P(head.bias), um, ef, ws, wsb, s)
+        if self.head_fused:
+            # forward + BCE + backward (dA masked by the ReLU below) + update
+            # of the N = 1 layer in one pass over its input
+            call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), B,
+                 head.n_in, P(self.labels), self.n_total, P(self.prob), P(self.glogit),
+                 P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None, None,
+                 P(head.storage), P(head.bias), um, ef, ws, wsb, s)
+        else:
+            call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), B,
+                 head.n_in, P(self.labels), self.n_total, P(self.logits),
+                 P(self.prob), P(self.glogit), None, P(self.stats), ws, wsb, s)
+            # head backward (dA masked by the ReLU below it) + fused update
+            call("dlrm_head_bwd_upd", P(a), lda, P(head.storage), P(self.glogit), B,
+                 head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None,
+                 None, P(head.storage), P(head.bias), um, ef, ws, wsb, s)
         # top MLP backward
         mark("top_mlp_bwd")
         for i in range(self.Lt - 2, -1, -1):
