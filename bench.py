@@ -32,6 +32,7 @@
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -249,6 +250,66 @@ def time_embedding_kernels(eng, flush, reps=5):
             tot += e0.elapsed_time(e1)
         out[name] = tot / reps
     return out
+
+
+def hybrid_roofline(c, tr, hb, flush):
+    """Embedding roofline of one rank of the hybrid step: its owned tables'
+    lookup over the global batch and the full sparse backward (prepare +
+    apply, lr = 0), launched alone (CUDA events, L2 flushed); algorithmic
+    bytes from the rank's own batch."""
+    import torch
+    from paper_1906_00091_b200 import _lib
+    e = tr.engine
+    To = len(e.own)
+    if To == 0:
+        return None
+    P, call = _lib.ptr, _lib.call
+    s = torch.cuda.current_stream()
+    h = _lib.stream_handle(s)
+    d, Bg = e.d, e.Bg
+    descs = C.cast(e._descs, C.c_void_p)
+    upd = _lib.Update(_lib.UPD_SGD, 0.0, 0.0, 0)
+
+    def fwd():
+        call("dlrm_emb_fwd", P(e.W_own), d, descs, To, Bg, P(e.send), To * d,
+             P(e.err_pos), P(e.err_flag), h)
+
+    def bwd():
+        call("dlrm_emb_bwd_prepare", d, descs, To, Bg, e.total_rows, P(e.emb_ws),
+             e.emb_ws_bytes, h)
+        call("dlrm_emb_bwd_apply", P(e.W_own), d, descs, To, Bg, P(e.grecv), To * d,
+             C.byref(upd), P(e.err_flag), e.total_rows, P(e.emb_ws), e.emb_ws_bytes, h)
+
+    ms = {}
+    for name, fn in (("fwd", fwd), ("bwd", bwd)):
+        fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for rep in range(5):
+            flush.fill_(rep & 0xff)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        ms[name] = tot / 5
+    fwd_b = bwd_b = 0.0
+    for o, i in zip(hb[2], hb[3]):
+        nnz, u = int(i.size), int(np.unique(i).size)
+        fwd_b += nnz * (4 * d + 8) + (Bg + 1) * 8 + Bg * 4 * d
+        bwd_b += Bg * 4 * d + nnz * 8 + (Bg + 1) * 8 + 2 * u * 4 * d
+    pk, pk_kind = peaks()
+    gbs = fwd_b / (ms["fwd"] / 1e3) / 1e9
+    return {"kernel": "embedding_fwd (owned tables, global batch)", "bound": "hbm",
+            "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": gbs / pk["hbm_gbs"], "traffic": None, "ms_per_launch": ms["fwd"],
+            "algorithmic_bytes_per_launch": fwd_b,
+            "embedding_bwd_full_standalone": {
+                "GB/s": bwd_b / (ms["bwd"] / 1e3) / 1e9, "ms": ms["bwd"], "bytes": bwd_b,
+                "frac": bwd_b / (ms["bwd"] / 1e3) / 1e9 / pk["hbm_gbs"]},
+            "peak_kind": pk_kind + " copy bandwidth (MEASURED_PEAKS.json)"}
 
 
 def algorithmic(c, B, hbs, eng):
@@ -488,11 +549,13 @@ def run_hybrid(args, c, rank, world, dist):
     model = init_model(cfg, table_init="device")
     plan = make_plan(cfg, Bg, world)
     own = plan.owned(rank)
-    caps = [Bg * c["k"]] * len(own)
     ar_group = dist.new_group(list(range(world)))
-    tr = HybridTrainer(model, plan, rank, caps, lr=0.1, ar_group=ar_group)
     P = args.pool
     hbs = rank_batches(c, plan, rank, P, seed=1)
+    # index capacity per owned table = the largest batch of the pool (the
+    # captured graph serves every batch; the sort runs over the capacity)
+    caps = [max(int(b[3][j].size) for b in hbs) for j in range(len(own))]
+    tr = HybridTrainer(model, plan, rank, caps, lr=0.1, ar_group=ar_group)
 
     # the data pipeline packs each batch once into the rank's input-block
     # layout (pinned host); the device pool holds the same blocks in HBM
@@ -544,6 +607,7 @@ def run_hybrid(args, c, rank, world, dist):
     torch.cuda.synchronize()
     r = tr.result()
     clk.__exit__()
+    roofline = hybrid_roofline(c, tr, hbs[0], flush)
     t = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e = Bg * K / (float(t.item()) / 1e3)
@@ -562,7 +626,7 @@ def run_hybrid(args, c, rank, world, dist):
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 12},
             "gpu_launches": launches * K, "loss_last": r.loss,
-            "clocks": clk.summary(), "roofline": None, "cpu_baseline": None,
+            "clocks": clk.summary(), "roofline": roofline, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
 
