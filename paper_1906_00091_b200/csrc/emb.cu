@@ -1232,9 +1232,14 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
   for (int i = 0; i < nt; ++i) cap_total += tables[i].capacity;
   const double avg_pool = double(cap_total) / double(num_bags * nt);
   const int64_t nv0 = dim / 4;
-  // streaming kernel for multi-hot bags and wide rows; pooling-1 narrow rows
-  // keep the sub-warp kernel (lower fixed latency)
-  bool stream_ok = v4 && nv0 <= 128 && (nv0 & (nv0 - 1)) == 0 && (avg_pool >= 3.0 || nv0 >= 32) &&
+  // streaming kernel for multi-hot bags, wide rows and large batches;
+  // pooling-1 narrow rows keep the sub-warp kernel (lower fixed latency)
+  static const bool force_stream = getenv("DLRM_EMB_FORCE_STREAM") != nullptr;
+  // (measured: pooling-1 bags of 256-byte rows stream faster from 128 k
+  // lookups up; 64-byte rows never do)
+  bool stream_ok = v4 && nv0 <= 128 && (nv0 & (nv0 - 1)) == 0 &&
+                   (avg_pool >= 3.0 || nv0 >= 32 || (nv0 >= 16 && cap_total >= 131072) ||
+                    force_stream) &&
                    !getenv("DLRM_EMB_NO_STREAM");
   for (int i = 0; i < nt && stream_ok; ++i) stream_ok = tables[i].num_rows < int64_t(kBadRow);
   if (stream_ok) {
