@@ -131,6 +131,13 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool ok
                : "memory");
 #endif
 }
+// the same through L1 (cp.async.ca): repeated rows hit in L1
+__device__ __forceinline__ void cp_async16_l1(void* smem, const void* gmem, bool ok) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int n = ok ? 16 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

@@ -390,7 +390,7 @@ emb_fwd_stream_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int
       return r;
     };
     StreamIdx q0 = load_idx(0), q1 = load_idx(1);
-    int issued = 0, islot = 0;
+    int issued = 0, islot = 0, hot = 0;
     auto issue = [&]() {
       if (issued < nch) {
         const int64_t p0 = P0 + int64_t(issued) * CH;
@@ -404,13 +404,32 @@ emb_fwd_stream_kernel(const float* __restrict__ W, int64_t dim, TableSet ts, int
         }
         float4* slot = ring + islot * SLOT;
         if (wts && lane < CH) wring[islot * CH + lane] = q0.w;
+        // Skew detector: a row repeated inside one chunk means a hot working
+        // set (e.g. Zipf indices), whose rows all SMs would otherwise fetch
+        // from the same few L2 slices; such a warp loads through L1 for the
+        // next 8 chunks, where the hot rows hit.  Uniform indices essentially
+        // never repeat within a chunk and keep the L1-bypassing path.
+        const unsigned peers = __match_any_sync(0xffffffffu, lane < cnt ? myrow : ~0u - lane);
+        if (__any_sync(0xffffffffu, lane < cnt && __popc(peers) > 1)) hot = 8;
+        else if (hot > 0) --hot;
+        if (hot > 0) {
 #pragma unroll
-        for (int i = 0; i < PER_LANE; ++i) {
-          const int e = lane + 32 * i;
-          const int r = e / NVM, cc = e % NVM;
-          const uint32_t rr = __shfl_sync(0xffffffffu, myrow, r < CH ? r : 0);
-          const bool ok = rr != kBadRow;
-          if (e < SLOT) cp_async16(slot + e, Wt + size_t(ok ? rr : 0u) * NVM + cc, ok);
+          for (int i = 0; i < PER_LANE; ++i) {
+            const int e = lane + 32 * i;
+            const int r = e / NVM, cc = e % NVM;
+            const uint32_t rr = __shfl_sync(0xffffffffu, myrow, r < CH ? r : 0);
+            const bool ok = rr != kBadRow;
+            if (e < SLOT) cp_async16_l1(slot + e, Wt + size_t(ok ? rr : 0u) * NVM + cc, ok);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < PER_LANE; ++i) {
+            const int e = lane + 32 * i;
+            const int r = e / NVM, cc = e % NVM;
+            const uint32_t rr = __shfl_sync(0xffffffffu, myrow, r < CH ? r : 0);
+            const bool ok = rr != kBadRow;
+            if (e < SLOT) cp_async16(slot + e, Wt + size_t(ok ? rr : 0u) * NVM + cc, ok);
+          }
         }
       }
       cp_async_commit();
@@ -1262,6 +1281,8 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
       if (cfg == 0) DLRM_STREAM(16, 32, 4, 6);
       if (cfg == 2) DLRM_STREAM(16, 16, 4, 12);
       if (cfg == 4) DLRM_STREAM(16, 32, 3, 8);
+      if (cfg == 5) DLRM_STREAM(16, 16, 3, 8);
+      if (cfg == 6) DLRM_STREAM(16, 16, 2, 8);
       DLRM_STREAM(16, 16, 3, 16);
     }
     if (nv0 == 32) {
