@@ -618,7 +618,10 @@ struct FoldArgs {
   uint4* long_runs;      // (start, end, row, 0)
 };
 
-constexpr int kLongRun = 96;
+#ifndef DLRM_LONG_RUN
+#define DLRM_LONG_RUN 96
+#endif
+constexpr int kLongRun = DLRM_LONG_RUN;
 
 template <int LPB>
 constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
@@ -1008,8 +1011,18 @@ seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
   const uint32_t g0 = seg_base[r];
   const uint32_t ns = (run.y - run.x + kSeg - 1) / kSeg;
   for (int64_t c = threadIdx.x; c < dim; c += blockDim.x) {
-    float v = partial[int64_t(g0) * dim + c];
-    for (uint32_t k = 1; k < ns; ++k) v = __fadd_rn(v, partial[int64_t(g0 + k) * dim + c]);
+    // partials added in segment order; loads issued 8 ahead of the adds
+    const float* pc = partial + int64_t(g0) * dim + c;
+    float v = pc[0];
+    uint32_t k = 1;
+    for (; k + 8 <= ns; k += 8) {
+      float q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = pc[int64_t(k + j) * dim];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v = __fadd_rn(v, q[j]);
+    }
+    for (; k < ns; ++k) v = __fadd_rn(v, pc[int64_t(k) * dim]);
     if constexpr (COALESCE) {
       const uint32_t u = fa.uid[run.x];
       fa.values_out[int64_t(u) * dim + c] = v;
