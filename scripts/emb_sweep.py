@@ -23,6 +23,9 @@ ap.add_argument("--d", type=int, nargs="*")
 ap.add_argument("--pool", type=int, nargs="*")
 ap.add_argument("--fwd-only", action="store_true")
 ap.add_argument("--nnz", type=int, default=1 << 20, help="lookups per point")
+ap.add_argument("--cpu", action="store_true",
+                help="instead: the reference algorithm (oracle/port.py, float64 numpy) on the "
+                     "host, 10^6-row tables, a 32k-lookup sample per point (SURVEY §8(d))")
 a = ap.parse_args()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] \
     if os.path.exists("MEASURED_PEAKS.json") else 6553.6
@@ -32,6 +35,39 @@ pool_list = [1, 8, 32, 128]
 rows_list = a.rows or rows_list
 d_list = a.d or d_list
 pool_list = a.pool or pool_list
+if a.cpu:
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import port
+    rng = np.random.default_rng(0)
+    m = 10 ** 6
+    for d in d_list:
+        W = rng.standard_normal((m, d))
+        for pool in pool_list:
+            for dist in ("uniform", "zipf"):
+                nnz = 1 << 15
+                B = max(1, nnz // pool)
+                nnz = B * pool
+                idx = (rng.integers(0, m, nnz) if dist == "uniform"
+                       else zipf_indices(m, nnz, 1.05, seed=d + pool))
+                offs = np.arange(0, nnz + 1, pool, dtype=np.int64)
+                g = rng.standard_normal((B, d))
+                t0 = time.perf_counter()
+                port.lookup(W, offs, idx)
+                t1 = time.perf_counter()
+                rows, vals = port.lookup_backward(W, offs, idx, g)
+                W[rows] -= 0.0 * vals
+                t2 = time.perf_counter()
+                u = int(np.unique(idx).size)
+                bf = nnz * (4 * d + 8) + (B + 1) * 8 + B * 4 * d
+                bb = B * 4 * d + nnz * 8 + (B + 1) * 8 + 2 * u * 4 * d
+                print(json.dumps(dict(impl="cpu-port (oracle/port.py, float64 numpy)",
+                                      threads=os.cpu_count(), rows=m, d=d, pooling=pool,
+                                      dist=dist, bags=B, nnz=nnz,
+                                      fwd_GBs=round(bf / (t1 - t0) / 1e9, 3),
+                                      bwd_sgd_GBs=round(bb / (t2 - t1) / 1e9, 3))), flush=True)
+    sys.exit(0)
+
 dev = torch.device("cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 s = _lib.stream_handle()
@@ -46,6 +82,7 @@ def timeit(fn, reps):
         e0.record(); fn(); e1.record(); torch.cuda.synchronize()
         tot += e0.elapsed_time(e1)
     return tot / reps
+
 
 for rows in rows_list:
     for d in d_list:
