@@ -176,3 +176,47 @@ def test_reference_model_round_trip():
     assert back.tables[0].weights.dtype == np.float64
     assert np.array_equal(back.top.layers[0].weight,
                           ref.top.layers[0].weight.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("M,K,mask", [(2048, 1024, 1), (1000, 256, 1), (37, 12, 0)])
+def test_fused_head_step(M, K, mask):
+    """dlrm_head_step (forward of the N=1 layer + BCE + backward + update in
+    two launches) vs float64 numpy of ref model.py:152, 448-461 and
+    mlp_backward_trace 173-179."""
+    import ctypes as C
+    from paper_1906_00091_b200 import _lib
+    rng = np.random.default_rng(M + K)
+    A = np.maximum(rng.standard_normal((M, K)), 0).astype(np.float32)
+    w = (rng.standard_normal(K) * 0.05).astype(np.float32)
+    b = np.float32(0.1)
+    y = (rng.random(M) < 0.5).astype(np.float32)
+    d = torch.device("cuda")
+    tA, tw = torch.as_tensor(A, device=d), torch.as_tensor(w, device=d).clone()
+    tb = torch.tensor([b], device=d)
+    ty = torch.as_tensor(y, device=d)
+    prob, gz = torch.empty(M, device=d), torch.empty(M, device=d)
+    stats = torch.zeros(2, device=d)
+    dA = torch.empty((M, K), device=d)
+    dw, db = torch.empty(K, device=d), torch.empty(1, device=d)
+    wu, bu = tw.clone(), tb.clone()
+    ws_b = _lib.size("dlrm_head_step_workspace_size", M, K)
+    ws = torch.empty(ws_b, dtype=torch.uint8, device=d)
+    upd = _lib.Update(_lib.UPD_SGD, 0.5, 0.0, 0)
+    P = _lib.ptr
+    _lib.call("dlrm_head_step", P(tA), K, P(tw), P(tb), M, K, P(ty), float(M), P(prob),
+              P(gz), P(stats), P(dA), K, mask, P(dw), P(db), P(wu), P(bu), C.byref(upd),
+              None, P(ws), ws_b, _lib.stream_handle())
+    z = A.astype(np.float64) @ w.astype(np.float64) + float(b)
+    p = 1 / (1 + np.exp(-z))
+    per = np.maximum(z, 0) - z * y + np.log1p(np.exp(-np.abs(z)))
+    g = (p - y) / M
+    eA = np.outer(g, w) * ((A > 0) if mask else 1)
+    edw = g @ A.astype(np.float64)
+    assert rel_err(prob.cpu().numpy(), p) < 1e-5
+    assert rel_err(gz.cpu().numpy(), g) < 1e-5
+    assert abs(float(stats[0]) - per.sum()) <= 1e-5 * abs(per.sum())
+    assert float(stats[1]) == float(np.sum((p > 0.5) == (y > 0.5)))
+    assert rel_err(dA.cpu().numpy(), eA) < 1e-5
+    assert rel_err(dw.cpu().numpy(), edw) < 1e-5
+    assert abs(float(db) - g.sum()) <= 1e-5 * max(abs(g).sum(), 1e-30)
+    assert rel_err(wu.cpu().numpy(), w - 0.5 * dw.cpu().numpy()) < 1e-6
