@@ -68,12 +68,21 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
       out[(b0 + s) * ld_out + (col < dim ? col : width + (col - int(dim)))] =
           col < dim ? z[size_t(s) * nf * pitch + col] : 0.f;
     }
-    // pair dots in 4x4 feature blocks (bi <= bj): 8 float4 smem loads feed
-    // 64 FMAs, so the staged rows are re-read nf/4 instead of nf times
+    // pair dots in 4x4 feature blocks (bi <= bj), each block split over 4
+    // consecutive lanes by column residue j = c % 4: lane j keeps the j-th of
+    // the four interleaved partial sums of all 16 pairs, and the lanes combine
+    // them as (p0 + p1) + (p2 + p3) — the same rounding as one thread with
+    // four partials, with 4x the parallelism.  Staged rows are re-read nf/4
+    // instead of nf times.
     const int nbk = (nf + 3) / 4, ntile = nbk * (nbk + 1) / 2;
-    for (int e = threadIdx.x; e < ns * ntile; e += blockDim.x) {
-      const int s = e / ntile;
-      int t = e - s * ntile, bi = 0;
+    const int total = ns * ntile * 4;
+    const int lane = threadIdx.x & 31;
+    for (int base = threadIdx.x & ~31; base < total; base += blockDim.x) {
+      const int e = base + lane;
+      const bool active = e < total;
+      const int item = active ? e >> 2 : 0, j = e & 3;
+      const int s = item / ntile;
+      int t = item - s * ntile, bi = 0;
       while (t >= nbk - bi) { t -= nbk - bi; ++bi; }
       const int bj = bi + t;
       const float* zs = z + size_t(s) * nf * pitch;
@@ -81,42 +90,39 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
       const float* rj[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        ri[k] = zs + min(4 * bi + k, nf - 1) * pitch;
-        rj[k] = zs + min(4 * bj + k, nf - 1) * pitch;
+        ri[k] = zs + min(4 * bi + k, nf - 1) * pitch + j;
+        rj[k] = zs + min(4 * bj + k, nf - 1) * pitch + j;
       }
-      // four interleaved partial sums per pair (columns c % 4), combined as
-      // (p0 + p1) + (p2 + p3): the same rounding as the per-pair kernel
-      float4 acc[4][4];
+      float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c = 0; c < dim; c += 4) {
-        float4 x[4], y[4];
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      if (active) {
+        for (int c = 0; c < dim; c += 4) {
+          float x[4], y[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          x[k] = *reinterpret_cast<const float4*>(ri[k] + c);
-          y[k] = *reinterpret_cast<const float4*>(rj[k] + c);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            acc[a][b].x = fmaf(x[a].x, y[b].x, acc[a][b].x);
-            acc[a][b].y = fmaf(x[a].y, y[b].y, acc[a][b].y);
-            acc[a][b].z = fmaf(x[a].z, y[b].z, acc[a][b].z);
-            acc[a][b].w = fmaf(x[a].w, y[b].w, acc[a][b].w);
+          for (int k = 0; k < 4; ++k) {
+            x[k] = ri[k][c];
+            y[k] = rj[k][c];
           }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(x[a], y[b], acc[a][b]);
+        }
       }
       float* orow = out + (b0 + s) * ld_out + dim;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          const int i = 4 * bi + a, j = 4 * bj + b;
-          if (i < j && j < nf)
-            orow[i * (2 * nf - i - 1) / 2 + (j - i - 1)] =
-                (acc[a][b].x + acc[a][b].y) + (acc[a][b].z + acc[a][b].w);
+          float v = acc[a][b];
+          v = v + __shfl_xor_sync(0xffffffffu, v, 1);  // lanes j, j^1: p0 + p1 / p2 + p3
+          v = v + __shfl_xor_sync(0xffffffffu, v, 2);  // (p0 + p1) + (p2 + p3)
+          const int i = 4 * bi + a, jj = 4 * bj + b;
+          if (active && j == 0 && i < jj && jj < nf)
+            orow[i * (2 * nf - i - 1) / 2 + (jj - i - 1)] = v;
         }
     }
     return;
