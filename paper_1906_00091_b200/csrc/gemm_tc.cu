@@ -6,7 +6,12 @@
 // x - hi (exact in fp32).  The tensor core itself ignores the low 13 mantissa
 // bits of a kind::tf32 operand, so the TMA-landed fp32 tile IS the hi operand
 // and only lo is materialised (by the splitter warps),
-// then D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.  Single
+// then D = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.  The A
+// operands (the 128-row side) are held in TMEM, not shared memory: the
+// splitter warps read each landed A tile once and tcgen05.st its hi / lo
+// halves into a TMEM slot, so neither A_lo stores nor the MMAs' A reads touch
+// the shared-memory port, which bounds this kernel (TMA fill + splitter +
+// MMA operand reads).  Single
 // TF32 fails the reference tolerance on updated weights (SURVEY Appendix A:
 // 6e-2); 3xTF32 matches fp32 (1.6e-7 loss, 9e-7 weights).
 //
@@ -18,14 +23,14 @@
 //   data grad    dX = gZ W       A = gZ (K-major)   B = W (MN-major)
 //   weight grad  dW = gZ^T X     A = gZ (MN-major)  B = X (MN-major)
 //
-// CTA = 6 warps, one 128 x BN output tile; a 4-stage TMA ring of raw tiles
-// and a 2-slot ring of lo tiles:
+// CTA = 10 warps, one 128 x BN output tile; a 4-stage TMA ring of raw tiles
+// and a ring of TMEM A slots [A_hi | A_lo] (32 + 32 columns):
 //   warp 0     TMA producer (one thread)
 //   warp 1     TMEM allocator + MMA issuer (one thread)
-//   warps 2-5  lo splitter for each landed stage, then the epilogue
-//              (tcgen05.ld 32x32b -> bias/ReLU/mask -> global)
+//   warps 2-9  splitter for each landed stage (A -> TMEM slot, B_lo -> smem),
+//              then the epilogue (tcgen05.ld 32x32b -> bias/ReLU/mask -> global)
 // Barriers: full[t] (TMA tx), empty_t[t] / empty_l[l] (tcgen05.commit),
-// conv[l] (4 splitter warps), acc_full (commit after the last k-block).
+// conv[l] (8 splitter warps), acc_full (commit after the last k-block).
 #include <cuda.h>
 #include <stdlib.h>
 
@@ -37,18 +42,14 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 per 128-byte swizzle row
-// Ring depths within 227 KB of shared memory: TSTAGES stages of
-// [A_hi | B_hi | B_lo] (TMA covers the L2 latency of a tile load) and
-// LSTAGES A_lo slots.
+// TSTAGES shared-memory stages of [A raw | B_hi | B_lo] (TMA covers the L2
+// latency of a tile load).
 constexpr int TSTAGES = 4;
-constexpr int LSTAGES = 2;
-#ifndef DLRM_TC_SPLIT_WARPS
-#define DLRM_TC_SPLIT_WARPS 8
-#endif
-// splitter warps; the first 8 of them are also the epilogue (2 per TMEM lane
-// quarter)
-constexpr int SPLIT_WARPS = DLRM_TC_SPLIT_WARPS;
+// splitter warps = epilogue warps: 2 per TMEM lane quarter
+constexpr int SPLIT_WARPS = 8;
 constexpr int EPI_WARPS = 8;
+// bias row sums: k-row partials per tile row in the bias scratch
+constexpr int kBiasRows = 8;
 constexpr int THREADS = 64 + 32 * SPLIT_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -119,15 +120,26 @@ __host__ __device__ constexpr uint32_t instr_desc(int n, bool a_mn, bool b_mn, i
          (uint32_t(b_mn) << 16) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
+// A operand from TMEM (K-major: lane = row, 8 columns per k-step of 8)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
       : "memory");
 }
 
@@ -192,13 +204,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
 // operand accumulated by the splitter warps).  No partial sums in global
 // memory, no reduction kernel, no counters.
 constexpr uint32_t kBiasScratch = 32 * 20 * 4 * 8;  // bias sums after the transpose tiles
-
-// First of the 4 consecutive tile rows (m) held by 16-byte column c16 of k-row
-// kr in A chunk r of an MN-major SWIZZLE_128B_ATOM_32B tile: 32-byte atoms are
-// XOR-permuted with (k-row % 4) inside each 128-byte row.
-__device__ __forceinline__ int bias_row0(int r, int kr, int c16) {
-  return 32 * r + 8 * ((c16 >> 1) ^ (kr & 3)) + 4 * (c16 & 1);
-}
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n"
@@ -278,7 +283,7 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
       if (row >= args.M) continue;
       float acc = 0.f;  // ranks in order, k-rows in order
       for (int k = 0; k < S; ++k)
-        for (int kr = 0; kr < 32; ++kr)
+        for (int kr = 0; kr < kBiasRows; ++kr)
           acc += ld_dsmem1(bb0 + uint32_t(k) * bstride + uint32_t(kr * BM + r) * 4);
       if (wf.db) wf.db[row] = acc;
       if (bupd) wf.bu[row] = upd_apply(wf.upd, wf.bu + row, wf.bu[row], acc);
@@ -288,15 +293,18 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
 }
 
 // One CTA computes a BM x BN tile of the fp32-accurate product with 3xTF32
-// tcgen05 MMAs.  Shared memory per k-step: a TMA stage [A_hi | B_hi | B_lo]
-// (the raw fp32 tiles are the hi operands; the splitter writes B_lo right
-// behind B_hi) and an A_lo slot.  With B_lo adjacent to B_hi, the two
-// products that share A_hi are ONE MMA of N = 2*BN (A_hi x [B_hi | B_lo]),
-// which reads A_hi from shared memory once instead of twice; the third
-// product A_lo x B_hi is an N = BN MMA.  Accumulators in TMEM:
-// [big0 | sm0 | big1 | sm1] (BN columns each): k-block it goes to pair
-// it % 2, so each truncating TMEM accumulation chain is half as long
-// (tensor-core fp32 accumulation truncates; the error grows with the chain).
+// tcgen05 MMAs.  Per k-step: a TMA stage [A raw | B_hi | B_lo] in shared
+// memory (the raw fp32 B tile is the hi operand; the splitter writes B_lo
+// right behind it) and a TMEM slot [A_hi | A_lo] written by the splitter
+// (A operands from TMEM must be K-major there: lane = tile row, column = k,
+// whatever the global layout — the splitter's per-row loads transpose
+// MN-major tiles for free).  With B_lo adjacent to B_hi, the two products
+// that share A_hi are ONE MMA of N = 2*BN (A_hi x [B_hi | B_lo]); the third,
+// A_lo x B_hi, is an N = BN MMA.  Accumulators in TMEM: [big | small] pairs
+// of BN columns; for BN <= 64 two pairs, k-block it going to pair it % 2, so
+// each truncating TMEM accumulation chain is half as long (tensor-core fp32
+// accumulation truncates; the error grows with the chain).  TMEM columns:
+// accumulators, then ASLOTS x 64 A slots.
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -306,17 +314,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   constexpr uint32_t B_BYTES = BN * BK * 4;
   constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;
   constexpr uint32_t TMA_BYTES = A_BYTES + B_BYTES;
-  constexpr int NACC = 2;
-  constexpr uint32_t COLS_NEEDED = 2 * NACC * BN;
-  constexpr uint32_t TMEM_COLS = COLS_NEEDED <= 32 ? 32 : COLS_NEEDED <= 64 ? 64
-                               : COLS_NEEDED <= 128 ? 128 : COLS_NEEDED <= 256 ? 256 : 512;
-  static_assert(COLS_NEEDED <= 512, "TMEM overflow");
-  constexpr uint32_t IDESC = instr_desc(BN, A_MN, B_MN);
-  constexpr uint32_t IDESC2 = instr_desc(FUSE ? 2 * BN : BN, A_MN, B_MN);
+  constexpr int NACC = BN >= 128 ? 1 : 2;
+  constexpr uint32_t ACC_COLS = 2 * NACC * BN;
+  // BN >= 64: > 113 KB of shared memory, one CTA per SM, all 512 columns;
+  // narrower tiles may share an SM and take 256
+  constexpr int ASLOTS = BN >= 64 ? 4 : 2;
+  constexpr uint32_t TMEM_COLS = BN >= 64 ? 512 : 256;
+  static_assert(ACC_COLS + 64 * ASLOTS <= TMEM_COLS, "TMEM overflow");
+  constexpr uint32_t IDESC = instr_desc(BN, false, B_MN);
+  constexpr uint32_t IDESC2 = instr_desc(FUSE ? 2 * BN : BN, false, B_MN);
   // epilogue scratch (transpose tiles, bias row sums) behind the dW partial
   // tile, inside the (by then idle) stage ring
   constexpr uint32_t PTILE_BYTES = (BM * (BN + 4) * 4 + 1023) / 1024 * 1024;
-  static_assert(PTILE_BYTES + kBiasScratch + 32 * BM * 4 <= TSTAGES * STAGE_BYTES,
+  static_assert(PTILE_BYTES + kBiasScratch + kBiasRows * BM * 4 <= TSTAGES * STAGE_BYTES,
                 "epilogue scratch exceeds the stage ring");
 
   extern __shared__ uint8_t smem_raw[];
@@ -325,13 +335,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   // shared window, so the splitter / epilogue accesses compile to LDS / STS
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;                                // TSTAGES x STAGE_BYTES
-  uint8_t* alo_ring = smem + TSTAGES * STAGE_BYTES;    // LSTAGES x A_BYTES
-  uint64_t* bars = reinterpret_cast<uint64_t*>(alo_ring + LSTAGES * A_BYTES);
-  uint64_t* full = bars;                               // TMA landed      [T]
-  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, stage [T]
-  uint64_t* conv = bars + 2 * TSTAGES;                 // lo ready        [L]
-  uint64_t* empty_l = bars + 2 * TSTAGES + LSTAGES;    // MMA done, A_lo  [L]
-  uint64_t* acc_full = bars + 2 * TSTAGES + 2 * LSTAGES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TSTAGES * STAGE_BYTES);
+  uint64_t* full = bars;                               // TMA landed        [T]
+  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, stage   [T]
+  uint64_t* conv = bars + 2 * TSTAGES;                 // A slot + B_lo set [L]
+  uint64_t* empty_l = bars + 2 * TSTAGES + ASLOTS;     // MMA done, A slot  [L]
+  uint64_t* acc_full = bars + 2 * TSTAGES + 2 * ASLOTS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   uint8_t* epi = ring + PTILE_BYTES;                   // epilogue scratch
 
@@ -347,7 +356,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&full[s], 1);
       mbar_init(&empty_t[s], 1);
     }
-    for (int s = 0; s < LSTAGES; ++s) {
+    for (int s = 0; s < ASLOTS; ++s) {
       mbar_init(&conv[s], SPLIT_WARPS);
       mbar_init(&empty_l[s], 1);
     }
@@ -406,35 +415,32 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // ---- MMA issuer
     if (lane == 0) {
       for (int it = 0; it < nk; ++it) {
-        const int t = it % TSTAGES, l = it % LSTAGES;
-        mbar_wait(&conv[l], (it / LSTAGES) & 1);
+        const int t = it % TSTAGES, l = it % ASLOTS;
+        mbar_wait(&conv[l], (it / ASLOTS) & 1);
         tc_fence_after();
-        const uint32_t a_hi = smem_u32(ring + t * STAGE_BYTES);
-        const uint32_t b_hi = a_hi + A_BYTES;
+        const uint32_t b_hi = smem_u32(ring + t * STAGE_BYTES) + A_BYTES;
         const uint32_t b_lo = b_hi + B_BYTES;
-        const uint32_t a_lo = smem_u32(alo_ring + l * A_BYTES);
+        const uint32_t a_hi = tmem + ACC_COLS + uint32_t(64 * l);  // TMEM slot
+        const uint32_t a_lo = a_hi + 32;
         const uint32_t big = tmem + uint32_t((it % NACC) * 2 * BN);
         const uint32_t small = big + uint32_t(BN);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          // K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows
-          const uint32_t ao = A_MN ? kk * 1024 : kk * 32;
+          // B K-major: advance 32 B inside the swizzle row; MN-major: 8 k-rows.
+          // A: 8 TMEM columns per k-step.
           const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
-          const uint32_t a_lbo = A_MN ? 32 * BK * 4 : 16, a_sbo = A_MN ? 512 : 1024;
           const uint32_t b_lbo = B_MN ? 32 * BK * 4 : 16, b_sbo = B_MN ? 512 : 1024;
-          const uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
-          const uint64_t dah = smem_desc(a_hi + ao, a_lbo, a_sbo, a_lay);
-          const uint64_t dal = smem_desc(a_lo + ao, a_lbo, a_sbo, a_lay);
+          const uint32_t b_lay = B_MN ? 1 : 2;
           const uint64_t dbh = smem_desc(b_hi + bo, b_lbo, b_sbo, b_lay);
           const uint32_t first = (it >= NACC || kk > 0) ? 1u : 0u;
           if (FUSE) {
-            mma_tf32(big, dah, dbh, IDESC2, first);      // [big | small] = A_hi x [B_hi | B_lo]
+            mma_tf32_ts(big, a_hi + 8 * kk, dbh, IDESC2, first);  // [big | small] = A_hi x [B_hi | B_lo]
           } else {
             const uint64_t dbl = smem_desc(b_lo + bo, b_lbo, b_sbo, b_lay);
-            mma_tf32(big, dah, dbh, IDESC, first);
-            mma_tf32(small, dah, dbl, IDESC, first);
+            mma_tf32_ts(big, a_hi + 8 * kk, dbh, IDESC, first);
+            mma_tf32_ts(small, a_hi + 8 * kk, dbl, IDESC, first);
           }
-          mma_tf32(small, dal, dbh, IDESC, 1u);          // small += A_lo x B_hi
+          mma_tf32_ts(small, a_lo + 8 * kk, dbh, IDESC, 1u);      // small += A_lo x B_hi
         }
         mma_commit(&empty_t[t]);
         mma_commit(&empty_l[l]);
@@ -442,48 +448,73 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mma_commit(acc_full);
     }
   } else {
-    // ---- splitter warps (2..9): lo = x - trunc_tf32(x) of the landed tiles:
-    // A_lo into the A_lo slot, B_lo into the stage right behind B_hi.
-    // Fused weight gradient, n-tile 0: the same pass accumulates the row sums
-    // of the (MN-major) A tile = the bias gradient.  Thread ct always sees
-    // A float4 ct + 256 r (r < 4) of a tile: chunk r (32 rows), k-row ct/8,
-    // 16-byte column ct%8 of the 128-byte row (swizzled, see bias_row0).
+    // ---- splitter warps (2..9), per landed stage:
+    //  A: warp (quarter q = warp % 4, half h) owns TMEM lanes / tile rows
+    //     [32q, 32q+32) and k columns [16h, 16h+16): each thread loads its
+    //     row's 16 values, tcgen05.st's hi = trunc_tf32(x) and lo = x - hi
+    //     into the A slot.  Fused weight gradient, n-tile 0: the same loads
+    //     accumulate the row sums of A (the bias gradient), 4 partials by k % 4.
+    //  B: lo = x - trunc_tf32(x) written right behind B_hi in the stage.
     const int ct = threadIdx.x - 64;  // 0 .. 32*SPLIT_WARPS-1
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int arow = 32 * q + lane;
     const bool do_bias = A_MN && args.wf.on && args.wf.bias && blockIdx.x == 0;
-    constexpr int RAW_F4 = int(TMA_BYTES / 16), A_F4 = int(A_BYTES / 16);
+    float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int B_F4 = int(B_BYTES / 16);
     constexpr int NSPLIT = 32 * SPLIT_WARPS;
-    constexpr int NB = (A_F4 + NSPLIT - 1) / NSPLIT;  // A float4s per thread per tile
-    float4 bsum[NB];
-#pragma unroll
-    for (int r = 0; r < NB; ++r) bsum[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    constexpr int NJ = (RAW_F4 + NSPLIT - 1) / NSPLIT;
+    constexpr int NJ = (B_F4 + NSPLIT - 1) / NSPLIT;
+    const uint32_t a_taddr = tmem + (uint32_t(32 * q) << 16) + ACC_COLS + uint32_t(16 * h);
     for (int it = 0; it < nk; ++it) {
-      const int t = it % TSTAGES, l = it % LSTAGES;
+      const int t = it % TSTAGES, l = it % ASLOTS;
       mbar_wait(&full[t], (it / TSTAGES) & 1);
-      if (it >= LSTAGES) mbar_wait(&empty_l[l], ((it / LSTAGES) - 1) & 1);
-      const float4* src = reinterpret_cast<const float4*>(ring + t * STAGE_BYTES);
-      float4* dst_a = reinterpret_cast<float4*>(alo_ring + l * A_BYTES);
-      float4* dst_b = reinterpret_cast<float4*>(ring + t * STAGE_BYTES + A_BYTES + B_BYTES) - A_F4;
+      if (it >= ASLOTS) mbar_wait(&empty_l[l], ((it / ASLOTS) - 1) & 1);
+      tc_fence_after();
+      const uint8_t* st = ring + t * STAGE_BYTES;
+      float x[16];
+      if (A_MN) {  // [chunk q][k-row][32 rows, 32-byte atoms XOR k-row % 4]
+        const float* src = reinterpret_cast<const float*>(st + q * 32 * BK * 4);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int kr = 16 * h + i;
+          x[i] = src[kr * 32 + 8 * ((lane >> 3) ^ (kr & 3)) + (lane & 7)];
+        }
+      } else {  // row arow: 128 bytes, 16-byte chunk c at c ^ (row % 8)
+        const float4* src = reinterpret_cast<const float4*>(st + arow * 128);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = src[(4 * h + c) ^ (arow & 7)];
+          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        }
+      }
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        hi[i] = __float_as_uint(x[i]) & 0xFFFFE000u;
+        lo[i] = __float_as_uint(x[i] - __uint_as_float(hi[i]));
+      }
+      if (do_bias) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) bsum[i & 3] += x[i];
+      }
+      const uint32_t slot = a_taddr + uint32_t(64 * l);
+      tmem_st16(slot, hi);
+      tmem_st16(slot + 32, lo);
+      const float4* src_b = reinterpret_cast<const float4*>(st + A_BYTES);
+      float4* dst_b = reinterpret_cast<float4*>(const_cast<uint8_t*>(st) + A_BYTES + B_BYTES);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int i = ct + NSPLIT * j;
-        if (RAW_F4 % NSPLIT == 0 || i < RAW_F4) {
-          const float4 x = src[i];
-          const float4 lo = make_float4(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u),
-                                        x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u),
-                                        x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u),
-                                        x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
-          if (i < A_F4) {
-            dst_a[i] = lo;
-            if (j < NB && do_bias) {
-              bsum[j].x += x.x; bsum[j].y += x.y; bsum[j].z += x.z; bsum[j].w += x.w;
-            }
-          } else {
-            dst_b[i] = lo;
-          }
+        if (B_F4 % NSPLIT == 0 || i < B_F4) {
+          const float4 v = src_b[i];
+          dst_b[i] = make_float4(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                                 v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u),
+                                 v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u),
+                                 v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_async_smem();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[l]);
     }
@@ -494,7 +525,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // 64-byte row segment, 8 rows per instruction).
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const int q = warp & 3;
     const int half = warp - 2 < EPI_WARPS ? (warp - 2) / 4 : 2;  // extra splitter warps: none
     float* tile = reinterpret_cast<float*>(epi) + (warp - 2) * (32 * 20);
     const GemmEpilogue& ep = args.ep;
@@ -510,10 +540,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(ra[0][i]) + __uint_as_float(ra[1][i]);
-      if (used > 1) {
+      if constexpr (NACC > 1) {
+        if (used > 1) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          v[i] += __uint_as_float(ra[2][i]) + __uint_as_float(ra[3][i]);
+          for (int i = 0; i < 16; ++i)
+            v[i] += __uint_as_float(ra[2][i]) + __uint_as_float(ra[3][i]);
+        }
       }
       if (args.wf.on) {  // fused weight gradient: the partial tile stays in smem
         float* prow = reinterpret_cast<float*>(ring) + (32 * q + lane) * (BN + 4) + c0;
@@ -536,16 +568,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       __syncwarp();
     }
-    if (do_bias) {  // per-thread row sums -> [k-row][m] scratch in unswizzled order
+    if (do_bias) {  // per-thread row-sum partials -> [k-row partial][m] scratch
       float* bs = reinterpret_cast<float*>(epi + kBiasScratch);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) {
-        const int i = ct + NSPLIT * j;  // A float4: chunk i/256, k-row (i/8)%32, column i%8
-        if (i < A_F4) {
-          const int kr = (i >> 3) & 31;
-          *reinterpret_cast<float4*>(bs + kr * BM + bias_row0(i >> 8, kr, i & 7)) = bsum[j];
-        }
-      }
+      for (int j = 0; j < 4; ++j) bs[(4 * h + j) * BM + arow] = bsum[j];
     }
   }
   if (args.wf.on) wgrad_cluster_reduce<BN>(args, ring, epi + kBiasScratch, m0, n0);
@@ -604,8 +630,7 @@ bool encode(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 constexpr size_t smem_bytes(int bn) {
-  return size_t(TSTAGES) * (BM * BK * 4 + 2 * bn * BK * 4) + size_t(LSTAGES) * BM * BK * 4 +
-         1024 + 256;
+  return size_t(TSTAGES) * (BM * BK * 4 + 2 * bn * BK * 4) + 1024 + 256;
 }
 
 template <bool A_MN, bool B_MN, int BN>
