@@ -204,6 +204,14 @@ class StepEngine:
         # DLRM_EMB_APPLY_SIDE=0 keeps the apply on the main stream
         self.apply_side = os.environ.get("DLRM_EMB_APPLY_SIDE", "1") != "0"
         self.side = torch.cuda.Stream(device=dev)
+        # more concurrency inside the step (graph branches once captured):
+        # the pooled lookups (HBM-bound) beside the bottom MLP forward
+        # (tensor / shared-memory bound), and each weight gradient + fused
+        # update beside the next layer's data gradient
+        self.emb_side = os.environ.get("DLRM_EMB_FWD_SIDE", "1") != "0"
+        self.wgrad_side = os.environ.get("DLRM_WGRAD_SIDE", "1") != "0"
+        self.fwd_stream = torch.cuda.Stream(device=dev)
+        self.wg_stream = torch.cuda.Stream(device=dev)
 
         for v in self.input_sets:
             v["descs"] = self._make_descs(v)
@@ -345,6 +353,17 @@ class StepEngine:
             done.record(self.side)
             return done
 
+        def fork(stream):
+            ev = torch.cuda.Event()
+            ev.record(main)
+            stream.wait_event(ev)
+            return _lib.stream_handle(stream)
+
+        def join(stream):
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            main.wait_event(ev)
+
         L, call, P = self.layers, _lib.call, _lib.ptr
         B, d, nf, lr = self.B, self.d, self.nf, self.lr
         relu = _lib.ACT["relu"]
@@ -352,6 +371,25 @@ class StepEngine:
         call("dlrm_err_reset", P(self.err_pos), self.T, ef, s)
         if self.prep_at == "start":
             prep_done = fork_prepare()
+        emb_side = self.emb_side and not profiling
+        wg = fork(self.wg_stream) if self.wgrad_side and not profiling else None
+
+        def emb_fwd(stream_handle):
+            call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
+                 P(self.Z), nf * d, P(self.err_pos), ef, stream_handle)
+
+        def wgrad(*args):
+            # after the data gradient that reads the same (pre-update) weights
+            if wg is None:
+                call("dlrm_linear_bwd_weight_upd", *args, s)
+                return
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self.wg_stream.wait_event(ev)
+            call("dlrm_linear_bwd_weight_upd", *args, wg)
+
+        if emb_side:
+            emb_fwd(fork(self.fwd_stream))
 
         # bottom MLP forward; the last layer writes feature 0 of Z
         mark("bottom_mlp_fwd")
@@ -366,8 +404,10 @@ class StepEngine:
             a, lda = out, ldo
         # pooled lookups -> features 1..T of Z
         mark("embedding_fwd")
-        call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
-             P(self.Z), nf * d, P(self.err_pos), ef, s)
+        if emb_side:
+            join(self.fwd_stream)
+        else:
+            emb_fwd(s)
         if self.prep_at == "after_fwd":
             prep_done = fork_prepare()
         # interaction -> R
@@ -415,9 +455,8 @@ class StepEngine:
             call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
                  l.ldw, P(mask), mask.stride(0) if mask is not None else 0,
                  P(dx), dx.stride(0), B, l.n_out, l.n_in, s)
-            call("dlrm_linear_bwd_weight_upd", P(gz), gz.stride(0), P(xin),
-                 xin.stride(0), B, l.n_out, l.n_in, None, 0, None,
-                 P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb, s)
+            wgrad(P(gz), gz.stride(0), P(xin), xin.stride(0), B, l.n_out, l.n_in,
+                  None, 0, None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
         # interaction backward (bottom's last ReLU folded in for feature 0)
         mark("interaction_bwd")
         call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
@@ -451,11 +490,12 @@ class StepEngine:
                 call("dlrm_linear_bwd_data", P(gz), ldg, P(l.storage), l.ldw,
                      P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), B, l.n_out, l.n_in, s)
-            call("dlrm_linear_bwd_weight_upd", P(gz), ldg, P(xin), xin.stride(0),
-                 B, l.n_out, l.n_in, None, 0, None, P(l.storage), l.ldw,
-                 P(l.bias), um, ef, ws, wsb, s)
+            wgrad(P(gz), ldg, P(xin), xin.stride(0), B, l.n_out, l.n_in, None, 0,
+                  None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
+        if wg is not None:
+            join(self.wg_stream)  # the next step reads the updated weights
         if apply_done is not None:
             main.wait_event(apply_done)  # join: the next step reads the tables
             return
