@@ -594,13 +594,31 @@ def run_hybrid(args, c, rank, world, dist):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = Bg * K / (ms / 1e3)
-    # e2e from pinned host buffers
+    # e2e from pinned host buffers: the H2D copy of batch s+1 (copy stream,
+    # into the landing buffer step s is not reading) overlaps step s; each
+    # step starts with a device copy landing -> input block, and ends with a
+    # D2H read of its result
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    copy_s = torch.cuda.Stream()
+    land = [torch.empty(h2d, dtype=torch.uint8, device=dev) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    for k in range(2):
+        free[k].record(stream)
     dist.barrier()
+    torch.cuda.synchronize()
     res_host = torch.zeros((K, 3), dtype=torch.float32).pin_memory()
     e0.record(stream)
+    copy_s.wait_event(e0)
     for s in range(K):
-        tr.stage(hpool[s % P])        # one H2D copy of the packed batch
+        k = s & 1
+        copy_s.wait_event(free[k])
+        with torch.cuda.stream(copy_s):
+            land[k].copy_(hpool[s % P], non_blocking=True)   # one H2D copy per batch
+        ready[k].record(copy_s)
+        stream.wait_event(ready[k])
+        tr.stage(land[k])
+        free[k].record(stream)
         tr.step(sync=False)
         res_host[s].copy_(tr.engine.stats, non_blocking=True)   # D2H of the step result
     e1.record(stream)

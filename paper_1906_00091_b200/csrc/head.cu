@@ -217,17 +217,34 @@ head_fused_kernel(const float* __restrict__ A, int64_t lda, const float* __restr
   }
 }
 
-// dw[k] / db / stats reduced over the CTA partials in CTA order; optional
+// dw[k] / db / stats reduced over the CTA partials in a fixed order; optional
 // outputs and the fused update (skipped when *err_flag).
 __global__ void __launch_bounds__(256)
 head_final_kernel(const float* __restrict__ part, int64_t nparts, int64_t K, float* dw,
                   float* db, float* stats, float* w_upd, float* b_upd, Upd u,
                   const int32_t* err_flag) {
+  // 32 columns per block; warp w sums partials w, w + 8, ... (two independent
+  // chains so loads stay in flight), then warp 0 adds the 8 warp sums in order
   pdl_entry();
-  const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // 0..K+2
-  if (c >= K + 3) return;
-  float t = part[c];
-  for (int64_t i = 1; i < nparts; ++i) t += part[i * (K + 3) + c];
+  __shared__ float s_t[8][33];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t c = int64_t(blockIdx.x) * 32 + lane;  // 0..K+2
+  const int64_t ncol = K + 3;
+  float t0 = 0.f, t1 = 0.f;
+  if (c < ncol) {
+    int64_t i = warp;
+    for (; i + 8 < nparts; i += 16) {
+      t0 += part[i * ncol + c];
+      t1 += part[(i + 8) * ncol + c];
+    }
+    if (i < nparts) t0 += part[i * ncol + c];
+  }
+  s_t[warp][lane] = t0 + t1;
+  __syncthreads();
+  if (warp != 0 || c >= ncol) return;
+  float t = s_t[0][lane];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) t += s_t[w][lane];
   const bool upd = !(err_flag && *err_flag);
   if (c < K) {
     if (dw) dw[c] = t;
@@ -277,7 +294,7 @@ extern "C" int dlrm_head_step(const float* A, int64_t lda, const float* w, const
   else if (kvl <= 4) go(head_fused_kernel<4>);
   else go(head_fused_kernel<8>);
   if (int rc = check_launch("head_fused_kernel")) return rc;
-  launch(head_final_kernel, unsigned(ceil_div(K + 3, 256)), 256, 0, s, part, nb, K, dw, db, stats,
+  launch(head_final_kernel, unsigned(ceil_div(K + 3, 32)), 256, 0, s, part, nb, K, dw, db, stats,
          w_upd, b_upd, upd_rule(upd), err_flag);
   return check_launch("head_final_kernel");
 }

@@ -359,7 +359,9 @@ class RankEngine:
                       C.cast(self._descs, C.c_void_p), To, self.Bg, P(self.send),
                       To * self.d, P(self.err_pos), P(self.err_flag), s)
 
-    def phase_b_forward(self, stream=None):
+    def phase_b_bottom_forward(self, stream=None):
+        """Bottom MLP forward of the local samples (independent of the
+        lookups and the exchange, so the trainer runs it beside them)."""
         s = _lib.stream_handle(stream)
         P, call, L = _lib.ptr, _lib.call, self.layers
         Bl, relu = self.Bl, _lib.ACT["relu"]
@@ -369,6 +371,15 @@ class RankEngine:
             call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
                  P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
             a, lda = out, out.stride(0)
+
+    def phase_b_forward(self, stream=None, bottom=True):
+        """(Bottom MLP forward unless ``bottom=False``,) interaction, top
+        MLP forward and the loss head."""
+        s = _lib.stream_handle(stream)
+        P, call, L = _lib.ptr, _lib.call, self.layers
+        Bl, relu = self.Bl, _lib.ACT["relu"]
+        if bottom:
+            self.phase_b_bottom_forward(stream)
         call("dlrm_interact_fwd", C.c_void_p(C.addressof(self._feats)), self.nf,
              self.d, Bl, P(self.R), self.R.stride(0), self.R.shape[1], s)
         a, lda = self.R, self.R.stride(0)
@@ -396,7 +407,20 @@ class RankEngine:
                  self.lin_ws_bytes, s)
         self._head_in = (a, lda)
 
-    def phase_b_top_backward(self, stream=None):
+    def _wgrad(self, stream, wgrad_stream, *args):
+        """Weight gradient (into its allreduce slot): on ``wgrad_stream``
+        after the work issued so far on ``stream``, when given."""
+        if wgrad_stream is None:
+            _lib.call("dlrm_linear_bwd_weight", *args, _lib.stream_handle(stream))
+            return
+        ev = torch.cuda.Event()
+        ev.record(stream if stream is not None else torch.cuda.current_stream())
+        wgrad_stream.wait_event(ev)
+        _lib.call("dlrm_linear_bwd_weight", *args, _lib.stream_handle(wgrad_stream))
+
+    def phase_b_top_backward(self, stream=None, wgrad_stream=None):
+        """Top MLP backward; with ``wgrad_stream`` each weight gradient runs
+        there beside the next data gradient (the caller joins it)."""
         s = _lib.stream_handle(stream)
         P, call, L = _lib.ptr, _lib.call, self.layers
         Bl = self.Bl
@@ -419,9 +443,9 @@ class RankEngine:
                  P(mask), mask.stride(0) if mask is not None else 0, P(dx),
                  dx.stride(0), Bl, l.n_out, l.n_in, s)
             gw, gb = self.gslots[li]
-            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
-                 Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+            self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
+                        Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                        0.0, None, P(self.lin_ws), self.lin_ws_bytes)
 
     def phase_b_interaction_backward(self, stream=None):
         s = _lib.stream_handle(stream)
@@ -430,7 +454,7 @@ class RankEngine:
                   C.cast(self._gfeat, C.c_void_p), C.cast(self._gstride, C.c_void_p),
                   1, s)
 
-    def phase_b_bottom_backward(self, stream=None):
+    def phase_b_bottom_backward(self, stream=None, wgrad_stream=None):
         s = _lib.stream_handle(stream)
         P, call, L = _lib.ptr, _lib.call, self.layers
         Bl = self.Bl
@@ -444,9 +468,9 @@ class RankEngine:
                      l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), Bl, l.n_out, l.n_in, s)
             gw, gb = self.gslots[i]
-            call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
-                 Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
+            self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
+                        Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                        0.0, None, P(self.lin_ws), self.lin_ws_bytes)
 
     def publish_error(self):
         """stats[2] <- this rank's error flag (allreduced with the loss)."""
@@ -520,6 +544,8 @@ class HybridTrainer:
         self.rank = rank
         self.comm_stream = torch.cuda.Stream()
         self.side = torch.cuda.Stream()
+        self.fwd_stream = torch.cuda.Stream()  # bottom MLP forward
+        self.wg_stream = torch.cuda.Stream()   # weight gradients + their allreduces
         self.graph = None
 
     def load(self, *args):
@@ -570,19 +596,30 @@ class HybridTrainer:
         fork.record(cur)
         self.side.wait_event(fork)
         e.prepare_sparse_backward(self.side)
+        # bottom MLP forward beside the owner lookups and the exchange
+        self.fwd_stream.wait_event(fork)
+        e.phase_b_bottom_forward(self.fwd_stream)
+        bot = torch.cuda.Event()
+        bot.record(self.fwd_stream)
         e.phase_a()
         ex.forward(e.send, e.recv)
-        e.phase_b_forward()
+        cur.wait_event(bot)
+        e.phase_b_forward(bottom=False)
         # loss, correct count and this rank's index-error flag are all known
         # after the head: reduce them now, so every rank can skip its updates
         # (on device) before any update is issued
         e.publish_error()
         ex.allreduce(e.stats)
         e.adopt_global_error()
-        e.phase_b_top_backward()
+        wg = self.wg_stream
+        e.phase_b_top_backward(wgrad_stream=wg)
         # top-MLP gradients reduce on the second communicator while the
-        # interaction / bottom backward and the reverse exchange run
-        h_top = ex.allreduce_async(e.grads[e.split_at:])
+        # interaction / bottom backward and the reverse exchange run: issued
+        # from the weight-gradient stream, so only the allreduce waits for
+        # the last weight gradient
+        wg.wait_event(self._mark(cur))  # the head's / data gradients' side too
+        with torch.cuda.stream(wg):
+            h_top = ex.allreduce_async(e.grads[e.split_at:])
         e.phase_b_interaction_backward()
         ex.backward(e.gsend, e.grecv)
         # owned-table fold + row update on the side stream, concurrently
@@ -593,12 +630,20 @@ class HybridTrainer:
         e.apply_sparse(self.side)
         applied = torch.cuda.Event()
         applied.record(self.side)
-        e.phase_b_bottom_backward()
-        h_bot = ex.allreduce_async(e.grads[:e.split_at])
+        e.phase_b_bottom_backward(wgrad_stream=wg)
+        wg.wait_event(self._mark(cur))
+        with torch.cuda.stream(wg):
+            h_bot = ex.allreduce_async(e.grads[:e.split_at])
         h_top.wait()
         h_bot.wait()
         e.sgd_dense()
         cur.wait_event(applied)
+
+    @staticmethod
+    def _mark(stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
 
     def check_errors(self):
         """Raise for the last step if any rank saw an out-of-range index
