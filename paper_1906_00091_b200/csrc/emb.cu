@@ -626,8 +626,12 @@ constexpr int kLongRun = DLRM_LONG_RUN;
 template <int LPB>
 constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
 
+// Rows up to 128 floats (NV == 1): registers capped for 4 blocks (32 warps)
+// per SM — the apply is bound by the rows in flight; measured on B200 at the
+// c3 shape (8 x 1M x 64, 827K lookups): 127 us at 3 blocks/SM (80 registers),
+// 102 us at 4 (64 registers, a few bytes of spills).
 template <int VEC, int LPB, int NV, bool COALESCE>
-__global__ void __launch_bounds__(fold_groups<LPB>() * LPB)
+__global__ void __launch_bounds__(fold_groups<LPB>() * LPB, NV == 1 ? 4 : 1)
 emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   pdl_entry();
   using V = typename VecT<VEC>::T;

@@ -223,26 +223,28 @@ __global__ void __launch_bounds__(256)
 head_final_kernel(const float* __restrict__ part, int64_t nparts, int64_t K, float* dw,
                   float* db, float* stats, float* w_upd, float* b_upd, Upd u,
                   const int32_t* err_flag) {
-  // 32 columns per block; warp w sums partials w, w + 8, ... (two independent
-  // chains so loads stay in flight), then warp 0 adds the 8 warp sums in order
+  // 32 columns per block; warp w sums partials [16w, 16w + 16) + 128 j (all
+  // 16 loads of a chunk in flight before the in-order sum), then warp 0 adds
+  // the 8 warp sums in order
   pdl_entry();
   __shared__ float s_t[8][33];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t c = int64_t(blockIdx.x) * 32 + lane;  // 0..K+2
   const int64_t ncol = K + 3;
-  float t0 = 0.f, t1 = 0.f;
+  float t = 0.f;
   if (c < ncol) {
-    int64_t i = warp;
-    for (; i + 8 < nparts; i += 16) {
-      t0 += part[i * ncol + c];
-      t1 += part[(i + 8) * ncol + c];
+    for (int64_t i0 = 16 * warp; i0 < nparts; i0 += 128) {
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = i0 + j < nparts ? part[(i0 + j) * ncol + c] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) t += v[j];
     }
-    if (i < nparts) t0 += part[i * ncol + c];
   }
-  s_t[warp][lane] = t0 + t1;
+  s_t[warp][lane] = t;
   __syncthreads();
   if (warp != 0 || c >= ncol) return;
-  float t = s_t[0][lane];
+  t = s_t[0][lane];
 #pragma unroll
   for (int w = 1; w < 8; ++w) t += s_t[w][lane];
   const bool upd = !(err_flag && *err_flag);

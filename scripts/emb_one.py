@@ -22,6 +22,7 @@ ap.add_argument("--batch", type=int, default=2048)
 ap.add_argument("--zipf", action="store_true")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--bwd", action="store_true")
+ap.add_argument("--apply", action="store_true", help="also time the apply half alone")
 a = ap.parse_args()
 
 dev = torch.device("cuda")
@@ -81,4 +82,10 @@ if a.bwd:
     bb = B * T * 4 * d + nnz * 8 + T * (B + 1) * 8 + 2 * u * 4 * d
     rec.update(bwd_us=round(tb * 1e3, 2), bwd_GBs=round(bb / tb / 1e6, 1),
                bwd_frac=round(bb / tb / 1e6 / peak, 3))
+    if a.apply:
+        upd = _lib.Update(_lib.UPD_SGD, 0.01, 0.0, 0)
+        _lib.call("dlrm_emb_bwd_prepare", d, C.cast(desc, C.c_void_p), T, B, T * m, P(ws), wsb, s)
+        ta = timeit(lambda: _lib.call("dlrm_emb_bwd_apply", P(W), d, C.cast(desc, C.c_void_p), T, B,
+                                      P(grad), T * d, C.byref(upd), P(ef), T * m, P(ws), wsb, s))
+        rec.update(apply_us=round(ta * 1e3, 2), apply_GBs=round(bb / ta / 1e6, 1))
 print(json.dumps(rec), flush=True)
