@@ -174,6 +174,8 @@ struct WgradFuse {
   Upd upd;  // SGD / Adagrad rule for W and b
   const int32_t* err_flag;
   int vec;  // dW / W rows 16-byte aligned
+  int generic;  // 1: split-K forward / data gradient: the reduced tile goes
+                // through the GemmEpilogue (bias / ReLU / mask) instead
 };
 
 struct TcArgs {
@@ -246,15 +248,21 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
   const float* pt = reinterpret_cast<const float*>(ptile);
   const uint32_t base0 = dsmem_addr(pt, 0);
   const uint32_t rank_stride = S > 1 ? dsmem_addr(pt, 1) - base0 : 0;
+  // generic: zero-padded output columns [N, pad_n) are written too
+  const int64_t ncols = wf.generic && args.ep.pad_n > args.N ? args.ep.pad_n : args.N;
   for (int e = threadIdx.x; e < (r1 - r0) * C4; e += blockDim.x) {
     const int r = r0 + e / C4, c = (e % C4) * 4;
     const int64_t row = m0 + r, col = n0 + c;
-    if (row >= args.M || col >= args.N) continue;
+    if (row >= args.M || col >= ncols) continue;
     const uint32_t off = uint32_t(r * P + c) * 4;
     float4 acc = ld_dsmem4(base0 + off);
     for (int k = 1; k < S; ++k) {
       const float4 v = ld_dsmem4(base0 + uint32_t(k) * rank_stride + off);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (wf.generic) {
+      apply_epilogue4(args.ep, row, col, args.N, acc, 0);
+      continue;
     }
     const float a[4] = {acc.x, acc.y, acc.z, acc.w};
     if (wf.vec && col + 3 < args.N) {
@@ -699,43 +707,11 @@ int max_clusters(int cz) {
   return n;
 }
 
-// Tile planner: pick the N tile (and, where a workspace exists, the split-K
-// factor) minimising a simple time model fitted on B200 measurements of this
-// kernel: per CTA  F + k_iters * (C0 + C1 * BN)  cycles, waves of 148 CTAs,
-// plus the partial-sum reduction when split.
+// Tile plan: the N tile and the split-K (cluster) size.
 struct TcPlan {
   int bn;
   int splits;
 };
-
-TcPlan plan_tc(int64_t M, int64_t n_grid, int64_t kt, bool allow_split, int min_bn,
-               int64_t out_elems) {
-  constexpr double F = 9000, C0 = 600, C1 = 7.5;
-  TcPlan best{128, 1};
-  double best_t = 1e30;
-  const int64_t mt = ceil_div(M, BM);
-  for (int bn : {128, 64, 32, 16}) {
-    if (bn < min_bn) continue;
-    if (bn > 16 && n_grid <= bn / 2) continue;  // mostly empty tile
-    const int64_t tiles = mt * ceil_div(n_grid, bn);
-    int64_t smax = allow_split ? (tiles < kNumSMs ? kNumSMs / tiles : 1) : 1;
-    if (smax > kt / 4) smax = kt / 4;
-    if (smax > 16) smax = 16;
-    if (smax < 1) smax = 1;
-    for (int64_t sp = 1; sp <= smax; ++sp) {
-      const int64_t ctas = tiles * sp;
-      const double waves = double(ceil_div(ctas, kNumSMs));
-      double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn));
-      if (sp > 1) t += 2000.0 + 0.002 * double(sp + 1) * double(out_elems);
-      if (t < best_t) {
-        best_t = t;
-        best = TcPlan{bn, int(sp)};
-      }
-    }
-  }
-  return best;
-}
-
 
 template <bool A_MN, bool B_MN>
 int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
@@ -780,9 +756,62 @@ bool map_operand(CUtensorMap* m, const float* p, bool mn_major, int64_t mn, int6
   return encode(m, p, k, mn, ld, BK, rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// Split-K plan for the cluster-reduced kernels (fused weight gradient; and
+// forward / data gradient when a tile grid is too small to fill the SMs):
+// BN and the split-K cluster size from the tile time model, waves counted
+// against the number of co-resident clusters.  Returns splits = 1 when
+// splitting does not pay.
+template <bool A_MN, bool B_MN>
+TcPlan cluster_plan(int64_t m_rows, int64_t n_grid, int64_t kt, int min_bn,
+                    bool one_per_sm = false) {
+  constexpr double F = 9000, C0 = 600, C1 = 7.5;
+  const int64_t mt = ceil_div(m_rows, BM);
+  TcPlan best{128, 1};
+  double best_t = 1e30;
+  for (int bn : {128, 64, 32, 16}) {
+    if (bn < min_bn) continue;
+    if (bn > 16 && n_grid <= bn / 2) continue;  // mostly empty tile
+    const int64_t tiles = mt * ceil_div(n_grid, bn);
+    int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
+    if (smax < 1) smax = 1;
+    for (int64_t sp = 1; sp <= smax; ++sp) {
+      const int cap_occ = bn == 128 ? max_clusters<A_MN, B_MN, 128>(int(sp))
+                    : bn == 64  ? max_clusters<A_MN, B_MN, 64>(int(sp))
+                    : bn == 32  ? max_clusters<A_MN, B_MN, 32>(int(sp))
+                                : max_clusters<A_MN, B_MN, 16>(int(sp));
+      // one_per_sm: narrow tiles sharing an SM also share its tensor core
+      const int cap = one_per_sm && cap_occ > kNumSMs / int(sp) ? kNumSMs / int(sp) : cap_occ;
+      const double waves = double(ceil_div(tiles, cap));
+      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn)) +
+                       (sp > 1 ? 400.0 * double(sp) : 0.0);
+      if (t < best_t) {
+        best_t = t;
+        best = TcPlan{bn, int(sp)};
+      }
+    }
+  }
+  return best;
+}
+
+// Fused weight gradient: m = N (MN-major gZ), n = K, k = M.
+TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
+  return cluster_plan<true, true>(N, K, ceil_div(M, BK), 32);
+}
+
 }  // namespace
 
 bool tc_enabled() { return g_tc_mode == 0; }
+
+namespace {
+// split-K clusters of a forward / data-gradient GEMM: partial tiles reduced
+// over DSMEM, then the normal epilogue
+WgradFuse cluster_epilogue() {
+  WgradFuse w{};
+  w.on = 1;
+  w.generic = 1;
+  return w;
+}
+}  // namespace
 
 bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* Y,
                       int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid) {
@@ -795,7 +824,10 @@ bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw, 
 int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* b,
                   float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
                   int act, cudaStream_t s) {
-  const int bn = plan_tc(M, n_grid, ceil_div(K, BK), false, 16, 0).bn;
+  // split-K over a thread-block cluster when the tile grid alone cannot
+  // fill the SMs (bias / ReLU applied after the DSMEM reduction)
+  const TcPlan pl = cluster_plan<false, false>(M, n_grid, ceil_div(K, BK), 16, true);
+  const int bn = pl.bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, X, false, M, K, ldx, BM) &&
                    map_operand(&mb, W, false, N, K, ldw, bn),
@@ -804,8 +836,10 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
                                         aligned16(Y) && ldy % 4 == 0 && aligned16(b)},
            0, 0};
   a.k_tiles = int(ceil_div(K, BK));
-  a.k_tiles_per_split = a.k_tiles;
-  return launch<false, false>(ma, mb, a, n_grid, bn, 1, s);
+  a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
+  const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
+  if (used > 1) a.wf = cluster_epilogue();
+  return launch<false, false>(ma, mb, a, n_grid, bn, used, s);
 }
 
 bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
@@ -820,7 +854,8 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
                        const float* mask, int64_t ldm, float* dX, int64_t ldx, int64_t M,
                        int64_t N, int64_t K, cudaStream_t s) {
   // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
-  const int bn = plan_tc(M, K, ceil_div(N, BK), false, 32, 0).bn;
+  const TcPlan pl = cluster_plan<false, true>(M, K, ceil_div(N, BK), 32, true);
+  const int bn = pl.bn;
   CUtensorMap ma, mb;
   DLRM_REQUIRE(map_operand(&ma, gZ, false, M, N, ldg, BM) &&
                    map_operand(&mb, W, true, K, N, ldw, bn),
@@ -830,8 +865,10 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
                                             (!mask || (aligned16(mask) && ldm % 4 == 0))},
            0, use3d(true, K, bn)};
   a.k_tiles = int(ceil_div(N, BK));
-  a.k_tiles_per_split = a.k_tiles;
-  return launch<false, true>(ma, mb, a, K, bn, 1, s);
+  a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
+  const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
+  if (used > 1) a.wf = cluster_epilogue();
+  return launch<false, true>(ma, mb, a, K, bn, used, s);
 }
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
@@ -842,35 +879,6 @@ bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64
          ldg % 4 == 0 && ldx % 4 == 0;
 }
 
-namespace {
-// Fused weight gradient: BN and the split-K cluster size from the same time
-// model, waves counted against the number of co-resident clusters.
-TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
-  constexpr double F = 9000, C0 = 600, C1 = 7.5;
-  const int64_t kt = ceil_div(M, BK), mt = ceil_div(N, BM);
-  TcPlan best{128, 1};
-  double best_t = 1e30;
-  for (int bn : {128, 64, 32}) {
-    if (bn > 32 && K <= bn / 2) continue;
-    const int64_t tiles = mt * ceil_div(K, bn);
-    int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
-    if (smax < 1) smax = 1;
-    for (int64_t sp = 1; sp <= smax; ++sp) {
-      const int cap = bn == 128 ? max_clusters<true, true, 128>(int(sp))
-                    : bn == 64  ? max_clusters<true, true, 64>(int(sp))
-                                : max_clusters<true, true, 32>(int(sp));
-      const double waves = double(ceil_div(tiles, cap));
-      const double t = waves * (F + double(ceil_div(kt, sp)) * (C0 + C1 * bn)) +
-                       (sp > 1 ? 400.0 * double(sp) : 0.0);
-      if (t < best_t) {
-        best_t = t;
-        best = TcPlan{bn, int(sp)};
-      }
-    }
-  }
-  return best;
-}
-}  // namespace
 
 int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int64_t M,
                          int64_t N, int64_t K, float* dW, int64_t lddw, float* W_upd,
