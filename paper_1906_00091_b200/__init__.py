@@ -25,7 +25,9 @@ from .parallel import (CommLog, DevicePlan, ParallelTrainer, ShuffleSlice,
                        allreduce,
                        allreduce_max, butterfly_shuffle, format_comm_report,
                        inverse_shuffle, make_plan, partition_tables,
-                       shard_bounds, train_step)
+                       shard_bounds, train_step, evaluate)
+from .checkpoint import (CHECKPOINT_MAGIC, CheckpointError, load_checkpoint,
+                         load_optimizer_state, restore_adagrad, save_checkpoint)
 
 from .distributed import (ExchangeLayout, HybridTrainer, LocalExchange,
                           NcclExchange, RankEngine)

@@ -24,7 +24,7 @@ from .trainer import StepEngine, StepResult
 __all__ = [
     "DevicePlan", "ShuffleSlice", "CommLog", "StepResult", "partition_tables",
     "shard_bounds", "make_plan", "butterfly_shuffle", "inverse_shuffle",
-    "allreduce", "allreduce_max", "train_step", "format_comm_report",
+    "allreduce", "allreduce_max", "train_step", "evaluate", "format_comm_report",
     "ParallelTrainer",
 ]
 
@@ -222,6 +222,20 @@ def _engine_for(model: DlrmModel, batch: int, batches, optimizer,
     if acc_p is not None:
         eng.params_acc.copy_(acc_p)
         eng.W_acc.copy_(acc_w)
+    elif kind == "adagrad" and (getattr(optimizer, "_mlp_state", None)
+                                or getattr(optimizer, "_table_state", None)):
+        # accumulators restored into the optimiser (checkpoint.restore_adagrad)
+        from .checkpoint import _engine_adagrad_views
+        views = _engine_adagrad_views(eng)
+        for name in ("bottom", "top"):
+            st = optimizer._mlp_state.get(name)
+            for l, (aw, ab) in enumerate(zip(st.mlp_weights, st.mlp_biases) if st else []):
+                views[f"{name}_w_{l}"].copy_(aw)
+                views[f"{name}_b_{l}"].copy_(ab)
+        for t, table in enumerate(model.tables):
+            acc = optimizer._table_state.get(table.table_id)
+            if acc is not None:
+                views[f"table_{t}"].copy_(acc)
     eng.eager_runs = 0
     model._engine = eng
     return eng
@@ -260,6 +274,50 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
     if timer is not None and hasattr(timer, "seconds"):
         timer.seconds.setdefault("train_step", 0.0)
     return eng.result()
+
+
+class _EngineSpec:
+    """Optimizer settings of an existing step engine (so evaluation reuses
+    it instead of rebinding the model's parameters to a new one)."""
+
+    def __init__(self, name, lr, eps):
+        self.name, self.lr, self.eps = name, lr, eps
+
+
+def evaluate(model: DlrmModel, eval_batches):
+    """(mean per-sample BCE loss, accuracy) over ``(dense, sparse_batches,
+    labels)`` triples — the reference's ``_evaluate`` (cli.py:542-552).
+
+    Forward-only on the device through the model's step engine: lookups,
+    interaction, MLP forwards and the loss head fused with the sigmoid; no
+    backward, no update.  Each batch's loss sum / correct count come back as
+    two floats; the totals accumulate in float64 on the host."""
+    loss_sum, correct, total = 0.0, 0.0, 0
+    for dense, batches, labels in eval_batches:
+        cfg = model.config
+        if len(batches) != cfg.num_tables:
+            raise ValueError(
+                f"got {len(batches)} sparse batches for {cfg.num_tables} tables")
+        b = int(dense.shape[0])
+        for t, sb in enumerate(batches):
+            if sb.num_segments != b:
+                raise ValueError(
+                    f"sparse batch {t} has {sb.num_segments} segments, batch is {b}")
+        weighted = any(sb.weights is not None for sb in batches)
+        cur = getattr(model, "_engine", None)
+        spec = (_EngineSpec(cur.optimizer, cur.lr, cur.eps) if cur is not None
+                else _EngineSpec("sgd", 0.1, 1e-10))
+        eng = _engine_for(model, b, batches, spec, weighted)
+        eng.load(dense, [sb.offsets for sb in batches], [sb.indices for sb in batches],
+                 labels, [sb.weights for sb in batches] if weighted else None)
+        eng.run_eval()
+        ls, c, _ = eng.eval_result()
+        loss_sum += ls
+        correct += c
+        total += b
+    if total == 0:
+        raise ValueError("no evaluation batches")
+    return loss_sum / total, correct / total
 
 
 # --------------------------------------------------------------------------

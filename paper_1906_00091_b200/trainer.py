@@ -218,6 +218,8 @@ class StepEngine:
         self.use_set(0)
         self._build_descs()
         self.graph = None
+        self.eval_graphs = {}
+        self._eval_runs = 0
         self.launches_per_step = None
 
     # ------------------------------------------------------------------
@@ -602,6 +604,70 @@ class StepEngine:
         out["step_total"] = sum(out[k] for k in self.STAGES)
         out["captured"] = False
         return out
+
+    # ------------------------------------------------------------------
+    # forward-only evaluation  (ref cli.py:542-552 ``_evaluate``)
+    def launch_eval(self, stream=None):
+        """Forward of the loaded batch with the loss head fused with the
+        sigmoid (``dlrm_bce_head``: prob, per-batch loss sum and correct count
+        into ``stats``); no backward, no update, no sort."""
+        main = stream if stream is not None else torch.cuda.current_stream()
+        s = _lib.stream_handle(main)
+        L, call, P = self.layers, _lib.call, _lib.ptr
+        B, d, nf = self.B, self.d, self.nf
+        relu = _lib.ACT["relu"]
+        ef = P(self.err_flag)
+        call("dlrm_err_reset", P(self.err_pos), self.T, ef, s)
+        a, lda = self.x, self.x.stride(0)
+        for i in range(self.Lb):
+            l = L[i]
+            last = i == self.Lb - 1
+            out, ldo = (self.Z, nf * d) if last else (self.bact[i], self.bact[i].stride(0))
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), ldo, B, l.n_out, l.n_in, l.n_out if last else out.shape[1],
+                 relu, s)
+            a, lda = out, ldo
+        call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
+             P(self.Z), nf * d, P(self.err_pos), ef, s)
+        call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
+             self.R.stride(0), self.R.shape[1], s)
+        a, lda = self.R, self.R.stride(0)
+        for i in range(self.Lt - 1):
+            l = L[self.Lb + i]
+            out = self.tact[i]
+            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
+                 P(out), out.stride(0), B, l.n_out, l.n_in, out.shape[1], relu, s)
+            a, lda = out, out.stride(0)
+        head = L[-1]
+        call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), B,
+             head.n_in, P(self.labels), self.n_total, P(self.logits),
+             P(self.prob), P(self.glogit), None, P(self.stats), P(self.lin_ws),
+             self.lin_ws_bytes, s)
+
+    def run_eval(self):
+        """Forward-only pass of the loaded input set (graph-replayed from the
+        second call on, one graph per input set)."""
+        g = self.eval_graphs.get(self._set)
+        if g is not None:
+            g.replay()
+            return
+        if self._eval_runs >= 1:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.launch_eval()
+            self.eval_graphs[self._set] = g
+            g.replay()
+            return
+        self.launch_eval()
+        self._eval_runs += 1
+
+    def eval_result(self):
+        """(loss sum, correct count, probs) of the last ``run_eval``; raises
+        LookupIndexError for an out-of-range index."""
+        self.check_errors()
+        st = self.stats.cpu()
+        return float(st[0]), float(st[1]), self.prob.clone()
 
     def run(self):
         if self.graph is not None:

@@ -17,7 +17,9 @@ For every trajectory config it
      parameters.
 
 It also stores embedding-bag fixtures (weighted bags, empty bags, duplicate
-rows) computed by ``dlrmkit.lookup_batch`` / ``lookup_backward``.
+rows) computed by ``dlrmkit.lookup_batch`` / ``lookup_backward``, a
+checkpoint written by ``dlrmkit.cli.save_checkpoint`` (``ckpt_toy.dlrmkit``)
+and the reference's ``_evaluate`` over validation batches (``eval_*.npz``).
 The GPU box never runs this script; it only reads the ``.npz`` files.
 """
 
@@ -209,8 +211,65 @@ def make_bags():
     print("bags: ok")
 
 
+def ref_start_model(c):
+    """dlrmkit model of a trajectory config at the GPU start point (every
+    parameter rounded to float32, held in float64)."""
+    cfg = dlrmkit.DlrmConfig(embedding_sizes=c["tables"], sparse_dim=c["d"],
+                             bottom_mlp_dims=c["bot"], top_mlp_dims=c["top"],
+                             seed=c["seed"])
+    m = dlrmkit.init_model(cfg)
+    for l in m.bottom.layers + m.top.layers:
+        l.weight[...] = l.weight.astype(np.float32)
+        l.bias[...] = l.bias.astype(np.float32)
+    for t in m.tables:
+        t.weights[...] = t.weights.astype(np.float32)
+    return cfg, m
+
+
+def make_ckpt():
+    """A reference-written checkpoint of the toy config's start point."""
+    _, m = ref_start_model(TRAJ["toy"])
+    path = os.path.join(HERE, "ckpt_toy.dlrmkit")
+    ref_cli.save_checkpoint(path, m)
+    back = ref_cli.load_checkpoint(path)
+    for a, b in zip(port_arrays(ref_model_to_port(m)), port_arrays(ref_model_to_port(back))):
+        assert np.array_equal(a, b)
+    print("ckpt: ok ->", path)
+
+
+def make_eval(name, nbatches=3):
+    """dlrmkit's _evaluate (cli.py:542-552) over validation batches of the
+    CLI random source (key 1, as run_training draws them), dense rounded to
+    float32, from the float32 start point."""
+    c = TRAJ[name]
+    cfg, m = ref_start_model(c)
+    ours = RandomBatchSource(c["tables"], c["bot"][0], c["batch"], c["k"], c["fixed"],
+                             seed=c["seed"], key=1)
+    opts = ref_cli.RunOptions(mini_batch_size=c["batch"], num_indices_per_lookup=c["k"],
+                              num_indices_per_lookup_fixed=c["fixed"])
+    src = ref_cli._RandomSource(cfg, opts, key=1)
+    batches, hbs = [], []
+    for _ in range(nbatches):
+        dense, sparse, labels = src.next_batch()
+        hb = ours.next_batch()
+        assert digest([dense, *[s.offsets for s in sparse], *[s.indices for s in sparse],
+                       labels]) == digest(batch_arrays(hb)), "batch mismatch"
+        batches.append((dense.astype(np.float32).astype(np.float64), sparse, labels))
+        hbs.append(hb)
+    vloss, vacc = ref_cli._evaluate(m, batches)
+    np.savez_compressed(os.path.join(HERE, f"eval_{name}.npz"), config=np.array(json.dumps(c)),
+                        nbatches=np.array(nbatches), loss=np.array(vloss), acc=np.array(vacc),
+                        input_digest=np.array(digest([a for hb in hbs for a in batch_arrays(hb)])))
+    print(f"eval {name}: loss {vloss:.6f} acc {vacc:.4f}")
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
+    if not only or "ckpt" in only:
+        make_ckpt()
+    if not only or "eval" in only:
+        make_eval("c3s")
+        make_eval("c1s")
     if not only:
         make_bags()
     for name, c in TRAJ.items():
