@@ -286,6 +286,27 @@ int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* up
  * wherever the shape and strides allow (default), 1 = SIMT fp32 only. */
 int dlrm_gemm_mode(int32_t mode);
 
+/* ---- input pipeline: Criteo TSV ingestion (host code, multithreaded) ----
+ * Replaces dlrmkit.datagen.parse_criteo / read_criteo (datagen.py:318-371)
+ * for whole blocks of text.  Parses up to max_records non-blank lines of
+ * text[0, nbytes) (whitespace-only lines skipped but counted)
+ * into labels[r] (0 / 1), dense[r * ld_dense + i] = fp32(log1p(max(x, 0)))
+ * (13 fields, empty -> 0) and cat[i * ld_cat + r] = blake2b64(token) %
+ * vocab_sizes[i] (26 fields, empty -> 0).  *consumed = bytes used.  Returns
+ * the record count; -1 bad arguments; -2 a malformed record, whose message
+ * ("line k: ...", k counted from first_lineno, the reference's
+ * CriteoFormatError text) is in dlrm_last_error().  flags: bit 0 = universal
+ * newlines ('\n', '\r', "\r\n" end a line, as Python text-mode files do for
+ * read_criteo; otherwise only '\n'); bits 8.. = threads (0: all cores).
+ * Pointers are HOST pointers (pinned buffers of the next batch). */
+int64_t dlrm_criteo_parse(const char* text, int64_t nbytes, const int64_t* vocab_sizes,
+                          int64_t max_records, float* labels, float* dense, int64_t ld_dense,
+                          int64_t* cat, int64_t ld_cat, int64_t first_lineno, int64_t* consumed,
+                          int32_t flags);
+/* The 64-bit token hash (ref datagen.py _hash_token): BLAKE2b, 8-byte digest,
+ * no key, digest bytes read little-endian. */
+uint64_t dlrm_blake2b64(const void* data, int64_t nbytes);
+
 /* Count of this library's kernel launches since load (for bench.py). */
 int64_t dlrm_launch_count(void);
 const char* dlrm_last_error(void);

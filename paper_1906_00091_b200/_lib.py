@@ -90,7 +90,8 @@ _SIZE_FNS = {
 
 # every symbol include/dlrm_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = sorted(list(_SIGS) + list(_SIZE_FNS) + [
-    "dlrm_launch_count", "dlrm_last_error", "dlrm_build_info"])
+    "dlrm_launch_count", "dlrm_last_error", "dlrm_build_info", "dlrm_criteo_parse",
+    "dlrm_blake2b64"])
 
 _lib = None
 
@@ -112,6 +113,11 @@ def lib():
             f = getattr(L, name)
             f.argtypes, f.restype = args, _sz
         L.dlrm_launch_count.argtypes, L.dlrm_launch_count.restype = [], _i64
+        # host-side input pipeline (no GPU needed)
+        L.dlrm_criteo_parse.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64,
+                                        _i64, _vp, _i32]
+        L.dlrm_criteo_parse.restype = _i64
+        L.dlrm_blake2b64.argtypes, L.dlrm_blake2b64.restype = [_vp, _i64], C.c_uint64
         L.dlrm_last_error.restype = C.c_char_p
         L.dlrm_build_info.restype = C.c_char_p
         _lib = L

@@ -263,14 +263,74 @@ def make_eval(name, nbatches=3):
     print(f"eval {name}: loss {vloss:.6f} acc {vacc:.4f}")
 
 
+def make_criteo():
+    """A Criteo-format TSV (empty fields, negative / large dense values,
+    unicode tokens, a trailing carriage return, blank lines) and dlrmkit's
+    read_criteo / parse_criteo results for it, plus malformed lines with the
+    reference's error messages."""
+    from dlrmkit import datagen
+    import tempfile
+    rng = np.random.default_rng(11)
+    vocab = [int(v) for v in rng.integers(1, 10**7, 26)]
+    vocab[3], vocab[7] = 1, 3
+    words = ["", "68fd1e64", "80e26c9b", "fb936136", "7b4723c4", "25c83c98", "7e0ccccf",
+             "de7995b8", "1f89b562", "a73ee510", "\u00e9t\u00e9", "\u6f22\u5b57", "x" * 140]
+    lines = []
+    for r in range(300):
+        lab = "" if r % 37 == 5 else str(int(rng.integers(0, 2)))
+        dense = []
+        for i in range(13):
+            u = rng.random()
+            dense.append("" if u < 0.15 else str(int(rng.integers(-3, 0))) if u < 0.25
+                         else str(int(rng.integers(0, 10**6))))
+        cats = [words[int(rng.integers(0, len(words)))] if rng.random() < 0.5
+                else format(int(rng.integers(0, 2**32)), "08x") for _ in range(26)]
+        lines.append("\t".join([lab] + dense + cats))
+        if r % 50 == 7:
+            lines.append("")          # blank line (skipped, counted)
+    lines[10] = lines[10] + "\r"     # stays in the last token
+    text = "\n".join(lines) + "\n"
+    with tempfile.NamedTemporaryFile("w", suffix=".tsv", delete=False, encoding="utf-8") as f:
+        f.write(text)
+        path = f.name
+    samples = list(datagen.read_criteo(path, vocab))
+    os.unlink(path)
+    store = {"text": np.frombuffer(text.encode("utf-8"), np.uint8),
+             "vocab": np.array(vocab, np.int64),
+             "labels": np.array([s.label for s in samples], np.int64),
+             "dense": np.stack([s.dense for s in samples]),
+             "cat": np.stack([s.categorical for s in samples])}
+    good = lines[0].split("\t")
+    bad = [("\t".join(good[:-1]), 7),
+           ("\t".join(["2"] + good[1:]), 3),
+           ("\t".join(["x"] + good[1:]), 1),
+           ("\t".join(good[:4] + ["1.5.2"] + good[5:]), 9),
+           ("\t".join(good + ["extra"]), 12)]
+    msgs = []
+    for ln, lineno in bad:
+        try:
+            datagen.parse_criteo(ln, vocab, lineno)
+            raise AssertionError("expected an error")
+        except datagen.CriteoFormatError as e:
+            msgs.append(str(e))
+    store["bad_lines"] = np.array([b[0] for b in bad])
+    store["bad_linenos"] = np.array([b[1] for b in bad])
+    store["bad_msgs"] = np.array(msgs)
+    np.savez_compressed(os.path.join(HERE, "criteo.npz"), **store)
+    print(f"criteo: {len(samples)} records, errors {msgs}")
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
+    if "criteo" in only:
+        make_criteo()
     if not only or "ckpt" in only:
         make_ckpt()
     if not only or "eval" in only:
         make_eval("c3s")
         make_eval("c1s")
     if not only:
+        make_criteo()
         make_bags()
     for name, c in TRAJ.items():
         if not only or name in only:

@@ -139,3 +139,22 @@ def test_adagrad_resume_is_bitwise(golden, tmp_path):
     assert rc.loss == ra[2].loss
     for a, b in zip(params(ma), params(mc)):
         assert np.array_equal(a, b)
+
+
+def test_criteo_batches_train_and_evaluate():
+    """Criteo TSV -> native parser -> CriteoBatch -> train_step / evaluate."""
+    from paper_1906_00091_b200.criteo import CriteoBatchReader
+    fx = dict(np.load(os.path.join(HERE, "golden", "criteo.npz")))
+    vocab = [1000 + 37 * i for i in range(26)]
+    p = "/tmp/_criteo_gpu_test.tsv"
+    with open(p, "wb") as f:
+        f.write(fx["text"].tobytes())
+    batches = list(CriteoBatchReader(p, vocab, 64))
+    os.unlink(p)
+    cfg = DlrmConfig(vocab, 16, [13, 64, 16], [64, 1], seed=3)
+    model = init_model(cfg)
+    opt = make_optimizer("sgd", 0.1)
+    losses = [train_step(model, *b.train_args(), opt).loss for b in batches]
+    assert all(np.isfinite(losses))
+    vloss, vacc = evaluate(model, [b.train_args() for b in batches[:2]])
+    assert np.isfinite(vloss) and 0.0 <= vacc <= 1.0
