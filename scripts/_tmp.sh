@@ -1,1 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_checkpoint_eval.py -x -q 2>&1 | tail -25
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
