@@ -245,6 +245,20 @@ int dlrm_head_step(const float* A, int64_t lda, const float* w, const float* b,
                    int32_t relu_mask, float* dw, float* db, float* w_upd, float* b_upd,
                    const dlrm_update* upd, const int32_t* err_flag, void* workspace,
                    size_t ws_bytes, dlrm_stream_t stream);
+/* dlrm_head_step as its two launches: _partials (prob, grad_z, dA and the
+ * per-CTA partial dw / db / loss / correct sums in the workspace) and _reduce
+ * (fixed-order reduction into dw / db / stats + the fused update).  Only the
+ * workspace links them, so _reduce may run on another stream, ordered after
+ * _partials (the step engine takes it off the critical path: the data
+ * gradients below the head need only dA). */
+int dlrm_head_step_partials(const float* A, int64_t lda, const float* w, const float* b,
+                            int64_t M, int64_t K, const float* y, float n_total, float* prob,
+                            float* grad_z, float* dA, int64_t ldda, int32_t relu_mask,
+                            void* workspace, size_t ws_bytes, dlrm_stream_t stream);
+int dlrm_head_step_reduce(int64_t M, int64_t K, float* stats, float* dw, float* db,
+                          float* w_upd, float* b_upd, const dlrm_update* upd,
+                          const int32_t* err_flag, void* workspace, size_t ws_bytes,
+                          dlrm_stream_t stream);
 
 /* Backward through the N = 1 head: dA[m,k] = g[m]*w[k] (* (A[m,k] > 0) when
  * relu_mask, i.e. A is a ReLU output); dw[k] = sum_m g[m]*A[m,k];

@@ -59,6 +59,9 @@ _SIGS = {
     "dlrm_update_dense": [_vp, _vp, _i64, _vp, _vp, _vp],
     "dlrm_head_step": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp,
                        _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+    "dlrm_head_step_partials": [_vp, _i64, _vp, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp,
+                                _i64, _i32, _vp, _sz, _vp],
+    "dlrm_head_step_reduce": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
     "dlrm_emb_bwd_coalesce": [_i64, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp,
                               _vp, _vp, _sz, _vp],
     "dlrm_sgd_rows": [_vp, _i64, _vp, _vp, _i64, _f32, _vp],

@@ -268,23 +268,18 @@ extern "C" size_t dlrm_head_step_workspace_size(int64_t M, int64_t K) {
   return size_t(ceil_div(M > 0 ? M : 1, HR)) * size_t(K + 3) * sizeof(float) + 256;
 }
 
-extern "C" int dlrm_head_step(const float* A, int64_t lda, const float* w, const float* b,
-                              int64_t M, int64_t K, const float* y, float n_total, float* prob,
-                              float* grad_z, float* stats, float* dA, int64_t ldda,
-                              int32_t relu_mask, float* dw, float* db, float* w_upd,
-                              float* b_upd, const dlrm_update* upd, const int32_t* err_flag,
-                              void* workspace, size_t ws_bytes, dlrm_stream_t stream) {
+static int head_partials(const float* A, int64_t lda, const float* w, const float* b,
+                         int64_t M, int64_t K, const float* y, float n_total, float* prob,
+                         float* grad_z, float* dA, int64_t ldda, int32_t relu_mask,
+                         void* workspace, size_t ws_bytes, cudaStream_t s) {
   DLRM_REQUIRE(M >= 1 && K >= 4 && K % 4 == 0 && K <= 128 * 8 && lda % 4 == 0 &&
                    (!dA || ldda % 4 == 0),
                "head_step needs K in [4, 1024], K % 4 == 0 and 16-byte rows");
   DLRM_REQUIRE(reinterpret_cast<uintptr_t>(A) % 16 == 0 && reinterpret_cast<uintptr_t>(w) % 16 == 0 &&
                    (!dA || reinterpret_cast<uintptr_t>(dA) % 16 == 0),
                "head_step needs 16-byte aligned A / w / dA");
-  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
-               "bad update rule");
   DLRM_REQUIRE(workspace && ws_bytes >= dlrm_head_step_workspace_size(M, K),
                "head_step workspace too small");
-  cudaStream_t s = as_stream(stream);
   float* part = static_cast<float*>(workspace);
   const int64_t nb = ceil_div(M, HR);
   const int kvl = int(ceil_div(K / 4, 32));
@@ -295,10 +290,53 @@ extern "C" int dlrm_head_step(const float* A, int64_t lda, const float* w, const
   if (kvl <= 2) go(head_fused_kernel<2>);
   else if (kvl <= 4) go(head_fused_kernel<4>);
   else go(head_fused_kernel<8>);
-  if (int rc = check_launch("head_fused_kernel")) return rc;
-  launch(head_final_kernel, unsigned(ceil_div(K + 3, 32)), 256, 0, s, part, nb, K, dw, db, stats,
-         w_upd, b_upd, upd_rule(upd), err_flag);
+  return check_launch("head_fused_kernel");
+}
+
+static int head_reduce(int64_t M, int64_t K, float* stats, float* dw, float* db, float* w_upd,
+                       float* b_upd, const dlrm_update* upd, const int32_t* err_flag,
+                       void* workspace, size_t ws_bytes, cudaStream_t s) {
+  DLRM_REQUIRE(M >= 1 && K >= 4 && K <= 128 * 8, "head_step needs K in [4, 1024]");
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  DLRM_REQUIRE(workspace && ws_bytes >= dlrm_head_step_workspace_size(M, K),
+               "head_step workspace too small");
+  launch(head_final_kernel, unsigned(ceil_div(K + 3, 32)), 256, 0, s,
+         static_cast<const float*>(workspace), ceil_div(M, HR), K, dw, db, stats, w_upd, b_upd,
+         upd_rule(upd), err_flag);
   return check_launch("head_final_kernel");
+}
+
+extern "C" int dlrm_head_step(const float* A, int64_t lda, const float* w, const float* b,
+                              int64_t M, int64_t K, const float* y, float n_total, float* prob,
+                              float* grad_z, float* stats, float* dA, int64_t ldda,
+                              int32_t relu_mask, float* dw, float* db, float* w_upd,
+                              float* b_upd, const dlrm_update* upd, const int32_t* err_flag,
+                              void* workspace, size_t ws_bytes, dlrm_stream_t stream) {
+  DLRM_REQUIRE(upd != nullptr && (upd->kind == DLRM_UPD_SGD || upd->kind == DLRM_UPD_ADAGRAD),
+               "bad update rule");
+  cudaStream_t s = as_stream(stream);
+  if (int rc = head_partials(A, lda, w, b, M, K, y, n_total, prob, grad_z, dA, ldda, relu_mask,
+                             workspace, ws_bytes, s))
+    return rc;
+  return head_reduce(M, K, stats, dw, db, w_upd, b_upd, upd, err_flag, workspace, ws_bytes, s);
+}
+
+extern "C" int dlrm_head_step_partials(const float* A, int64_t lda, const float* w,
+                                       const float* b, int64_t M, int64_t K, const float* y,
+                                       float n_total, float* prob, float* grad_z, float* dA,
+                                       int64_t ldda, int32_t relu_mask, void* workspace,
+                                       size_t ws_bytes, dlrm_stream_t stream) {
+  return head_partials(A, lda, w, b, M, K, y, n_total, prob, grad_z, dA, ldda, relu_mask,
+                       workspace, ws_bytes, as_stream(stream));
+}
+
+extern "C" int dlrm_head_step_reduce(int64_t M, int64_t K, float* stats, float* dw, float* db,
+                                     float* w_upd, float* b_upd, const dlrm_update* upd,
+                                     const int32_t* err_flag, void* workspace, size_t ws_bytes,
+                                     dlrm_stream_t stream) {
+  return head_reduce(M, K, stats, dw, db, w_upd, b_upd, upd, err_flag, workspace, ws_bytes,
+                     as_stream(stream));
 }
 
 extern "C" int dlrm_relu_grad(const float* g, int64_t ldg, const float* act,

@@ -210,6 +210,10 @@ class StepEngine:
         # update beside the next layer's data gradient
         self.emb_side = os.environ.get("DLRM_EMB_FWD_SIDE", "1") != "0"
         self.wgrad_side = os.environ.get("DLRM_WGRAD_SIDE", "1") != "0"
+        # DLRM_HEAD_SPLIT=1 moves the head's reduction + update to the
+        # weight-gradient stream; measured slower at c3 (0.431 vs 0.428 ms:
+        # it delays the first weight gradient), so off by default
+        self.head_split = os.environ.get("DLRM_HEAD_SPLIT", "0") == "1"
         self.fwd_stream = torch.cuda.Stream(device=dev)
         self.wg_stream = torch.cuda.Stream(device=dev)
 
@@ -432,12 +436,22 @@ class StepEngine:
         ga = self.gtop[-1] if self.Lt > 1 else self.gR
         um, ue = C.byref(self.upd_mlp), C.byref(self.upd_emb)
         if self.head_fused:
-            # forward + BCE + backward (dA masked by the ReLU below) + update
-            # of the N = 1 layer in one pass over its input
-            call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), B,
+            # forward + BCE + backward (dA masked by the ReLU below) of the
+            # N = 1 layer in one pass over its input, then the reduction of
+            # its dw / db / loss partials + the update (optionally on the
+            # weight-gradient stream: the data gradients need only dA)
+            call("dlrm_head_step_partials", P(a), lda, P(head.storage), P(head.bias), B,
                  head.n_in, P(self.labels), self.n_total, P(self.prob), P(self.glogit),
-                 P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None, None,
-                 P(head.storage), P(head.bias), um, ef, ws, wsb, s)
+                 P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, ws, wsb, s)
+            red = (B, head.n_in, P(self.stats), None, None, P(head.storage), P(head.bias),
+                   um, ef, ws, wsb)
+            if wg is not None and self.head_split:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                self.wg_stream.wait_event(ev)
+                call("dlrm_head_step_reduce", *red, wg)
+            else:
+                call("dlrm_head_step_reduce", *red, s)
         else:
             call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), B,
                  head.n_in, P(self.labels), self.n_total, P(self.logits),
