@@ -15,6 +15,17 @@
 namespace dlrm {
 namespace {
 
+// 512 threads per CTA: at the Terabyte shape (27 features, d = 128, B = 32768)
+// the backward takes 361 vs 446 us with 256 (scripts/interact_bench.py);
+// 1024 is slower (register-limited); small shapes are unchanged
+#ifndef DLRM_IA_THREADS
+#define DLRM_IA_THREADS 512
+#endif
+#ifndef DLRM_IA_BUDGET_KB
+#define DLRM_IA_BUDGET_KB 96
+#endif
+constexpr int kIaThreads = DLRM_IA_THREADS;
+
 __device__ __forceinline__ void pair_of(int p, int nf, int& i, int& j) {
   // row-major upper triangle: row i holds nf-1-i pairs
   int row = 0, base = 0;
@@ -24,7 +35,7 @@ __device__ __forceinline__ void pair_of(int p, int nf, int& i, int& j) {
 }
 
 template <bool V4>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kIaThreads)
 interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
                     float* __restrict__ out, int64_t ld_out, int64_t pad_to) {
   pdl_entry();
@@ -148,7 +159,7 @@ interact_fwd_kernel(FeatureSet fs, int nf, int64_t dim, int64_t batch, int S,
 }
 
 template <bool V4>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kIaThreads)
 interact_bwd_kernel(FeatureSet fs, GradFeatureSet gs, int nf, int64_t dim,
                     int64_t batch, int S, const float* __restrict__ gout,
                     int64_t ld_gout, int mask_f0) {
@@ -284,13 +295,13 @@ extern "C" int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf,
   if (batch == 0) return 0;
   const int npairs = nf * (nf - 1) / 2;
   const size_t fixed = align_up(size_t(npairs) * 4, 16);
-  const int S = pick_samples(nf, dim, batch, 0, fixed, 96 * 1024);
+  const int S = pick_samples(nf, dim, batch, 0, fixed, DLRM_IA_BUDGET_KB * 1024);
   const size_t smem = size_t(S) * nf * (dim + 4) * 4 + fixed;
   DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
   cudaStream_t s = as_stream(stream);
   auto k = v4 ? interact_fwd_kernel<true> : interact_fwd_kernel<false>;
   DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  launch(k, unsigned(ceil_div(batch, S)), 256, smem, s, fs, nf, dim, batch, S, out,
+  launch(k, unsigned(ceil_div(batch, S)), kIaThreads, smem, s, fs, nf, dim, batch, S, out,
                                                      ld_out, pad_to);
   return check_launch("interact_fwd_kernel");
 }
@@ -315,13 +326,13 @@ extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
   v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
   if (batch == 0) return 0;
   const size_t extra = size_t(nf) * ((nf + 3) & ~3) * 4;
-  const int S = pick_samples(nf, dim, batch, extra, 0, 96 * 1024);
+  const int S = pick_samples(nf, dim, batch, extra, 0, DLRM_IA_BUDGET_KB * 1024);
   const size_t smem = size_t(S) * (nf * (dim + 4) * 4 + extra);
   DLRM_REQUIRE(smem <= 200 * 1024, "interaction tile exceeds shared memory");
   cudaStream_t s = as_stream(stream);
   auto k = v4 ? interact_bwd_kernel<true> : interact_bwd_kernel<false>;
   DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  launch(k, unsigned(ceil_div(batch, S)), 256, smem, s, fs, gs, nf, dim, batch, S,
+  launch(k, unsigned(ceil_div(batch, S)), kIaThreads, smem, s, fs, gs, nf, dim, batch, S,
                                                      gout, ld_gout, relu_mask_f0);
   return check_launch("interact_bwd_kernel");
 }
