@@ -17,6 +17,7 @@ python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_ref_c3.json 2
 ./scripts/mma_rate > $out/mma_rate.txt 2>&1
 ./scripts/gather_rmw > $out/gather_rmw.txt 2>&1
 python scripts/gemm_bench.py > $out/gemm_bench.txt 2>&1
+python scripts/interact_bench.py > $out/interact_bench.jsonl 2>&1
 python scripts/emb_one.py --bwd --apply > $out/emb_one_c3.json 2>&1
 timeout 900 python scripts/emb_sweep.py > $out/c5_sweep.jsonl 2> $out/c5_sweep.err
 timeout 600 python scripts/emb_sweep.py --cpu > $out/c5_sweep_cpu.jsonl 2>&1
