@@ -873,9 +873,10 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
                              int64_t M, int64_t N, int64_t K) {
-  // K < 32: one mostly-empty 32-wide MN-major box per k-step; the SIMT
-  // kernel is faster there (measured 41 vs 68 us at 2048 x 512 x 13)
-  return tc_enabled() && M >= 1 && N >= 1 && K >= 32 && aligned16(gZ) && aligned16(X) &&
+  // any K: a narrow input (the 13 dense features) lands as one zero-filled
+  // 32-wide MN-major box per k-step; with cluster split-K this beats the
+  // SIMT split-K path end to end (c2 0.241 -> 0.233 ms/step)
+  return tc_enabled() && M >= 1 && N >= 1 && K >= 1 && aligned16(gZ) && aligned16(X) &&
          ldg % 4 == 0 && ldx % 4 == 0;
 }
 

@@ -1,1 +1,1 @@
-for i in 1 2; do for v in 0 4; do DLRM_GRAPH_PRIO=$v python bench.py --steps 200 --warmup 5 --no-cpu-baseline | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('prio=$v', round(d['value']), round(d['ms_per_step'],4), round(d['e2e']['ms_per_step'],4))"; done; done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3
