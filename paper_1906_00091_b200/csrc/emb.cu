@@ -630,12 +630,14 @@ constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
 // per SM — the apply is bound by the rows in flight; measured on B200 at the
 // c3 shape (8 x 1M x 64, 827K lookups): 127 us at 3 blocks/SM (80 registers),
 // 102 us at 4 (64 registers, a few bytes of spills).
-template <int VEC, int LPB, int NV, bool COALESCE>
+// CH sorted slots per chunk (and per staged batch): 32, or 8 when the
+// lookups are few (the chunks are the kernel's only parallelism: at the
+// Kaggle shape, 53 k one-index bags, CH = 32 left 52 CTAs).
+template <int VEC, int LPB, int NV, bool COALESCE, int CH>
 __global__ void __launch_bounds__(fold_groups<LPB>() * LPB, NV == 1 ? 4 : 1)
 emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   pdl_entry();
   using V = typename VecT<VEC>::T;
-  constexpr int CH = 32;  // sorted slots staged per batch
   constexpr int U = COALESCE ? 8 : 4;  // gradient rows in flight per lane
   constexpr int GROUPS = fold_groups<LPB>();
   __shared__ uint32_t s_key[GROUPS][CH];
@@ -1161,8 +1163,16 @@ template <int VEC, int LPB, int NV, bool CO>
 void launch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim,
                  cudaStream_t s) {
   constexpr int GROUPS = fold_groups<LPB>();
-  const int64_t chunks = ceil_div(fa.n, 32);
-  launch(emb_fold_kernel<VEC, LPB, NV, CO>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, 0, s, fa, ts, dim);
+  // fewer than ~1k threads per SM with 32-slot chunks: 8-slot chunks
+  if (ceil_div(fa.n, 32) * LPB < int64_t(kNumSMs) * 1024) {
+    const int64_t chunks = ceil_div(fa.n, 8);
+    launch(emb_fold_kernel<VEC, LPB, NV, CO, 8>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB,
+           0, s, fa, ts, dim);
+  } else {
+    const int64_t chunks = ceil_div(fa.n, 32);
+    launch(emb_fold_kernel<VEC, LPB, NV, CO, 32>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB,
+           0, s, fa, ts, dim);
+  }
 }
 
 template <bool CO>

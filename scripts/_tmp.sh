@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3
+python scripts/emb_one.py --tables 26 --rows 1000000 --d 16 --pool-max 1 --pool-fixed --batch 2048 --bwd --apply
+python scripts/emb_one.py --bwd --apply
