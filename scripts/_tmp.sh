@@ -1,2 +1,3 @@
-python scripts/emb_one.py --tables 26 --rows 1000000 --d 16 --pool-max 1 --pool-fixed --batch 2048 --bwd --apply
-python scripts/emb_one.py --bwd --apply
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+python scripts/gemm_bench.py 2>&1 | grep "'K': 13"
+for i in 1 2; do for c in c2 c1; do python bench.py --config $c --steps 200 --warmup 5 --no-cpu-baseline | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value']), round(d['ms_per_step'],4))"; done; done

@@ -16,7 +16,9 @@ TOL = 1e-5
 
 SHAPES = [(2048, 1024, 1024), (2048, 512, 512), (2048, 64, 512), (2048, 1024, 100),
           (2048, 512, 13), (128, 512, 52), (64, 256, 367), (33, 30, 64), (300, 16, 64),
-          (4096, 128, 479), (2048, 16, 64)]
+          (4096, 128, 479), (2048, 16, 64),
+          # narrow layer inputs (the dense features): the slab weight gradient
+          (128, 512, 13), (32768, 512, 13), (2048, 300, 32), (1000, 7, 3), (5, 130, 16)]
 
 
 def ceil4(n):
