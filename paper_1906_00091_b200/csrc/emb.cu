@@ -618,8 +618,14 @@ struct FoldArgs {
   uint4* long_runs;      // (start, end, row, 0)
 };
 
+// Runs (equal-row segments) longer than kLongRun slots are folded by the
+// segment path (a whole warp per 256-slot segment, 8-32 rows in flight)
+// instead of by the one sub-warp that owns the run start (4 rows in flight).
+// The fold order within a segment is the same strict order, so results do
+// not depend on the threshold; 16 measured best (Kaggle-shaped step 0.234 ->
+// 0.201 ms: its small tables make many 20-700-slot runs; c3 unchanged).
 #ifndef DLRM_LONG_RUN
-#define DLRM_LONG_RUN 96
+#define DLRM_LONG_RUN 16
 #endif
 constexpr int kLongRun = DLRM_LONG_RUN;
 
