@@ -524,7 +524,7 @@ template <int LPB>
 __global__ void __launch_bounds__(256)
 emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots, int64_t bag_blocks,
                 uint32_t sentinel, uint32_t* __restrict__ keys,
-                uint32_t* __restrict__ vals, int32_t* __restrict__ bag_of,
+                uint32_t* __restrict__ vals, int32_t* __restrict__ bag_of, int by_bag,
                 int64_t* err_pos, int32_t* err_flag) {
   pdl_entry();
   if (blockIdx.x < bag_blocks) {
@@ -548,8 +548,12 @@ emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots, int64_t bag_
       if (idx >= 0 && idx < nrows) key = uint32_t(rbase + idx);
       else record_error(err_pos, err_flag, t, k);
       keys[cb + k] = key;
-      vals[cb + k] = uint32_t(cb + k);
-      bag_of[cb + k] = int32_t(j);
+      if (by_bag) {
+        vals[cb + k] = uint32_t(j);
+      } else {
+        vals[cb + k] = uint32_t(cb + k);
+        bag_of[cb + k] = int32_t(j);
+      }
     }
     return;
   }
@@ -563,8 +567,8 @@ emb_keys_kernel(TableSet ts, int64_t num_bags, int64_t total_slots, int64_t bag_
   const int64_t k = s - ts.cap_base[lo];
   if (k < __ldg(ts.t[lo].offsets + num_bags)) return;  // live: written by its bag
   keys[s] = sentinel;
-  vals[s] = uint32_t(s);
-  bag_of[s] = 0;
+  vals[s] = by_bag ? 0u : uint32_t(s);
+  if (!by_bag) bag_of[s] = 0;
 }
 
 __device__ __forceinline__ int table_of_row(const TableSet& ts, uint32_t row) {
@@ -602,8 +606,9 @@ __global__ void count_unique_kernel(const uint32_t* uid, const uint32_t* flags,
 // rows_out/values_out[uid] = (row, acc) (coalesce mode).
 struct FoldArgs {
   const uint32_t* keys;  // sorted
-  const uint32_t* vals;  // slots, sorted by key (stable)
-  const int32_t* bag_of;
+  const uint32_t* vals;  // sorted by key (stable): bags (by_bag) or slots
+  const int32_t* bag_of;  // slot -> bag (slot values only)
+  int by_bag;             // 1: no table is weighted, the sort carried the bag itself
   int64_t n;
   uint32_t sentinel;
   const float* grad;
@@ -671,9 +676,13 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
       float w = 1.f;
       if (k != fa.sentinel) {
         const int t = table_of_row(ts, k);
-        const uint32_t slot = fa.vals[base + i];
-        goff = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
-        if (ts.t[t].weights) w = __ldg(ts.t[t].weights + (slot - ts.cap_base[t]));
+        const uint32_t v = fa.vals[base + i];
+        if (fa.by_bag) {  // one memory level less on the staging path
+          goff = ts.t[t].out_offset + int64_t(v) * fa.grad_stride;
+        } else {
+          goff = ts.t[t].out_offset + int64_t(fa.bag_of[v]) * fa.grad_stride;
+          if (ts.t[t].weights) w = __ldg(ts.t[t].weights + (v - ts.cap_base[t]));
+        }
       }
       s_goff[g][i] = goff;
       s_w[g][i] = w;
@@ -837,9 +846,11 @@ emb_long_run_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs) {
     const int cnt = int(s1 - p0 < CHUNK ? s1 - p0 : CHUNK);
     __syncthreads();
     if (threadIdx.x < cnt) {
-      const uint32_t slot = fa.vals[p0 + threadIdx.x];
-      s_goff[threadIdx.x] = ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride;
-      s_w[threadIdx.x] = ts.t[t].weights ? __ldg(ts.t[t].weights + (slot - ts.cap_base[t])) : 1.f;
+      const uint32_t v = fa.vals[p0 + threadIdx.x];
+      const int64_t bag = fa.by_bag ? int64_t(v) : int64_t(fa.bag_of[v]);
+      s_goff[threadIdx.x] = ts.t[t].out_offset + bag * fa.grad_stride;
+      s_w[threadIdx.x] = (!fa.by_bag && ts.t[t].weights)
+                             ? __ldg(ts.t[t].weights + (v - ts.cap_base[t])) : 1.f;
     }
     __syncthreads();
     for (int64_t e = threadIdx.x; e < int64_t(cnt) * dim; e += blockDim.x) {
@@ -963,9 +974,10 @@ seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
     int64_t goff = 0;  // float4 offset of this lane's slot's gradient row
     float w = 1.f;
     if (lane < cnt) {
-      const uint32_t slot = fa.vals[p0 + lane];
-      goff = (ts.t[t].out_offset + int64_t(fa.bag_of[slot]) * fa.grad_stride) / 4;
-      if (wts) w = __ldg(wts + (slot - ts.cap_base[t]));
+      const uint32_t v = fa.vals[p0 + lane];
+      const int64_t bag = fa.by_bag ? int64_t(v) : int64_t(fa.bag_of[v]);
+      goff = (ts.t[t].out_offset + bag * fa.grad_stride) / 4;
+      if (wts && !fa.by_bag) w = __ldg(wts + (v - ts.cap_base[t]));
     }
     for (int q = 0; q < cnt; q += RPI * U) {
       float4 rr[U][NV];
@@ -1136,6 +1148,16 @@ int end_bit_for(int64_t total_rows) {
   return b;  // total_rows < 2^b, so sentinel = 2^b - 1 > every real row
 }
 
+// The sort's value: the bag of the lookup when no table is weighted (the
+// backward then reads the gradient row without a slot -> bag lookup), else
+// the slot (for its weight) with the bag in bag_of.  The sort is stable, so
+// either way equal rows keep ascending-position order.
+int by_bag_values(const TableSet& ts) {
+  for (int t = 0; t < ts.nt; ++t)
+    if (ts.t[t].weights) return 0;
+  return 1;
+}
+
 // Sort (row, slot) pairs of all tables into keys_b / vals_b of the workspace.
 int sort_pairs(const TableSet& ts, int64_t nb, char* ws, const WsLayout& L, int64_t n,
                int64_t* err_pos, int32_t* err_flag, uint32_t sentinel, int end_bit,
@@ -1152,11 +1174,11 @@ int sort_pairs(const TableSet& ts, int64_t nb, char* ws, const WsLayout& L, int6
     const int64_t bag_blocks = ceil_div(nb * ts.nt * lpb, 256);
     const unsigned grid = unsigned(bag_blocks + ceil_div(n, 256));
     if (lpb == 32)
-      launch(emb_keys_kernel<32>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<32>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, by_bag_values(ts), err_pos, err_flag);
     else if (lpb == 8)
-      launch(emb_keys_kernel<8>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<8>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, by_bag_values(ts), err_pos, err_flag);
     else
-      launch(emb_keys_kernel<1>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, err_pos, err_flag);
+      launch(emb_keys_kernel<1>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, by_bag_values(ts), err_pos, err_flag);
     if (int rc = check_launch("emb_keys_kernel")) return rc;
   }
   size_t tb = L.temp_bytes;
@@ -1429,6 +1451,7 @@ int emb_apply(float* W_all, int64_t dim, const dlrm_table_desc* tables, int32_t 
   fa.keys = reinterpret_cast<const uint32_t*>(ws + p.L.keys_b);
   fa.vals = reinterpret_cast<const uint32_t*>(ws + p.L.vals_b);
   fa.bag_of = reinterpret_cast<const int32_t*>(ws + p.L.bag);
+  fa.by_bag = by_bag_values(ts);
   fa.n = p.n;
   fa.sentinel = p.sentinel;
   fa.grad = grad;
@@ -1525,6 +1548,7 @@ extern "C" int dlrm_emb_bwd_coalesce(int64_t dim, const dlrm_table_desc* table,
   fa.keys = ks;
   fa.vals = vs;
   fa.bag_of = reinterpret_cast<const int32_t*>(ws + L.bag);
+  fa.by_bag = by_bag_values(ts);
   fa.n = n;
   fa.sentinel = sentinel;
   fa.grad = grad;
