@@ -633,6 +633,13 @@ struct FoldArgs {
 #define DLRM_LONG_RUN 16
 #endif
 constexpr int kLongRun = DLRM_LONG_RUN;
+// ring depth of the fold's cp.async fast path (0: register batches only)
+// (measured at the c3 shape: 4 -> step 0.413 ms; register batches 0.425;
+// 8 -> 0.420; 12 -> 0.440); narrow rows (<= 16 floats) keep the register
+// batches (Kaggle-shaped step 0.197 vs 0.202 ms)
+#ifndef DLRM_FOLD_RING
+#define DLRM_FOLD_RING 4
+#endif
 
 template <int LPB>
 constexpr int fold_groups() { return 256 / LPB < 32 ? 256 / LPB : 32; }
@@ -702,6 +709,101 @@ emb_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim) {
   uint32_t cur = s_key[g][i];
   if (cur == fa.sentinel) return;
   int64_t run_start = base + i;
+
+#if DLRM_FOLD_RING > 0
+  if constexpr (!COALESCE && VEC == 4 && NV == 1 && LPB >= 8) {
+    // SGD / Adagrad fast path (rows <= 128 floats): a per-sub-warp ring of
+    // RR slots in shared memory, each the gradient row of one sorted slot and
+    // (for a run start) its table row, filled by cp.async RR slots ahead of
+    // the fold — RR rows in flight per sub-warp without holding them in
+    // registers.  Same arithmetic, same order as the register path below.
+    constexpr int RR = DLRM_FOLD_RING;
+    extern __shared__ float4 fold_ring[];
+    float4* rg = fold_ring + (size_t(g) * RR * 2) * LPB;  // [RR][LPB] gradient rows
+    float4* rw = rg + size_t(RR) * LPB;                    // [RR][LPB] table rows
+    const bool col_ok = lane < nvec;
+    float4 acc4 = vzero4(), w4 = vzero4();
+    bool first = true;
+    // issue slot jj of the staged chunk into ring position q
+    auto issue = [&](int jj, int q, uint32_t prevk, bool first_slot) {
+      if (jj < cnt) {
+        const uint32_t k = s_key[g][jj];
+        const bool live = k != fa.sentinel;
+        const bool starts = live && (first_slot || k != prevk);
+        const float4* src = reinterpret_cast<const float4*>(fa.grad + s_goff[g][jj]) + lane;
+        cp_async16(rg + q * LPB + lane, live && col_ok ? src : reinterpret_cast<const float4*>(fa.grad),
+                   live && col_ok);
+        const float4* wsrc = reinterpret_cast<const float4*>(fa.W + int64_t(k) * dim) + lane;
+        cp_async16(rw + q * LPB + lane, starts && col_ok ? wsrc : reinterpret_cast<const float4*>(fa.W),
+                   starts && col_ok);
+      }
+      cp_async_commit();
+    };
+    auto flush4 = [&](uint32_t row) {
+      float4* wrow = reinterpret_cast<float4*>(fa.W + int64_t(row) * dim);
+      if (col_ok) wrow[lane] = vupd(fa.upd, wrow + lane, w4, acc4);
+    };
+    while (true) {
+      // prologue: RR slots in flight
+      const int j0 = i;
+      for (int r = 0; r < RR; ++r)
+        issue(j0 + r, r, j0 + r > 0 ? s_key[g][j0 + r - 1] : cur, first && r == 0);
+      for (int jj = j0, q = 0; jj < cnt; ++jj, q = q == RR - 1 ? 0 : q + 1) {
+        cp_async_wait<RR - 1>();
+        __syncwarp(mask);
+        const uint32_t k = s_key[g][jj];
+        if (first) {
+          w4 = rw[q * LPB + lane];
+          first = false;
+        } else if (k != cur) {
+          flush4(cur);
+          if (k == fa.sentinel || base + jj >= limit) {
+            cp_async_wait<0>();
+            return;
+          }
+          cur = k;
+          run_start = base + jj;
+          acc4 = vzero4();
+          w4 = rw[q * LPB + lane];
+        }
+        const float4 r4 = rg[q * LPB + lane];
+        acc4 = vadd(acc4, vmul(s_w[g][jj], r4));
+        __syncwarp(mask);
+        issue(jj + RR, q, s_key[g][jj + RR - 1 < cnt ? jj + RR - 1 : 0], false);
+      }
+      cp_async_wait<0>();
+      base += CH;
+      if (base >= fa.n) break;
+      if (fa.keys[base] != cur) break;  // our last run ends exactly here
+      if (base - run_start >= CH) {
+        int64_t lo2 = base, step = CH;
+        int64_t hi2 = base + step;
+        while (hi2 < fa.n && fa.keys[hi2] == cur) {
+          lo2 = hi2;
+          step *= 2;
+          hi2 = lo2 + step;
+        }
+        if (hi2 > fa.n) hi2 = fa.n;
+        while (hi2 - lo2 > 1) {
+          const int64_t mid = (lo2 + hi2) >> 1;
+          if (fa.keys[mid] == cur) lo2 = mid; else hi2 = mid;
+        }
+        const int64_t run_end = lo2 + 1;
+        if (run_end - run_start > kLongRun) {
+          if (lane == 0) {
+            const uint32_t slot = atomicAdd(fa.long_count, 1u);
+            fa.long_runs[slot] = make_uint4(uint32_t(run_start), uint32_t(run_end), cur, 0u);
+          }
+          return;
+        }
+      }
+      cnt = stage(base);
+      i = 0;
+    }
+    flush4(cur);
+    return;
+  }
+#endif
 
   V acc[NV], wcur[NV];
 #pragma unroll
@@ -1192,15 +1294,20 @@ void launch_fold(const FoldArgs& fa, const TableSet& ts, int64_t dim,
                  cudaStream_t s) {
   constexpr int GROUPS = fold_groups<LPB>();
   // fewer than ~1k threads per SM with 32-slot chunks: 8-slot chunks
-  if (ceil_div(fa.n, 32) * LPB < int64_t(kNumSMs) * 1024) {
-    const int64_t chunks = ceil_div(fa.n, 8);
-    launch(emb_fold_kernel<VEC, LPB, NV, CO, 8>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB,
-           0, s, fa, ts, dim);
-  } else {
-    const int64_t chunks = ceil_div(fa.n, 32);
-    launch(emb_fold_kernel<VEC, LPB, NV, CO, 32>, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB,
-           0, s, fa, ts, dim);
-  }
+  const bool ring = DLRM_FOLD_RING > 0 && !CO && VEC == 4 && NV == 1 && LPB >= 8;
+  const size_t smem = ring ? size_t(GROUPS) * 2 * (DLRM_FOLD_RING > 0 ? DLRM_FOLD_RING : 1) * LPB * 16 : 0;
+  auto go = [&](auto kern, int64_t chunks) {
+    static bool attr = false;
+    if (smem > 0 && !attr) {  // dynamic + the static staging arrays may pass 48 KB
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      attr = true;
+    }
+    launch(kern, unsigned(ceil_div(chunks, GROUPS)), GROUPS * LPB, smem, s, fa, ts, dim);
+  };
+  if (ceil_div(fa.n, 32) * LPB < int64_t(kNumSMs) * 1024)
+    go(emb_fold_kernel<VEC, LPB, NV, CO, 8>, ceil_div(fa.n, 8));
+  else
+    go(emb_fold_kernel<VEC, LPB, NV, CO, 32>, ceil_div(fa.n, 32));
 }
 
 template <bool CO>
