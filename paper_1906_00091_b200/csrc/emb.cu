@@ -1114,10 +1114,31 @@ seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
     }
   }
   if (sub == 0) {
+    if (run.y - run.x <= uint32_t(kSeg)) {
+      // a single-segment run is finished here (seg_combine skips it): the
+      // combine of one partial is the partial itself
+      if (fa.values_out) {  // coalesce mode (lookup_backward)
+        const uint32_t u = fa.uid[run.x];
+        if (col == 0) fa.rows_out[u] = int64_t(row) - ts.t[t].row_base;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int64_t c = col + int64_t(v) * LPB;
-      if (c < nvec) reinterpret_cast<float4*>(partial + int64_t(seg) * dim)[c] = acc[v];
+        for (int v = 0; v < NV; ++v) {
+          const int64_t c = col + int64_t(v) * LPB;
+          if (c < nvec) reinterpret_cast<float4*>(fa.values_out + int64_t(u) * dim)[c] = acc[v];
+        }
+      } else if (!(fa.err_flag && *fa.err_flag)) {
+        float4* wrow = reinterpret_cast<float4*>(fa.W + int64_t(row) * dim);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int64_t c = col + int64_t(v) * LPB;
+          if (c < nvec) wrow[c] = vupd(fa.upd, wrow + c, wrow[c], acc[v]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int64_t c = col + int64_t(v) * LPB;
+        if (c < nvec) reinterpret_cast<float4*>(partial + int64_t(seg) * dim)[c] = acc[v];
+      }
     }
   }
   }  // segments (grid-stride)
@@ -1136,6 +1157,7 @@ seg_combine_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
   const int t = table_of_row(ts, row);
   const uint32_t g0 = seg_base[r];
   const uint32_t ns = (run.y - run.x + kSeg - 1) / kSeg;
+  if (ns <= 1) continue;  // finished by seg_fold_kernel
   for (int64_t c = threadIdx.x; c < dim; c += blockDim.x) {
     // partials added in segment order; loads issued 8 ahead of the adds
     const float* pc = partial + int64_t(g0) * dim + c;
