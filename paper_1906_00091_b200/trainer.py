@@ -181,6 +181,10 @@ class StepEngine:
             os.environ.get("DLRM_HEAD_FUSED", "1") != "0"
         self.lin_ws_bytes = lin
         self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
+        # the last bottom weight gradient runs on the main stream (below),
+        # concurrently with the weight-gradient stream: its own workspace
+        self.lin_ws2 = torch.empty(lin, dtype=torch.uint8, device=dev)
+        self.last_wgrad_main = os.environ.get("DLRM_LAST_WGRAD_MAIN", "1") != "0"
         self.stats = torch.zeros(2, **f32)
         self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -506,8 +510,16 @@ class StepEngine:
                 call("dlrm_linear_bwd_data", P(gz), ldg, P(l.storage), l.ldw,
                      P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), B, l.n_out, l.n_in, s)
-            wgrad(P(gz), ldg, P(xin), xin.stride(0), B, l.n_out, l.n_in, None, 0,
-                  None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
+            if i == 0 and wg is not None and self.last_wgrad_main:
+                # the main stream is idle after the last data gradient: the
+                # first layer's weight gradient runs there, beside the
+                # weight-gradient stream's queue
+                call("dlrm_linear_bwd_weight_upd", P(gz), ldg, P(xin), xin.stride(0), B,
+                     l.n_out, l.n_in, None, 0, None, P(l.storage), l.ldw, P(l.bias), um, ef,
+                     P(self.lin_ws2), self.lin_ws_bytes, s)
+            else:
+                wgrad(P(gz), ldg, P(xin), xin.stride(0), B, l.n_out, l.n_in, None, 0,
+                      None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
         if wg is not None:
