@@ -191,3 +191,24 @@ def table_array(descs):
     for i, d in enumerate(descs):
         arr[i] = d
     return arr
+
+
+class capture_guard:
+    """Around a CUDA-graph capture: collect garbage first and keep the cyclic
+    collector off while capturing.  A model and its cached step engine
+    reference each other, so dead engines (and their CUDA graphs) are freed
+    by the cyclic GC — which may otherwise run in the middle of a capture,
+    where destroying a graph is an illegal operation that invalidates it."""
+
+    def __enter__(self):
+        import gc
+        gc.collect()
+        self._was = gc.isenabled()
+        gc.disable()
+        return self
+
+    def __exit__(self, *exc):
+        import gc
+        if self._was:
+            gc.enable()
+        return False

@@ -565,7 +565,7 @@ class HybridTrainer:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         try:
-            with torch.cuda.graph(g):
+            with _lib.capture_guard(), torch.cuda.graph(g):
                 self._issue()
         except Exception:
             self.graph = None

@@ -544,7 +544,7 @@ class StepEngine:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
-        with torch.cuda.graph(g):
+        with _lib.capture_guard(), torch.cuda.graph(g):
             self.launch()
         self.launches_per_step = _lib.launch_count() - n0
         self.graph = g
@@ -572,7 +572,7 @@ class StepEngine:
         try:
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            with _lib.capture_guard(), torch.cuda.graph(graph):
                 self.launch(mark=mark)
                 mark("end")
         except Exception:
@@ -680,7 +680,7 @@ class StepEngine:
         if self._eval_runs >= 1:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with _lib.capture_guard(), torch.cuda.graph(g):
                 self.launch_eval()
             self.eval_graphs[self._set] = g
             g.replay()
