@@ -147,11 +147,16 @@ def cpu_port_rate(c, batch, steps, warmup, seed=0):
     """samples/s of the float64 reference algorithm on this host."""
     from oracle import port
     from paper_1906_00091_b200.rng import RandomBatchSource
+    # all host threads, also under torchrun (which sets OMP_NUM_THREADS=1 per
+    # rank; only rank 0 runs the reference arm)
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    limiter = None
     try:
-        from threadpoolctl import threadpool_info
+        from threadpoolctl import threadpool_info, threadpool_limits
+        limiter = threadpool_limits(limits=ncpu)
         threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
     except Exception:
-        threads = os.cpu_count()
+        threads = ncpu
     # tables capped at 2^20 rows per table for host memory (per-sample compute
     # does not depend on the row count); the cap is reported in `sample`
     cap = 1 << 20
@@ -165,6 +170,8 @@ def cpu_port_rate(c, batch, steps, warmup, seed=0):
     for hb in hbs[warmup:]:
         port.train_step(model, hb.dense, hb.offsets, hb.indices, hb.labels, 0.1)
     dt = time.perf_counter() - t0
+    if limiter is not None:
+        limiter.restore_original_limits()
     sample = (f"oracle/port.py float64 train_step (reference algorithm), batch "
               f"{batch} of the {c['batch']}-sample workload, {steps} timed steps "
               f"after {warmup} warm-up, tables capped at {cap} rows")
