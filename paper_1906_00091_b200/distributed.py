@@ -256,6 +256,7 @@ class RankEngine:
             os.environ.get("DLRM_HEAD_FUSED", "1") != "0"
         self.lin_ws_bytes = lin
         self.lin_ws = torch.empty(lin, dtype=torch.uint8, device=dev)
+        self.lin_ws2 = torch.empty(lin, dtype=torch.uint8, device=dev)  # main-stream wgrad
         self.stats = torch.zeros(3, **f32)
         self.err_pos = torch.empty(max(To, 1), dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -468,9 +469,16 @@ class RankEngine:
                      l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), Bl, l.n_out, l.n_in, s)
             gw, gb = self.gslots[i]
-            self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
-                        Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                        0.0, None, P(self.lin_ws), self.lin_ws_bytes)
+            if i == 0 and wgrad_stream is not None:
+                # the first layer's weight gradient on the (then idle) calling
+                # stream, beside the weight-gradient stream (own workspace)
+                call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
+                     Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                     0.0, None, P(self.lin_ws2), self.lin_ws_bytes, s)
+            else:
+                self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
+                            Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
+                            0.0, None, P(self.lin_ws), self.lin_ws_bytes)
 
     def publish_error(self):
         """stats[2] <- this rank's error flag (allreduced with the loss)."""
