@@ -204,6 +204,10 @@ def run_reference(args, c, rank, world):
 # by row bytes) — the access pattern of the pooled lookup.  See
 # profiles/round1/gather_ceiling.txt.
 GATHER_CEILING = {64: 1610.0, 128: 3201.0, 256: 4223.0, 512: 4981.0}
+# Read-modify-write of ~787k distinct random 256-byte rows of an 8M-row table
+# (scripts/gather_rmw.cu, both directions counted; profiles/round1/gather_rmw.txt)
+# — the sparse apply's access pattern.
+RMW_CEILING = {256: 5008.0}
 # Dense kind::tf32 tcgen05 MMA peak of this part, chip-wide (128x256x8 MMAs,
 # profiles/round1/mma_rate.txt); MEASURED_PEAKS.json has bf16 only.
 MEASURED_TF32 = 1093.0
@@ -475,6 +479,9 @@ def run_ours(args, c, rank, world, dist):
                 "peak_kind": pk_kind + " copy bandwidth (MEASURED_PEAKS.json)",
                 "algorithmic_bytes_per_launch": kb, "ms_per_launch": kms,
                 "random_row_gather_ceiling_gbs": GATHER_CEILING.get(4 * c["d"])}
+    if dom == "embedding_bwd_apply" and 4 * c["d"] in RMW_CEILING:
+        # the apply reads AND writes its rows: its own measured ceiling
+        roofline["random_row_rmw_ceiling_gbs"] = RMW_CEILING[4 * c["d"]]
     tf = flops / (stages["mlp_total"] / 1e3) / 1e12
     mlp_roof = {"bound": "tensor", "achieved": tf, "unit": "TFLOP/s",
                 "peak": pk["bf16_tflops"], "frac": tf / pk["bf16_tflops"],
