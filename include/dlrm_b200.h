@@ -76,6 +76,13 @@ typedef struct {
 int dlrm_err_reset(int64_t* err_pos, int32_t nt, int32_t* err_flag,
                    dlrm_stream_t stream);
 
+/* err_val[t] = tables[t].indices[err_pos[t]] when *err_flag is set and
+ * table t has a recorded position, else 0: the offending index VALUE for
+ * LookupIndexError (ref embedding.py:117-124), read on the device from the
+ * batch that ran.  Launch it after the kernels that record errors. */
+int dlrm_err_resolve(const dlrm_table_desc* tables, int32_t nt, const int64_t* err_pos,
+                     const int32_t* err_flag, int64_t* err_val, dlrm_stream_t stream);
+
 /* Pooled lookup S = A^T W for nt tables (ref lookup_batch,
  * embedding.py:155-179): out[out_offset_t + j*out_stride + c] =
  * strict ascending-position fold over bag j of W[row_base+idx]*a.  Empty bags

@@ -42,6 +42,7 @@ class Features(C.Structure):
 
 _SIGS = {
     "dlrm_err_reset": [_vp, _i32, _vp, _vp],
+    "dlrm_err_resolve": [_vp, _i32, _vp, _vp, _vp, _vp],
     "dlrm_emb_fwd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _vp, _vp, _vp],
     "dlrm_emb_bwd_sgd": [_vp, _i64, _vp, _i32, _i64, _vp, _i64, _f32, _vp,
                          _i64, _vp, _sz, _vp],

@@ -123,14 +123,10 @@ def _engine_adagrad_views(engine):
 
 
 def _adagrad_views(opt, model):
-    """name -> accumulator tensor for an optim.Adagrad (lazily created state)
-    or a StepEngine built with optimizer="adagrad".  ``train_step`` keeps the
-    live accumulators in the model's step engine: when it has one, those are
-    the optimiser's state."""
-    if not hasattr(opt, "params_acc"):
-        eng = getattr(model, "_engine", None)
-        if eng is not None and getattr(eng, "optimizer", None) == "adagrad":
-            opt = eng
+    """name -> accumulator tensor for an optim.Adagrad or a StepEngine built
+    with optimizer="adagrad".  An Adagrad that drives a ``train_step`` engine
+    holds views of that engine's live accumulators (parallel._mirror_adagrad),
+    so its state is always the one to read or write."""
     if hasattr(opt, "params_acc"):
         if getattr(opt, "optimizer", None) != "adagrad":
             raise ValueError("engine was not built with Adagrad")
@@ -214,8 +210,7 @@ def restore_adagrad(opt, model, state: dict) -> None:
     the next ``train_step`` engine starts from it) or an Adagrad
     ``StepEngine``."""
     import torch
-    if not hasattr(opt, "params_acc") and getattr(getattr(model, "_engine", None),
-                                                  "optimizer", None) != "adagrad":
+    if not hasattr(opt, "params_acc"):
         from .optim import AdagradState
         for name, mlp in (("bottom", model.bottom), ("top", model.top)):
             if name not in opt._mlp_state:

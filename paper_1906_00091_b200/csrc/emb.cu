@@ -986,6 +986,21 @@ __global__ void err_reset_kernel(int64_t* err_pos, int32_t nt, int32_t* err_flag
   if (i == 0 && err_flag) *err_flag = 0;
 }
 
+// The offending index VALUE of each table's first bad position, read on the
+// device from the batch that ran (the host's copy of the indices may already
+// hold the next batch when the step was pipelined).
+__global__ void err_resolve_kernel(TableSet ts, const int64_t* __restrict__ err_pos,
+                                   const int32_t* __restrict__ err_flag,
+                                   int64_t* __restrict__ err_val) {
+  pdl_entry();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ts.nt) return;
+  const int64_t p = err_pos[t];
+  int64_t v = 0;
+  if (*err_flag && p != INT64_MAX && p >= 0 && p < ts.t[t].capacity) v = ts.t[t].indices[p];
+  err_val[t] = v;
+}
+
 template <int VEC>
 __global__ void sgd_rows_kernel(float* __restrict__ W, int64_t dim,
                                 const int64_t* __restrict__ rows,
@@ -1414,6 +1429,17 @@ extern "C" int dlrm_err_reset(int64_t* err_pos, int32_t nt, int32_t* err_flag,
   launch(err_reset_kernel, unsigned(ceil_div(nt > 0 ? nt : 1, 128)), 128, 0,
                      as_stream(stream), err_pos, nt, err_flag);
   return check_launch("err_reset_kernel");
+}
+
+extern "C" int dlrm_err_resolve(const dlrm_table_desc* tables, int32_t nt,
+                                const int64_t* err_pos, const int32_t* err_flag,
+                                int64_t* err_val, dlrm_stream_t stream) {
+  DLRM_REQUIRE(err_pos && err_flag && err_val, "bad error buffers");
+  static thread_local TableSet ts;
+  if (int rc = fill_tableset(ts, tables, nt)) return rc;
+  launch(err_resolve_kernel, unsigned(ceil_div(nt, 128)), 128, 0, as_stream(stream), ts,
+         err_pos, err_flag, err_val);
+  return check_launch("err_resolve_kernel");
 }
 
 extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,

@@ -352,7 +352,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   uint8_t* epi = ring + PTILE_BYTES;                   // epilogue scratch
 
-  pdl_trigger();  // prologue below touches no data of the previous kernel
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
   const int kt0 = blockIdx.z * args.k_tiles_per_split;
@@ -384,6 +383,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // Dependents are released only once this CTA HOLDS its TMEM: a PDL-launched
+  // successor that allocates TMEM and then spins in griddepcontrol.wait can
+  // therefore never keep a CTA of this grid (or, through it, a cluster
+  // sibling on another stream) from allocating.  The prologue above touches
+  // no data of the previous kernel.
+  pdl_trigger();
   pdl_wait();  // operands / epilogue inputs come from earlier kernels
 
   if (warp == 0) {

@@ -159,8 +159,9 @@ class RankEngine:
 
     def __init__(self, model: DlrmModel, layout: ExchangeLayout,
                  capacities=None, lr: float = 0.1, optimizer: str = "sgd",
-                 eps: float = 1e-10):
+                 eps: float = 1e-10, weighted: bool = False):
         _lib.require_cuda()
+        self.weighted = bool(weighted)
         cfg = model.config
         self.model, self.cfg, self.L = model, cfg, layout
         self.lr = float(lr)
@@ -208,14 +209,17 @@ class RankEngine:
         self.caps = [max(1, int(c)) for c in caps]
         self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
 
-        # inputs: ONE contiguous block [x | labels | offsets | indices] so a
+        # inputs: ONE contiguous block [x | labels | offsets | indices
+        # (| per-index weights)] so a
         # step's inputs move with one copy (pack() builds the same layout in
         # pinned host memory); x / labels / offsets / indices are views
         a16 = lambda n: (n + 15) // 16 * 16
         lay, o = {}, 0
         for name, nbytes in (("x", Bl * ceil4(cfg.dense_dim) * 4), ("labels", Bl * 4),
                              ("offsets", max(To, 1) * (Bg + 1) * 8),
-                             ("indices", max(int(self.cap_base[-1]), 1) * 8)):
+                             ("indices", max(int(self.cap_base[-1]), 1) * 8),
+                             ("iweights", max(int(self.cap_base[-1]), 1) * 4
+                              if self.weighted else 0)):
             lay[name] = (o, nbytes)
             o = a16(o + nbytes)
         self.block_layout, self.block_bytes = lay, o
@@ -223,6 +227,9 @@ class RankEngine:
         v = self._views(self.block)
         self.x, self.labels = v["x"], v["labels"]
         self.offsets, self.indices = v["offsets"], v["indices"]
+        self.iweights = v["iweights"]
+        if self.iweights is not None:
+            self.iweights.fill_(1.0)
 
         # exchange buffers
         self.send = torch.zeros(max(layout.send_numel, 1), **f32)
@@ -260,6 +267,7 @@ class RankEngine:
         self.stats = torch.zeros(3, **f32)
         self.err_pos = torch.empty(max(To, 1), dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.err_val = torch.zeros(max(To, 1), dtype=torch.int64, device=dev)
         # update rule (SGD / Adagrad with same-layout accumulators)
         from .optim import update_rule
         self.optimizer = optimizer
@@ -279,7 +287,8 @@ class RankEngine:
         To = len(self.own)
         descs = [_lib.TableDesc(
             self.offsets[j].data_ptr(), self.indices.data_ptr() + 8 * int(self.cap_base[j]),
-            None, int(self.row_base[j]), self.model.tables[t].num_rows, j * d,
+            (self.iweights.data_ptr() + 4 * int(self.cap_base[j])) if self.weighted else None,
+            int(self.row_base[j]), self.model.tables[t].num_rows, j * d,
             self.caps[j], self.model.tables[t].table_id) for j, t in enumerate(self.own)]
         self._descs = _lib.table_array(descs) if descs else None
         feats = [(self.bact[-1].data_ptr(), self.bact[-1].stride(0))]
@@ -297,15 +306,25 @@ class RankEngine:
 
         def view(name, dtype, shape):
             o, n = lay[name]
+            if n == 0:
+                return None
             return blk[o:o + n].view(dtype).view(*shape)
         return {"x": view("x", torch.float32, (self.Bl, ceil4(self.cfg.dense_dim))),
                 "labels": view("labels", torch.float32, (self.Bl,)),
                 "offsets": view("offsets", torch.int64, (To, self.Bg + 1)),
-                "indices": view("indices", torch.int64, (max(int(self.cap_base[-1]), 1),))}
+                "indices": view("indices", torch.int64, (max(int(self.cap_base[-1]), 1),)),
+                "iweights": view("iweights", torch.float32, (max(int(self.cap_base[-1]), 1),))}
 
-    def pack(self, dense_local, labels_local, offsets_owned, indices_owned):
+    def _check_weights(self, weights_owned):
+        if weights_owned is not None and any(w is not None for w in weights_owned) \
+                and not self.weighted:
+            raise ValueError("weighted bags need a RankEngine built with weighted=True")
+
+    def pack(self, dense_local, labels_local, offsets_owned, indices_owned,
+             weights_owned=None):
         """This rank's batch in the input-block layout, in pinned host memory
         (done once per batch by the data pipeline)."""
+        self._check_weights(weights_owned)
         blk = torch.zeros(self.block_bytes, dtype=torch.uint8).pin_memory()
         v = self._views(blk)
         v["x"][:, :self.cfg.dense_dim].copy_(torch.as_tensor(np.asarray(dense_local, np.float32)))
@@ -318,7 +337,11 @@ class RankEngine:
             v["offsets"][j].copy_(torch.as_tensor(np.asarray(offsets_owned[j], np.int64)))
             cb = int(self.cap_base[j])
             v["indices"][cb:cb + i.size].copy_(torch.as_tensor(i))
-        self._host_indices = indices_owned
+            if self.weighted:
+                w = None if weights_owned is None else weights_owned[j]
+                v["iweights"][cb:cb + i.size].copy_(
+                    torch.ones(i.size) if w is None
+                    else torch.as_tensor(np.asarray(w, np.float32)))
         return blk
 
     def stage(self, packed: torch.Tensor):
@@ -326,9 +349,11 @@ class RankEngine:
         self.block.copy_(packed, non_blocking=True)
 
     # ------------------------------------------------------------------
-    def load(self, dense_local, labels_local, offsets_owned, indices_owned):
-        """dense/labels: this rank's shard; offsets/indices: one global-batch
-        bag set per OWNED table (host arrays or device tensors)."""
+    def load(self, dense_local, labels_local, offsets_owned, indices_owned,
+             weights_owned=None):
+        """dense/labels: this rank's shard; offsets/indices (/ weights): one
+        global-batch bag set per OWNED table (host arrays or device tensors)."""
+        self._check_weights(weights_owned)
         # copy_ straight from the source: pinned host tensors move with an
         # async H2D copy on the current stream (no host synchronisation)
         def src(a, dtype):
@@ -346,7 +371,12 @@ class RankEngine:
             self.offsets[j].copy_(src(offsets_owned[j], torch.int64), non_blocking=True)
             cb = int(self.cap_base[j])
             self.indices[cb:cb + n].copy_(src(i, torch.int64), non_blocking=True)
-        self._host_indices = indices_owned
+            if self.weighted:
+                w = None if weights_owned is None else weights_owned[j]
+                if w is None:
+                    self.iweights[cb:cb + n].fill_(1.0)
+                else:
+                    self.iweights[cb:cb + n].copy_(src(w, torch.float32), non_blocking=True)
 
     # ------------------------------------------------------------------
     def phase_a(self, stream=None):
@@ -494,9 +524,14 @@ class RankEngine:
         the trainer runs it on a side stream under the dense work."""
         To = len(self.own)
         if To:
+            sh = _lib.stream_handle(stream)
             _lib.call("dlrm_emb_bwd_prepare", self.d, C.cast(self._descs, C.c_void_p), To,
-                      self.Bg, self.total_rows, _lib.ptr(self.emb_ws), self.emb_ws_bytes,
-                      _lib.stream_handle(stream))
+                      self.Bg, self.total_rows, _lib.ptr(self.emb_ws), self.emb_ws_bytes, sh)
+            # the keys pass records every bad position: resolve the offending
+            # values on the device, from the batch that ran
+            _lib.call("dlrm_err_resolve", C.cast(self._descs, C.c_void_p), To,
+                      _lib.ptr(self.err_pos), _lib.ptr(self.err_flag),
+                      _lib.ptr(self.err_val), sh)
 
     def apply_sparse(self, stream=None):
         """Owned tables: segmented fold of the received gradients + row SGD
@@ -528,13 +563,11 @@ class RankEngine:
         if not int(self.err_flag.item()):
             return None
         pos = self.err_pos.cpu().numpy()
+        val = self.err_val.cpu().numpy()
         for j, t in enumerate(self.own):
             if pos[j] != INT64_MAX:
-                k = int(pos[j])
-                idx = self._host_indices[j]
-                val = int(idx[k].item() if isinstance(idx, torch.Tensor) else idx[k])
                 tab = self.model.tables[t]
-                return tab.table_id, k, val, tab.num_rows
+                return tab.table_id, int(pos[j]), int(val[j]), tab.num_rows
         return None
 
 
@@ -545,9 +578,10 @@ class HybridTrainer:
 
     def __init__(self, model: DlrmModel, plan: DevicePlan, rank: int,
                  capacities=None, lr: float = 0.1, group=None, ar_group=None,
-                 optimizer: str = "sgd", eps: float = 1e-10):
+                 optimizer: str = "sgd", eps: float = 1e-10, weighted: bool = False):
         self.layout = ExchangeLayout(plan, rank, model.config.sparse_dim)
-        self.engine = RankEngine(model, self.layout, capacities, lr, optimizer, eps)
+        self.engine = RankEngine(model, self.layout, capacities, lr, optimizer, eps,
+                                 weighted)
         self.ex = NcclExchange(self.layout, group, ar_group)
         self.rank = rank
         self.comm_stream = torch.cuda.Stream()

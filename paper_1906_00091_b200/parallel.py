@@ -12,6 +12,7 @@
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -208,37 +209,95 @@ def _engine_for(model: DlrmModel, batch: int, batches, optimizer,
             and eng.optimizer == kind and (kind != "adagrad" or eng.eps == eps)
             and eng.weighted == weighted
             and all(n <= c for n, c in zip(nnz, eng.caps))):
+        if isinstance(optimizer, _EngineSpec):
+            return eng
+        _bind_optimizer(eng, optimizer, model)
         return eng
     caps = [max(n, batch) for n in nnz]
     if eng is not None:  # grow geometrically so graphs are rarely rebuilt
         caps = [max(c, int(1.25 * old)) for c, old in zip(caps, eng.caps)]
-    if eng is not None and kind == "adagrad" and eng.optimizer == "adagrad":
-        # a rebuilt engine keeps the Adagrad accumulators
-        acc_p, acc_w = eng.params_acc, eng.W_acc
-    else:
-        acc_p = acc_w = None
+    old_owner = getattr(eng, "opt_owner", None) if eng is not None else None
+    old_owner = old_owner() if old_owner is not None else None
     eng = StepEngine(model, batch, caps, lr=optimizer.lr, weighted=weighted,
                      optimizer=kind, eps=eps)
-    if acc_p is not None:
-        eng.params_acc.copy_(acc_p)
-        eng.W_acc.copy_(acc_w)
-    elif kind == "adagrad" and (getattr(optimizer, "_mlp_state", None)
-                                or getattr(optimizer, "_table_state", None)):
-        # accumulators restored into the optimiser (checkpoint.restore_adagrad)
-        from .checkpoint import _engine_adagrad_views
-        views = _engine_adagrad_views(eng)
-        for name in ("bottom", "top"):
-            st = optimizer._mlp_state.get(name)
-            for l, (aw, ab) in enumerate(zip(st.mlp_weights, st.mlp_biases) if st else []):
-                views[f"{name}_w_{l}"].copy_(aw)
-                views[f"{name}_b_{l}"].copy_(ab)
-        for t, table in enumerate(model.tables):
-            acc = optimizer._table_state.get(table.table_id)
-            if acc is not None:
-                views[f"table_{t}"].copy_(acc)
+    # Adagrad: the optimiser's state (views of the previous engine's
+    # accumulators when it drove that engine, restored arrays, or nothing)
+    # seeds the new engine; another optimiser that drove the old engine keeps
+    # a private copy.  Evaluation (_EngineSpec) carries the current owner over.
+    src = None
+    if kind == "adagrad":
+        src = old_owner if isinstance(optimizer, _EngineSpec) else optimizer
+        if old_owner is not None and old_owner is not src:
+            _detach_adagrad(old_owner)
+        if src is not None:
+            _load_adagrad(eng, src, model)
     eng.eager_runs = 0
     model._engine = eng
+    if src is not None:
+        eng.opt_owner = weakref.ref(src)
+        _mirror_adagrad(eng, src, model)
     return eng
+
+
+def _detach_adagrad(opt):
+    """Give an optimiser that no longer drives the step engine its own
+    copies of the accumulators it was viewing."""
+    from .optim import AdagradState
+    opt._mlp_state = {k: AdagradState([a.clone() for a in st.mlp_weights],
+                                      [a.clone() for a in st.mlp_biases])
+                      for k, st in opt._mlp_state.items()}
+    opt._table_state = {k: a.clone() for k, a in opt._table_state.items()}
+
+
+def _load_adagrad(eng, opt, model):
+    """Engine accumulators <- the optimiser's state (zero where it has none:
+    a fresh Adagrad starts from zero sums, ref optim.py:112-140)."""
+    from .checkpoint import _engine_adagrad_views
+    eng.params_acc.zero_()
+    eng.W_acc.zero_()
+    views = _engine_adagrad_views(eng)
+    for name in ("bottom", "top"):
+        st = opt._mlp_state.get(name)
+        for l, (aw, ab) in enumerate(zip(st.mlp_weights, st.mlp_biases) if st else []):
+            views[f"{name}_w_{l}"].copy_(aw)
+            views[f"{name}_b_{l}"].copy_(ab)
+    for t, table in enumerate(model.tables):
+        acc = opt._table_state.get(table.table_id)
+        if acc is not None:
+            views[f"table_{t}"].copy_(acc)
+
+
+def _mirror_adagrad(eng, opt, model):
+    """The optimiser's state becomes views of the engine's live accumulators
+    (so checkpointing or a manual ``opt.apply`` sees what the fused step
+    updated)."""
+    from .checkpoint import _engine_adagrad_views
+    from .optim import AdagradState
+    views = _engine_adagrad_views(eng)
+    for name, layers in (("bottom", model.bottom.layers), ("top", model.top.layers)):
+        opt._mlp_state[name] = AdagradState(
+            [views[f"{name}_w_{l}"] for l in range(len(layers))],
+            [views[f"{name}_b_{l}"] for l in range(len(layers))])
+    for t, table in enumerate(model.tables):
+        opt._table_state[table.table_id] = views[f"table_{t}"]
+
+
+def _bind_optimizer(eng, optimizer, model):
+    """Adagrad accumulators belong to the optimiser OBJECT (as in the
+    reference): when another Adagrad instance drives a cached engine, the
+    previous one keeps a private copy and the engine loads the new one's
+    state."""
+    if optimizer.name != "adagrad":
+        return
+    ref = getattr(eng, "opt_owner", None)
+    cur = ref() if ref is not None else None
+    if cur is optimizer:
+        return
+    if cur is not None:
+        _detach_adagrad(cur)
+    _load_adagrad(eng, optimizer, model)
+    eng.opt_owner = weakref.ref(optimizer)
+    _mirror_adagrad(eng, optimizer, model)
 
 
 def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
@@ -337,7 +396,7 @@ class ParallelTrainer:
     def __init__(self, model: DlrmModel, plan: DevicePlan,
                  optimizer_name: str = "sgd", lr: float = 0.1,
                  eps: float = 1e-10, concurrent: bool = False,
-                 capacities=None):
+                 capacities=None, weighted: bool = False):
         from .distributed import ExchangeLayout, LocalExchange, RankEngine
         if optimizer_name not in ("sgd", "adagrad"):
             raise ValueError(f"unknown optimizer: {optimizer_name!r}")
@@ -349,18 +408,33 @@ class ParallelTrainer:
         G = plan.num_devices
         self.layouts = [ExchangeLayout(plan, r, model.config.sparse_dim)
                         for r in range(G)]
+        self._spec = (optimizer_name, lr, eps, capacities)
         self.engines = []
         for r in range(G):
             replica = DlrmModel(model.config, model.bottom.copy(),
                                 model.top.copy(), self.tables)
-            own = self.layouts[r].owned[r]
-            caps = None if capacities is None else [capacities[t] for t in own]
-            self.engines.append(RankEngine(replica, self.layouts[r], caps, lr,
-                                           optimizer_name, eps))
+            self.engines.append(self._rank_engine(replica, r, weighted))
         self.ex = LocalExchange(self.layouts)
         self.comm = CommLog()
         self.step_count = 0
         self.concurrent = concurrent
+
+    def _rank_engine(self, replica, r, weighted):
+        from .distributed import RankEngine
+        optimizer_name, lr, eps, capacities = self._spec
+        own = self.layouts[r].owned[r]
+        caps = None if capacities is None else [capacities[t] for t in own]
+        return RankEngine(replica, self.layouts[r], caps, lr, optimizer_name, eps, weighted)
+
+    def _rebuild(self, weighted):
+        """New rank engines (other input layout) around the current replica
+        parameters, tables and optimiser state."""
+        old = self.engines
+        self.engines = [self._rank_engine(e.model, r, weighted) for r, e in enumerate(old)]
+        if self._spec[0] == "adagrad":
+            for e, o in zip(self.engines, old):
+                e.params_acc.copy_(o.params_acc)
+                e.W_acc.copy_(o.W_acc)
 
     def close(self):
         pass
@@ -381,12 +455,18 @@ class ParallelTrainer:
             raise ValueError(f"batch size {n_total} does not match plan "
                              f"({plan.batch_size})")
         G, step = plan.num_devices, self.step_count
+        weighted = any(sb.weights is not None for sb in batches)
+        if weighted and not self.engines[0].weighted:
+            # per-index weights need the weighted input layout: rebuild the
+            # rank engines around the current parameters once
+            self._rebuild(weighted=True)
         for r, e in enumerate(self.engines):
             lo, hi = plan.shard(r)
             own = self.layouts[r].owned[r]
             e.load(dense_x[lo:hi], labels[lo:hi],
                    [batches[t].offsets for t in own],
-                   [batches[t].indices for t in own])
+                   [batches[t].indices for t in own],
+                   [batches[t].weights for t in own] if weighted else None)
         for e in self.engines:
             e.phase_a()
         self.ex.forward_all([e.send for e in self.engines],

@@ -188,6 +188,9 @@ class StepEngine:
         self.stats = torch.zeros(2, **f32)
         self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
         self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # the offending index value per table, resolved on the device from the
+        # batch that ran (dlrm_err_resolve)
+        self.err_val = torch.zeros(T, dtype=torch.int64, device=dev)
         # update rule fused into the step's kernels (ref optim.py): SGD, or
         # Adagrad with accumulators laid out exactly like the parameters
         from .optim import update_rule
@@ -287,7 +290,6 @@ class StepEngine:
                 w = np.ones(i.size, np.float32) if weights is None or weights[t] is None \
                     else np.asarray(weights[t], np.float32)
                 v["iweights"][cb:cb + i.size].copy_(torch.as_tensor(w))
-        self._host_indices = indices
         return blk
 
     def stage(self, packed: torch.Tensor, k: int = 0, stream=None):
@@ -337,7 +339,6 @@ class StepEngine:
                         self.iweights[cb:cb + n].copy_(
                             _to_dev_f32(w, self.dev), non_blocking=True)
             self.labels.copy_(_to_dev_f32(labels, self.dev), non_blocking=True)
-        self._host_indices = indices
 
     # ------------------------------------------------------------------
     STAGES = ("bottom_mlp_fwd", "embedding_fwd", "interaction_fwd",
@@ -357,8 +358,12 @@ class StepEngine:
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
+            sh = _lib.stream_handle(self.side)
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
-                 P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(self.side))
+                 P(self.emb_ws), self.emb_ws_bytes, sh)
+            # the keys pass records every bad position: resolve the values
+            # here, off the critical path
+            self._resolve(sh)
             done = torch.cuda.Event()
             done.record(self.side)
             return done
@@ -530,6 +535,7 @@ class StepEngine:
         if prep_done is None:
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
                  P(self.emb_ws), self.emb_ws_bytes, s)
+            self._resolve(s)
         else:
             main.wait_event(prep_done)
         call("dlrm_emb_bwd_apply", P(self.W_all), d, self._descs_p, self.T, B,
@@ -655,6 +661,7 @@ class StepEngine:
             a, lda = out, ldo
         call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
              P(self.Z), nf * d, P(self.err_pos), ef, s)
+        self._resolve(s)
         call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
              self.R.stride(0), self.R.shape[1], s)
         a, lda = self.R, self.R.stride(0)
@@ -704,17 +711,19 @@ class StepEngine:
             self.launches_per_step = _lib.launch_count() - n0
 
     # ------------------------------------------------------------------
+    def _resolve(self, stream_handle):
+        _lib.call("dlrm_err_resolve", self._descs_p, self.T, _lib.ptr(self.err_pos),
+                  _lib.ptr(self.err_flag), _lib.ptr(self.err_val), stream_handle)
+
     def check_errors(self):
         if int(self.err_flag.item()):
             pos = self.err_pos.cpu().numpy()
+            val = self.err_val.cpu().numpy()
             for t in range(self.T):
                 if pos[t] != INT64_MAX:
-                    k = int(pos[t])
-                    idx = self._host_indices[t]
-                    val = int(idx[k].item() if isinstance(idx, torch.Tensor)
-                              else idx[k])
                     tab = self.model.tables[t]
-                    raise LookupIndexError(tab.table_id, k, val, tab.num_rows)
+                    raise LookupIndexError(tab.table_id, int(pos[t]), int(val[t]),
+                                           tab.num_rows)
 
     def result(self) -> StepResult:
         self.check_errors()

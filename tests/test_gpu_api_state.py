@@ -1,0 +1,183 @@
+"""Engine state that must follow the batch / optimiser it belongs to.
+
+* LookupIndexError's ``index`` comes from the batch that RAN, read on the
+  device (dlrm_err_resolve) — not from whatever batch the host packed last
+  (ref embedding.py:117-124: the payload is the offending value itself).
+* Weighted bags through the hybrid-parallel step (ref ParallelTrainer calls
+  lookup_batch / lookup_backward, which apply SparseBatch.weights,
+  parallel.py:363-506, embedding.py:155-210).
+* Adagrad accumulators belong to the optimiser OBJECT (ref optim.py:112-140:
+  ``Adagrad`` keeps ``_mlp_state`` / ``_table_state`` per instance), also
+  when train_step's cached engine is reused.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1906_00091_b200 import (Adagrad, DlrmConfig, LookupIndexError,
+                                   ParallelTrainer, Sgd, SparseBatch, init_model,
+                                   make_plan, train_step)
+from paper_1906_00091_b200.trainer import StepEngine
+from tests._util import rel_err, traj_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def build(c):
+    return init_model(DlrmConfig(c["tables"], c["d"], c["bot"], c["top"], seed=c["seed"]))
+
+
+def arrays(bottom, top, tables):
+    out = []
+    for l in bottom.layers + top.layers:
+        out += [l.weight.detach().cpu().double().numpy(),
+                l.bias.detach().cpu().double().numpy()]
+    return out + [t.weights.detach().cpu().double().numpy() for t in tables]
+
+
+def test_pipelined_error_reports_the_batch_that_ran(golden):
+    """Pack-ahead: batch A (bad index) staged into input set 0, batch B
+    (another bad value at the same position) packed and staged into set 1
+    AFTER it; running set 0 must report A's value."""
+    fx = golden("traj_c1s.npz")
+    c, batches = traj_inputs(fx)
+    model = build(c)
+    caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
+    eng = StepEngine(model, c["batch"], caps, lr=0.1, input_sets=2)
+    ha, hb = batches[0], batches[1]
+    ia = [i.copy() for i in ha.indices]
+    ib = [i.copy() for i in hb.indices]
+    ia[3][17] = c["tables"][3] + 5
+    ib[3][17] = c["tables"][3] + 999
+    pa = eng.pack_host_batch(ha.dense, ha.offsets, ia, ha.labels)
+    pb = eng.pack_host_batch(hb.dense, hb.offsets, ib, hb.labels)
+    eng.stage(pa, 0)
+    eng.stage(pb, 1)
+    before = arrays(model.bottom, model.top, model.tables)
+    eng.use_set(0)
+    eng.run()
+    with pytest.raises(LookupIndexError) as e:
+        eng.check_errors()
+    assert (e.value.table_id, e.value.position, e.value.index) == (3, 17, c["tables"][3] + 5)
+    eng.use_set(1)
+    eng.run()
+    with pytest.raises(LookupIndexError) as e:
+        eng.check_errors()
+    assert e.value.index == c["tables"][3] + 999
+    # neither failing step mutated anything
+    for x, y in zip(before, arrays(model.bottom, model.top, model.tables)):
+        assert np.array_equal(x, y)
+
+
+def test_pipelined_error_graph_replay(golden):
+    """Same through captured graphs (one per input set)."""
+    fx = golden("traj_c1s.npz")
+    c, batches = traj_inputs(fx)
+    model = build(c)
+    caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
+    eng = StepEngine(model, c["batch"], caps, lr=0.1, input_sets=2)
+    good = [eng.pack_host_batch(h.dense, h.offsets, h.indices, h.labels) for h in batches[:2]]
+    for k in range(2):
+        eng.use_set(k)
+        eng.stage(good[k], k)
+        eng.run()
+        eng.capture()
+    ha = batches[2]
+    ia = [i.copy() for i in ha.indices]
+    ia[0][3] = -7
+    eng.stage(eng.pack_host_batch(ha.dense, ha.offsets, ia, ha.labels), 0)
+    eng.stage(good[1], 1)
+    eng.use_set(0)
+    eng.run()
+    with pytest.raises(LookupIndexError) as e:
+        eng.check_errors()
+    assert (e.value.table_id, e.value.position, e.value.index) == (0, 3, -7)
+    eng.use_set(1)
+    eng.run()
+    eng.check_errors()   # the good batch clears the error records
+
+
+def _weighted(batches, seed=5):
+    rng = np.random.default_rng(seed)
+    out = []
+    for hb in batches:
+        out.append([SparseBatch(o, i, rng.uniform(0.25, 2.0, len(i)))
+                    for o, i in zip(hb.offsets, hb.indices)])
+    return out
+
+
+def test_parallel_trainer_applies_bag_weights(golden):
+    """ParallelTrainer with weighted bags: G = 1 bitwise equal to the fused
+    weighted train_step; G = 2 within the north-star tolerance of it."""
+    fx = golden("traj_c1s.npz")
+    c, batches = traj_inputs(fx)
+    sparse = _weighted(batches)
+    ref = build(c)
+    opt = Sgd(c["lr"])
+    ref_loss = [train_step(ref, hb.dense.astype(np.float32), sp, hb.labels, opt).loss
+                for hb, sp in zip(batches, sparse)]
+    ref_arr = arrays(ref.bottom, ref.top, ref.tables)
+    for G in (1, 2):
+        m = build(c)
+        caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
+        tr = ParallelTrainer(m, make_plan(m.config, c["batch"], G), "sgd", c["lr"],
+                             capacities=caps)
+        loss = [tr.step(hb.dense.astype(np.float32), sp, hb.labels.astype(np.float32)).loss
+                for hb, sp in zip(batches, sparse)]
+        b, t = tr.replica_params(0)
+        got = arrays(b, t, tr.tables)
+        if G == 1:
+            assert loss == ref_loss
+            for x, y in zip(got, ref_arr):
+                assert np.array_equal(x, y)
+        else:
+            for a, r in zip(loss, ref_loss):
+                assert abs(a - r) <= 1e-4 * abs(r)
+            for i, (x, y) in enumerate(zip(got, ref_arr)):
+                assert rel_err(x, y, floor=1e-2) < 1e-4, i
+    # weights actually matter: the unweighted run differs
+    m = build(c)
+    plain = [train_step(m, hb.dense.astype(np.float32),
+                        [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)],
+                        hb.labels, Sgd(c["lr"])).loss for hb in batches]
+    assert plain != ref_loss
+
+
+def test_adagrad_state_belongs_to_the_optimizer(golden):
+    fx = golden("traj_c1a.npz")
+    c, batches = traj_inputs(fx)
+    lr, eps = c["lr"], c["eps"]
+
+    def sp(hb):
+        return [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)]
+
+    # model 1: two steps with optimiser A, then one with a FRESH optimiser B
+    m1 = build(c)
+    oa = Adagrad(lr, eps)
+    for hb in batches[:2]:
+        train_step(m1, hb.dense.astype(np.float32), sp(hb), hb.labels, oa)
+    a_state = [a.clone() for a in oa._table_state.values()]
+    assert any(float(a.abs().sum()) > 0 for a in a_state)
+    ob = Adagrad(lr, eps)
+    r1 = train_step(m1, batches[2].dense.astype(np.float32), sp(batches[2]),
+                    batches[2].labels, ob)
+    # model 2: the same two steps, then a fresh optimiser on a copy of the
+    # parameters in a NEW model (no cached engine): zero accumulators
+    m2 = build(c)
+    oc = Adagrad(lr, eps)
+    for hb in batches[:2]:
+        train_step(m2, hb.dense.astype(np.float32), sp(hb), hb.labels, oc)
+    m3 = m2.copy()
+    r3 = train_step(m3, batches[2].dense.astype(np.float32), sp(batches[2]),
+                    batches[2].labels, Adagrad(lr, eps))
+    assert r1.loss == r3.loss
+    for x, y in zip(arrays(m1.bottom, m1.top, m1.tables), arrays(m3.bottom, m3.top, m3.tables)):
+        assert np.array_equal(x, y)
+    # A kept its own accumulators (not B's step)
+    for x, y in zip(a_state, oa._table_state.values()):
+        assert torch.equal(x, y)
+    # and A resumes from them: A again on model 1 continues A's sums
+    train_step(m1, batches[3 % len(batches)].dense.astype(np.float32),
+               sp(batches[3 % len(batches)]), batches[3 % len(batches)].labels, oa)
+    assert not all(torch.equal(x, y) for x, y in zip(a_state, oa._table_state.values()))

@@ -1,0 +1,142 @@
+"""Whole-step parity at the BENCHMARKED configurations (BASELINE.json configs).
+
+The drop-in ``train_step`` and the float64 oracle (``oracle/port.py``, the
+reference algorithm op for op — bit-identical to dlrmkit, pinned by
+tests/test_oracle.py) run on identical inputs from the same fp32-rounded
+start point:
+
+* inputs: the reference's own random source (``RandomBatchSource`` =
+  dlrmkit ``_RandomSource``, seed 0) at the config's full shape;
+* start point: ``port.init_params`` (the reference's seeded draws), rounded to
+  fp32, loaded into both.
+
+Contract (BASELINE.json north_star): per step, loss within
+rtol 1e-4 and probabilities within 1e-4 (``rel_err``, floor 1e-3·max); after
+the run every MLP tensor within ``|Δ| ≤ 1e-4 (|ref| + 1e-3 max|ref|)`` and
+every TOUCHED table row within ``|Δ| ≤ 1e-4 (|ref| + 1e-2 max|ref|)``;
+untouched rows are bit-identical to their start values.
+
+Configs:
+* c3 — Big Basin: 8 × 1M rows, d = 64, pooling U[1,100], bottom 512-512-64,
+  top 1024-1024-1024-1, B = 2048 (the bench line's workload), 5 steps; also
+  Adagrad, 3 steps;
+* c2 — Criteo-Kaggle cardinalities (26 tables, 33.8M rows), d = 16, B = 2048,
+  5 steps;
+* c4 — Criteo-Terabyte shape, d = 128, bottom 13-512-256-128, top
+  1024-1024-512-256-1, B = 32768, rows capped at 2^18 per table (host
+  memory of the float64 oracle), 2 steps; the oracle's GEMMs are single BLAS
+  calls here (``port.ROWWISE = False``, see its note);
+* c1 — the reference default (8 × 1e4, d = 16, B = 128), 50 steps (SURVEY
+  Appendix A's drift experiment).
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1906_00091_b200 import (Adagrad, DlrmConfig, EmbeddingTable, MlpLayer,
+                                   MlpParams, Sgd, SparseBatch, train_step)
+from paper_1906_00091_b200.model import DlrmModel
+from paper_1906_00091_b200.rng import RandomBatchSource
+from tests._util import rel_err
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from bench import KAGGLE, TERABYTE_40M  # noqa: E402
+from oracle import port  # noqa: E402  (test infrastructure: the checker)
+
+pytestmark = pytest.mark.gpu
+
+CAP4 = 1 << 18
+FULL = {
+    "c3": dict(tables=[10 ** 6] * 8, d=64, bot=[512, 512, 64], top=[1024, 1024, 1024, 1],
+               batch=2048, k=100, fixed=False, steps=5),
+    "c2": dict(tables=KAGGLE, d=16, bot=[13, 512, 256, 64, 16], top=[512, 256, 1],
+               batch=2048, k=1, fixed=True, steps=5),
+    "c4": dict(tables=[min(m, CAP4) for m in TERABYTE_40M], d=128, bot=[13, 512, 256, 128],
+               top=[1024, 1024, 512, 256, 1], batch=32768, k=1, fixed=True, steps=2,
+               rowwise=False),
+    "c1": dict(tables=[10 ** 4] * 8, d=16, bot=[13, 512, 256, 64, 16], top=[512, 256, 1],
+               batch=128, k=1, fixed=True, steps=50),
+}
+
+
+def model_from_port(c, pm):
+    cfg = DlrmConfig(list(c["tables"]), c["d"], list(c["bot"]), list(c["top"]), seed=0)
+    mlp = lambda layers: MlpParams([MlpLayer(w, b, a) for w, b, a in layers])
+    tables = [EmbeddingTable(W, t) for t, W in enumerate(pm["tables"])]
+    return DlrmModel(cfg, mlp(pm["bottom"]), mlp(pm["top"]), tables)
+
+
+def run_pair(c, opt_name="sgd", lr=0.1, eps=1e-10, steps=None):
+    steps = steps or c["steps"]
+    pm = port.round_params_f32(port.init_params(c["tables"], c["d"], c["bot"], c["top"], 0))
+    model = model_from_port(c, pm)
+    start = [np.asarray(W, np.float32) for W in pm["tables"]]
+    src = RandomBatchSource(c["tables"], c["bot"][0], c["batch"], c["k"], c["fixed"], seed=0)
+    opt = Sgd(lr) if opt_name == "sgd" else Adagrad(lr, eps)
+    ada = port.adagrad_state(pm) if opt_name == "adagrad" else None
+    touched = [[] for _ in c["tables"]]
+    old = port.ROWWISE
+    port.ROWWISE = c.get("rowwise", True)
+    out = []
+    try:
+        for s in range(steps):
+            hb = src.next_batch()
+            # the GPU takes the fp32-rounded dense rows, so the oracle does too
+            dense = np.asarray(hb.dense, np.float32)
+            r = train_step(model, dense, [SparseBatch(o, i) for o, i in
+                                          zip(hb.offsets, hb.indices)], hb.labels, opt)
+            ref = port.train_step(pm, dense.astype(np.float64), hb.offsets, hb.indices,
+                                  hb.labels, lr, adagrad=ada, eps=eps)
+            out.append((r.loss, r.accuracy, r.probs.cpu().double().numpy(), ref))
+            for t, i in enumerate(hb.indices):
+                touched[t].append(np.unique(i))
+    finally:
+        port.ROWWISE = old
+    return model, pm, start, touched, out
+
+
+def check(c, model, pm, start, touched, out):
+    B = c["batch"]
+    worst = {"loss": 0.0, "probs": 0.0, "mlp": 0.0, "rows": 0.0}
+    for s, (loss, acc, probs, (rloss, racc, rprob)) in enumerate(out):
+        worst["loss"] = max(worst["loss"], abs(loss - rloss) / abs(rloss))
+        assert abs(loss - rloss) <= 1e-4 * abs(rloss), (s, loss, rloss)
+        e = rel_err(probs, rprob)
+        worst["probs"] = max(worst["probs"], e)
+        assert e < 1e-4, (s, e)
+        # a probability within ~1e-7 of 0.5 may round to the other side
+        assert abs(acc - racc) <= 2.0 / B, (s, acc, racc)
+    for got_l, (w, b, _) in zip(model.bottom.layers + model.top.layers,
+                                pm["bottom"] + pm["top"]):
+        for g, r in ((got_l.weight, w), (got_l.bias, b)):
+            e = rel_err(g.detach().cpu().double().numpy(), r)
+            worst["mlp"] = max(worst["mlp"], e)
+            assert e < 1e-4, e
+    for t, (tab, ref, st) in enumerate(zip(model.tables, pm["tables"], start)):
+        rows = np.unique(np.concatenate(touched[t])) if touched[t] else \
+            np.empty(0, np.int64)
+        got = tab.weights.detach().cpu().numpy()
+        e = rel_err(got[rows], ref[rows], floor=1e-2) if rows.size else 0.0
+        worst["rows"] = max(worst["rows"], e)
+        assert e < 1e-4, (t, e)
+        mask = np.ones(got.shape[0], bool)
+        mask[rows] = False
+        assert np.array_equal(got[mask], st[mask]), t
+    return worst
+
+
+@pytest.mark.parametrize("name", ["c3", "c2", "c4", "c1"])
+def test_full_config_matches_oracle(name):
+    c = FULL[name]
+    w = check(c, *run_pair(c))
+    print(f"{name}: worst relative errors {w}")
+
+
+def test_c3_adagrad_matches_oracle():
+    c = FULL["c3"]
+    w = check(c, *run_pair(c, "adagrad", lr=0.01, eps=1e-8, steps=3))
+    print(f"c3 adagrad: worst relative errors {w}")
