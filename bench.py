@@ -173,22 +173,27 @@ def cpu_port_rate(c, batch, steps, warmup, seed=0):
     if limiter is not None:
         limiter.restore_original_limits()
     sample = (f"oracle/port.py float64 train_step (reference algorithm), batch "
-              f"{batch} of the {c['batch']}-sample workload, {steps} timed steps "
-              f"after {warmup} warm-up, tables capped at {cap} rows")
+              f"{batch} ({'the full' if batch == c['batch'] else 'part of the'} "
+              f"{c['batch']}-sample step), {steps} timed steps after {warmup} warm-up, "
+              f"tables capped at {cap} rows")
     return batch * steps / dt, threads, sample, dt / steps
 
 
 def run_reference(args, c, rank, world):
     if rank != 0:
         return
-    batch = max(16, min(c["batch"], int(args.cpu_batch)))
+    # the per-GPU batch of our arm's workload (at N = 1: exactly its config)
+    batch = max(16, min(c["batch"] // world if c.get("global_batch") else c["batch"],
+                        int(args.cpu_batch) if args.cpu_batch else 1 << 30))
     rate, threads, sample, per = cpu_port_rate(c, batch, args.steps, args.warmup)
     line = {"impl": "reference", "metric": "train samples/s", "value": rate,
             "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (reference random source)",
-            "config": {"workload": c["name"], "global_batch": c["batch"] * world},
+            "config": {"workload": c["name"],
+                       "global_batch": c["batch"] if c.get("global_batch") else c["batch"] * world,
+                       "per_step_batch": batch},
             "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": rate, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -496,10 +501,17 @@ def run_ours(args, c, rank, world, dist):
     emb_roof = {k: {"GB/s": v[0], "ms": v[1], "bytes": v[2], "frac": v[0] / hbm}
                 for k, v in cands.items()}
 
+    # e2e through the drop-in API: the reference's host arrays (numpy, as
+    # RandomBatchSource / dlrmkit produce them) -> Prefetcher (worker threads
+    # pack each batch into a reused pinned block, one H2D copy on a copy
+    # stream) -> train_step(model, dense, batches, labels, Sgd) -> the
+    # StepResult's loss as a Python float (D2H + host sync) every step.
+    e2e_api = e2e_train_step(model, cfg, hbs, B, K, args.warmup, dist, dev)
+
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            batch = max(16, min(c["batch"], int(args.cpu_batch)))
+            batch = max(16, min(c["batch"], int(args.cpu_batch) if args.cpu_batch else 1 << 30))
             rate, threads, sample, _ = cpu_port_rate(c, batch, 2, 1)
             cpu = {"value": rate, "unit": "samples/s", "cores": threads,
                    "kind": "port", "sample": sample}
@@ -514,8 +526,16 @@ def run_ours(args, c, rank, world, dist):
                        "per_gpu_batch": B, "parallelism": f"hybrid{world}",
                        "l2": "flushed (256 MiB write) between timed steps",
                        "graph": use_graph},
-            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
-                    "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / K},
+            "e2e": {"value": world * B * K / (e2e_api["ms"] / 1e3), "unit": "samples/s",
+                    "h2d_bytes_per_step": e2e_api["h2d_bytes"], "d2h_bytes_per_step": 12,
+                    "ms_per_step": e2e_api["ms"] / K,
+                    "path": "train_step(model, dense, batches, labels, Sgd) on Prefetcher "
+                            "batches packed from the reference's numpy arrays; loss read "
+                            "back every step", "loss_last": e2e_api["loss_last"]},
+            "e2e_engine": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
+                           "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / K,
+                           "path": "StepEngine: pre-packed pinned blocks, H2D of step s+1 "
+                                   "overlapping step s, loss sum + #correct read back"},
             "gpu_launches": int(launches) * K if launches else None,
             "roofline": roofline, "embedding_roofline": emb_roof, "mlp_roofline": mlp_roof,
             "stages_ms": {k: v for k, v in stages.items() if k != "captured"},
@@ -524,6 +544,47 @@ def run_ours(args, c, rank, world, dist):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+
+
+def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
+    """K steps of the public API (see run_ours); device-timed with CUDA events
+    on the compute stream, max over ranks."""
+    import torch
+    from paper_1906_00091_b200 import Prefetcher, Sgd, train_step
+    T = cfg.num_tables
+    caps = [max(int(hb.indices[t].size) for hb in hbs) for t in range(T)]
+
+    def source():
+        s = 0
+        while True:
+            yield hbs[s % len(hbs)]
+            s += 1
+    pf = Prefetcher(source(), B, T, cfg.dense_dim, capacities=caps, depth=3,
+                    threads=min(8, max(1, (os.cpu_count() or 2) // 2)))
+    it = iter(pf)
+    opt = Sgd(0.1)
+    for _ in range(warmup + 2):   # eager step, graph capture, warm-up
+        d, b, l = next(it)
+        train_step(model, d, b, l, opt)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    loss = None
+    for _ in range(K):
+        d, b, l = next(it)
+        loss = train_step(model, d, b, l, opt).loss
+    e1.record(stream)
+    torch.cuda.synchronize()
+    pf.close()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"ms": ms, "h2d_bytes": int(pf.layout.nbytes), "loss_last": loss}
 
 
 def rank_batches(c, plan, rank, P, seed):
@@ -561,15 +622,16 @@ def run_hybrid(args, c, rank, world, dist):
     Bg = B * world
     cfg = DlrmConfig(c["tables"], c["d"], c["bot"], c["top"], seed=0)
     model = init_model(cfg, table_init="device")
-    plan = make_plan(cfg, Bg, world)
+    pool = (c["k"] if c["fixed"] else (c["k"] + 1) / 2.0)
+    plan = make_plan(cfg, Bg, world, policy=args.plan, pooling=[pool] * cfg.num_tables,
+                     capacity_bytes=150e9)
     own = plan.owned(rank)
-    ar_group = dist.new_group(list(range(world)))
     P = args.pool
     hbs = rank_batches(c, plan, rank, P, seed=1)
     # index capacity per owned table = the largest batch of the pool (the
     # captured graph serves every batch; the sort runs over the capacity)
     caps = [max(int(b[3][j].size) for b in hbs) for j in range(len(own))]
-    tr = HybridTrainer(model, plan, rank, caps, lr=0.1, ar_group=ar_group)
+    tr = HybridTrainer(model, plan, rank, caps, lr=0.1)
 
     # the data pipeline packs each batch once into the rank's input-block
     # layout (pinned host); the device pool holds the same blocks in HBM
@@ -651,8 +713,8 @@ def run_hybrid(args, c, rank, world, dist):
             "vs_baseline": (value / c["published"]) if c["published"] else None,
             "dtype": "f32", "data": "synthetic (seeded numpy; device-seeded tables)",
             "config": {"workload": c["name"], "global_batch": Bg, "per_gpu_batch": B,
-                       "parallelism": f"hybrid: tables model-parallel {plan.table_assignment}, "
-                                      f"MLP data-parallel x{world}",
+                       "parallelism": f"hybrid: tables model-parallel {plan.table_assignment} "
+                                      f"({args.plan} plan), MLP data-parallel x{world}",
                        "l2": "flushed (256 MiB write) between timed steps",
                        "graph": captured},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d,
@@ -674,13 +736,30 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--hybrid", action="store_true",
                     help="run the multi-process hybrid path even at N=1 (under torchrun)")
+    ap.add_argument("--plan", default="size", choices=["size", "traffic"],
+                    help="table placement for N > 1: the reference's size-balanced plan or "
+                         "the traffic-balanced one")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-batch", type=int, default=256)
+    ap.add_argument("--cpu-batch", type=int, default=0,
+                    help="batch of the CPU reference / baseline sample (0: the workload's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     dist = None
     if args.impl == "reference":
         run_reference(args, c, rank, world)

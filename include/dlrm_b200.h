@@ -303,8 +303,9 @@ int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* up
 
 /* ---- misc --------------------------------------------------------------- */
 
-/* GEMM kernel selection (tests / A-B measurements): 0 = tcgen05 3xTF32
- * wherever the shape and strides allow (default), 1 = SIMT fp32 only. */
+/* Kernel selection (tests / A-B measurements): 0 = tcgen05 3xTF32 wherever
+ * the shape and strides allow (default), 1 = SIMT fp32 only (MLP GEMMs and
+ * the dot interaction). */
 int dlrm_gemm_mode(int32_t mode);
 
 /* ---- input pipeline: Criteo TSV ingestion (host code, multithreaded) ----

@@ -17,9 +17,11 @@ from .model import (DlrmCache, DlrmConfig, DlrmGradients, DlrmModel, MlpCache,
                     embedding_param_count, from_reference, init_mlp, init_model,
                     interact, to_reference,
                     interact_backward, interaction_width, mlp_backward,
-                    mlp_forward, mlp_param_count, param_count)
+                    mlp_forward, mlp_param_count, param_count, sigmoid)
 from .optim import (Adagrad, AdagradState, Sgd, adagrad_step, adagrad_step_rows,
                     make_optimizer, sgd_step, sgd_step_rows)
+from .timing import NullTimer, StageTimer
+from .pipeline import InputLayout, Prefetcher
 from .trainer import StepEngine, StepResult
 from .parallel import (CommLog, DevicePlan, ParallelTrainer, ShuffleSlice,
                        allreduce,

@@ -7,6 +7,10 @@
 
 namespace dlrm {
 
+// false after dlrm_gemm_mode(1): every tensor-core kernel (GEMMs and the
+// interaction) is replaced by its SIMT fp32 counterpart (A/B tests)
+bool tc_enabled();
+
 bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw,
                       const float* Y, int64_t ldy, int64_t M, int64_t N,
                       int64_t K, int64_t n_grid);

@@ -1,4 +1,7 @@
-// Pairwise dot-product feature interaction (SIMT, shared-memory tiled).
+// Pairwise dot-product feature interaction: C-ABI entry points, dispatching
+// to the tcgen05 kernels (interact_tc.cu) and the SIMT fallback below
+// (shapes the tensor-core path does not take: d % 8 / d % 16, d > 128,
+// nf > 64, unaligned features; DLRM_IA_SIMT=1 forces it).
 //
 // Reference (dlrmkit, pkg/src/dlrmkit/model.py):
 //   interact           218-242  out = [z0 | z_i . z_j for i < j, row-major]
@@ -13,6 +16,18 @@
 #include "common.cuh"
 
 namespace dlrm {
+
+// tcgen05 path (interact_tc.cu): used whenever the shape / alignment allows
+bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t ld_out,
+                        const float* out);
+int interact_tc_fwd(const FeatureSet& fs, int nf, int64_t dim, int64_t batch, float* out,
+                    int64_t ld_out, int64_t pad_to, cudaStream_t s);
+bool interact_tc_bwd_ok(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
+                        const float* gout, int64_t ld_gout);
+int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
+                    int64_t batch, const float* gout, int64_t ld_gout, int mask_f0,
+                    cudaStream_t s);
+
 namespace {
 
 // 512 threads per CTA: at the Terabyte shape (27 features, d = 128, B = 32768)
@@ -293,6 +308,8 @@ extern "C" int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf,
   bool v4;
   if (int rc = fill_features(fs, feats, nf, dim, &v4)) return rc;
   if (batch == 0) return 0;
+  if (interact_tc_fwd_ok(fs, nf, dim, ld_out, out))
+    return interact_tc_fwd(fs, nf, dim, batch, out, ld_out, pad_to, as_stream(stream));
   const int npairs = nf * (nf - 1) / 2;
   const size_t fixed = align_up(size_t(npairs) * 4, 16);
   const int S = pick_samples(nf, dim, batch, 0, fixed, DLRM_IA_BUDGET_KB * 1024);
@@ -325,6 +342,9 @@ extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
   }
   v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
   if (batch == 0) return 0;
+  if (interact_tc_bwd_ok(fs, gs, nf, dim, gout, ld_gout))
+    return interact_tc_bwd(fs, gs, nf, dim, batch, gout, ld_gout, relu_mask_f0,
+                           as_stream(stream));
   const size_t extra = size_t(nf) * ((nf + 3) & ~3) * 4;
   const int S = pick_samples(nf, dim, batch, extra, 0, DLRM_IA_BUDGET_KB * 1024);
   const size_t smem = size_t(S) * (nf * (dim + 4) * 4 + extra);

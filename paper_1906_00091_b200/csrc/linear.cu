@@ -141,6 +141,45 @@ int skinny_wgrad(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int6
 
 using namespace dlrm;
 
+namespace dlrm {
+namespace {
+// N = 1 layer (the top MLP's last, identity layer): one warp per row with
+// EXACTLY the loss head's dot order (head.cu bce_head_kernel /
+// head_fused_kernel: lane l folds float4 chunks l, l+32, ... with fmaf, then
+// an xor-shuffle tree), so mlp_forward's logits and dlrm_forward's
+// probabilities are bitwise those of the fused training step.
+__global__ void __launch_bounds__(256)
+linear_n1_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ w,
+                 const float* __restrict__ b, float* __restrict__ Y, int64_t ldy, int64_t M,
+                 int64_t K, int64_t ng, int act) {
+  pdl_entry();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t m = int64_t(blockIdx.x) * 8 + warp;
+  if (m >= M) return;
+  const float* a = X + m * ldx;
+  float acc = 0.f;
+  if ((K % 4) == 0 && (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(X) % 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(w) % 16) == 0) {
+    for (int64_t k = 4 * lane; k < K; k += 128) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(a + k));
+      const float4 v = __ldg(reinterpret_cast<const float4*>(w + k));
+      acc = fmaf(x.x, v.x, acc);
+      acc = fmaf(x.y, v.y, acc);
+      acc = fmaf(x.z, v.z, acc);
+      acc = fmaf(x.w, v.w, acc);
+    }
+  } else {
+    for (int64_t k = lane; k < K; k += 32) acc = fmaf(__ldg(a + k), __ldg(w + k), acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  float z = acc + (b ? b[0] : 0.f);
+  if (act == DLRM_ACT_RELU) z = fmaxf(z, 0.f);
+  for (int64_t c = lane; c < ng; c += 32) Y[m * ldy + c] = c == 0 ? z : 0.f;
+}
+}  // namespace
+}  // namespace dlrm
+
 extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
                                int64_t ldw, const float* b, float* Y,
                                int64_t ldy, int64_t M, int64_t N, int64_t K,
@@ -152,6 +191,11 @@ extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
   if (M == 0) return 0;
   cudaStream_t s = as_stream(stream);
   const int64_t ng = pad_n > N ? pad_n : N;
+  if (N == 1) {
+    launch(linear_n1_kernel, unsigned(ceil_div(M, 8)), 256, 0, s, X, ldx, W, b, Y, ldy, M,
+           K, ng, int(act));
+    return check_launch("linear_n1_kernel");
+  }
   if (tc_linear_fwd_ok(X, ldx, W, ldw, Y, ldy, M, N, K, ng))
     return tc_linear_fwd(X, ldx, W, ldw, b, Y, ldy, M, N, K, ng, act, s);
   GemmEpilogue ep{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, ng, M};

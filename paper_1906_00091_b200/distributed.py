@@ -85,15 +85,19 @@ class ExchangeLayout:
 
 class NcclExchange:
     """torch.distributed transport (NCCL on GPUs, gloo on CPU): the forward
-    and reverse all-to-all on one communicator, gradient allreduces on a
-    second one so they overlap the reverse all-to-all."""
+    and reverse all-to-all and the allreduces, all on ONE communicator
+    (``group``) — the trainer issues them in a fixed order on one stream.
+    ``ar_group`` is accepted for compatibility and must be None or the same
+    group."""
 
     def __init__(self, layout: ExchangeLayout, group=None, ar_group=None):
         import torch.distributed as dist
+        if ar_group is not None and ar_group is not group:
+            raise ValueError("all collectives share one communicator (ar_group must be None)")
         self.dist = dist
         self.L = layout
         self.group = group
-        self.ar_group = ar_group if ar_group is not None else group
+        self.ar_group = group
 
     def forward(self, send: torch.Tensor, recv: torch.Tensor):
         self.dist.all_to_all_single(recv, send, self.L.recv_split,
@@ -159,7 +163,7 @@ class RankEngine:
 
     def __init__(self, model: DlrmModel, layout: ExchangeLayout,
                  capacities=None, lr: float = 0.1, optimizer: str = "sgd",
-                 eps: float = 1e-10, weighted: bool = False):
+                 eps: float = 1e-10, weighted: bool = False, force_exchange: bool = False):
         _lib.require_cuda()
         self.weighted = bool(weighted)
         cfg = model.config
@@ -231,11 +235,16 @@ class RankEngine:
         if self.iweights is not None:
             self.iweights.fill_(1.0)
 
-        # exchange buffers
+        # exchange buffers; with one rank the exchange is the identity (the
+        # send layout [B_g, T, d] IS the receive layout), so they alias
+        self.single = layout.plan.num_devices == 1 and not force_exchange
         self.send = torch.zeros(max(layout.send_numel, 1), **f32)
-        self.recv = torch.zeros(max(layout.recv_numel, 1), **f32)
+        self.recv = self.send if self.single else torch.zeros(max(layout.recv_numel, 1), **f32)
         self.gsend = torch.zeros(max(layout.recv_numel, 1), **f32)
-        self.grecv = torch.zeros(max(layout.send_numel, 1), **f32)
+        self.grecv = self.gsend if self.single else torch.zeros(max(layout.send_numel, 1), **f32)
+        # one rank: no gradient exchange, so the update rule is fused into the
+        # weight-gradient / head kernels exactly like the single-device step
+        self.fuse_update = self.single
 
         # activations / gradients
         bl, tl = model.bottom.layers, model.top.layers
@@ -426,11 +435,18 @@ class RankEngine:
             # loss statistics, dA for the top backward and the head's dw / db
             gw, gb = self.gslots[-1]
             ga = self.gtop[-1] if self.Lt > 1 else self.gR
-            call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), Bl,
-                 head.n_in, P(self.labels), float(self.Bg), P(self.prob), P(self.glogit),
-                 P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw), P(gb),
-                 None, None, C.byref(self.upd_mlp), None, P(self.lin_ws),
-                 self.lin_ws_bytes, s)
+            if self.fuse_update:
+                call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), Bl,
+                     head.n_in, P(self.labels), float(self.Bg), P(self.prob), P(self.glogit),
+                     P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None, None,
+                     P(head.storage), P(head.bias), C.byref(self.upd_mlp), P(self.err_flag),
+                     P(self.lin_ws), self.lin_ws_bytes, s)
+            else:
+                call("dlrm_head_step", P(a), lda, P(head.storage), P(head.bias), Bl,
+                     head.n_in, P(self.labels), float(self.Bg), P(self.prob), P(self.glogit),
+                     P(self.stats), P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw), P(gb),
+                     None, None, C.byref(self.upd_mlp), None, P(self.lin_ws),
+                     self.lin_ws_bytes, s)
         else:
             call("dlrm_bce_head", P(a), lda, P(head.storage), P(head.bias), Bl,
                  head.n_in, P(self.labels), float(self.Bg), None, P(self.prob),
@@ -438,16 +454,31 @@ class RankEngine:
                  self.lin_ws_bytes, s)
         self._head_in = (a, lda)
 
-    def _wgrad(self, stream, wgrad_stream, *args):
-        """Weight gradient (into its allreduce slot): on ``wgrad_stream``
-        after the work issued so far on ``stream``, when given."""
+    def _wgrad_call(self, li, gz, ldg, xin, ws, stream_handle):
+        """Layer li's weight / bias gradient: into its allreduce slot, or
+        (one rank) straight into the update rule, fused."""
+        P, l = _lib.ptr, self.layers[li]
+        if self.fuse_update:
+            _lib.call("dlrm_linear_bwd_weight_upd", P(gz), ldg, P(xin), xin.stride(0), self.Bl,
+                      l.n_out, l.n_in, None, 0, None, P(l.storage), l.ldw, P(l.bias),
+                      C.byref(self.upd_mlp), P(self.err_flag), P(ws), self.lin_ws_bytes,
+                      stream_handle)
+            return
+        gw, gb = self.gslots[li]
+        _lib.call("dlrm_linear_bwd_weight", P(gz), ldg, P(xin), xin.stride(0), self.Bl,
+                  l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None, 0.0, None,
+                  P(ws), self.lin_ws_bytes, stream_handle)
+
+    def _wgrad(self, stream, wgrad_stream, li, gz, ldg, xin):
+        """Weight gradient on ``wgrad_stream`` after the work issued so far
+        on ``stream``, when given (else on ``stream``)."""
         if wgrad_stream is None:
-            _lib.call("dlrm_linear_bwd_weight", *args, _lib.stream_handle(stream))
+            self._wgrad_call(li, gz, ldg, xin, self.lin_ws, _lib.stream_handle(stream))
             return
         ev = torch.cuda.Event()
         ev.record(stream if stream is not None else torch.cuda.current_stream())
         wgrad_stream.wait_event(ev)
-        _lib.call("dlrm_linear_bwd_weight", *args, _lib.stream_handle(wgrad_stream))
+        self._wgrad_call(li, gz, ldg, xin, self.lin_ws, _lib.stream_handle(wgrad_stream))
 
     def phase_b_top_backward(self, stream=None, wgrad_stream=None):
         """Top MLP backward; with ``wgrad_stream`` each weight gradient runs
@@ -459,7 +490,12 @@ class RankEngine:
         head = L[-1]
         gw, gb = self.gslots[-1]
         ga = self.gtop[-1] if self.Lt > 1 else self.gR
-        if not self.head_fused:
+        if not self.head_fused and self.fuse_update:
+            call("dlrm_head_bwd_upd", P(a), lda, P(head.storage), P(self.glogit), Bl,
+                 head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, None, None,
+                 P(head.storage), P(head.bias), C.byref(self.upd_mlp), P(self.err_flag),
+                 P(self.lin_ws), self.lin_ws_bytes, s)
+        elif not self.head_fused:
             call("dlrm_head_bwd", P(a), lda, P(head.storage), P(self.glogit), Bl,
                  head.n_in, P(ga), ga.stride(0), 1 if self.Lt > 1 else 0, P(gw),
                  P(gb), None, None, 0.0, None, P(self.lin_ws), self.lin_ws_bytes, s)
@@ -473,10 +509,7 @@ class RankEngine:
             call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage), l.ldw,
                  P(mask), mask.stride(0) if mask is not None else 0, P(dx),
                  dx.stride(0), Bl, l.n_out, l.n_in, s)
-            gw, gb = self.gslots[li]
-            self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
-                        Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                        0.0, None, P(self.lin_ws), self.lin_ws_bytes)
+            self._wgrad(stream, wgrad_stream, li, gz, gz.stride(0), xin)
 
     def phase_b_interaction_backward(self, stream=None):
         s = _lib.stream_handle(stream)
@@ -498,17 +531,12 @@ class RankEngine:
                 call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
                      l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
                      dx.stride(0), Bl, l.n_out, l.n_in, s)
-            gw, gb = self.gslots[i]
             if i == 0 and wgrad_stream is not None:
                 # the first layer's weight gradient on the (then idle) calling
                 # stream, beside the weight-gradient stream (own workspace)
-                call("dlrm_linear_bwd_weight", P(gz), gz.stride(0), P(xin), xin.stride(0),
-                     Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                     0.0, None, P(self.lin_ws2), self.lin_ws_bytes, s)
+                self._wgrad_call(i, gz, gz.stride(0), xin, self.lin_ws2, s)
             else:
-                self._wgrad(stream, wgrad_stream, P(gz), gz.stride(0), P(xin), xin.stride(0),
-                            Bl, l.n_out, l.n_in, P(gw), gw.stride(0), P(gb), None, 0, None,
-                            0.0, None, P(self.lin_ws), self.lin_ws_bytes)
+                self._wgrad(stream, wgrad_stream, i, gz, gz.stride(0), xin)
 
     def publish_error(self):
         """stats[2] <- this rank's error flag (allreduced with the loss)."""
@@ -524,14 +552,18 @@ class RankEngine:
         the trainer runs it on a side stream under the dense work."""
         To = len(self.own)
         if To:
-            sh = _lib.stream_handle(stream)
             _lib.call("dlrm_emb_bwd_prepare", self.d, C.cast(self._descs, C.c_void_p), To,
-                      self.Bg, self.total_rows, _lib.ptr(self.emb_ws), self.emb_ws_bytes, sh)
-            # the keys pass records every bad position: resolve the offending
-            # values on the device, from the batch that ran
+                      self.Bg, self.total_rows, _lib.ptr(self.emb_ws), self.emb_ws_bytes,
+                      _lib.stream_handle(stream))
+
+    def resolve_errors(self, stream=None):
+        """Offending index value per owned table (dlrm_err_resolve), read on
+        the device from the batch that ran; ordered after the lookups."""
+        To = len(self.own)
+        if To:
             _lib.call("dlrm_err_resolve", C.cast(self._descs, C.c_void_p), To,
                       _lib.ptr(self.err_pos), _lib.ptr(self.err_flag),
-                      _lib.ptr(self.err_val), sh)
+                      _lib.ptr(self.err_val), _lib.stream_handle(stream))
 
     def apply_sparse(self, stream=None):
         """Owned tables: segmented fold of the received gradients + row SGD
@@ -545,7 +577,10 @@ class RankEngine:
                       P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(stream))
 
     def sgd_dense(self, stream=None):
-        """Dense update of the MLP replica from the allreduced gradients."""
+        """Dense update of the MLP replica from the allreduced gradients
+        (nothing to do with one rank: the updates were fused)."""
+        if self.fuse_update:
+            return
         P = _lib.ptr
         _lib.call("dlrm_update_dense", P(self.params), P(self.grads),
                   self.params.numel(), C.byref(self.upd_mlp), P(self.err_flag),
@@ -578,10 +613,13 @@ class HybridTrainer:
 
     def __init__(self, model: DlrmModel, plan: DevicePlan, rank: int,
                  capacities=None, lr: float = 0.1, group=None, ar_group=None,
-                 optimizer: str = "sgd", eps: float = 1e-10, weighted: bool = False):
+                 optimizer: str = "sgd", eps: float = 1e-10, weighted: bool = False,
+                 force_exchange: bool = False):
+        # force_exchange: run the collectives (and the unfused updates) even
+        # with one rank — tests the multi-rank code path on one GPU
         self.layout = ExchangeLayout(plan, rank, model.config.sparse_dim)
         self.engine = RankEngine(model, self.layout, capacities, lr, optimizer, eps,
-                                 weighted)
+                                 weighted, force_exchange)
         self.ex = NcclExchange(self.layout, group, ar_group)
         self.rank = rank
         self.comm_stream = torch.cuda.Stream()
@@ -633,52 +671,70 @@ class HybridTrainer:
     def _issue(self):
         e, ex = self.engine, self.ex
         cur = torch.cuda.current_stream()
-        # sort the owned lookups on the side stream while the step runs
-        fork = torch.cuda.Event()
-        fork.record(cur)
-        self.side.wait_event(fork)
-        e.prepare_sparse_backward(self.side)
+        comm, wg, side = self.comm_stream, self.wg_stream, self.side
+        mark = self._mark
+        single = e.single
+        # keys + sort of the owned lookups on the side stream from the start
+        fork = mark(cur)
+        side.wait_event(fork)
+        e.prepare_sparse_backward(side)
         # bottom MLP forward beside the owner lookups and the exchange
         self.fwd_stream.wait_event(fork)
         e.phase_b_bottom_forward(self.fwd_stream)
-        bot = torch.cuda.Event()
-        bot.record(self.fwd_stream)
+        bot = mark(self.fwd_stream)
         e.phase_a()
-        ex.forward(e.send, e.recv)
+        # Every collective of the step runs on ONE stream over ONE
+        # communicator, issued in the same order on every rank: forward
+        # all-to-all, loss statistics, reverse all-to-all, top-MLP gradients,
+        # bottom-MLP gradients — no two communicators are ever in flight
+        # together for NCCL to deadlock on.  Events tie them to the compute
+        # streams, so they still overlap the backward pass.  One rank: the
+        # exchanges are the identity and the updates are fused (no collective).
+        if not single:
+            comm.wait_event(mark(cur))
+            with torch.cuda.stream(comm):
+                ex.forward(e.send, e.recv)
+            cur.wait_event(mark(comm))
         cur.wait_event(bot)
         e.phase_b_forward(bottom=False)
-        # loss, correct count and this rank's index-error flag are all known
-        # after the head: reduce them now, so every rank can skip its updates
-        # (on device) before any update is issued
+        # loss, correct count and this rank's index-error flag are known after
+        # the head; the reduced flag gates every update (on device)
         e.publish_error()
-        ex.allreduce(e.stats)
-        e.adopt_global_error()
-        wg = self.wg_stream
+        if not single:
+            comm.wait_event(mark(cur))
+            with torch.cuda.stream(comm):
+                ex.allreduce(e.stats)
+                e.adopt_global_error()
         e.phase_b_top_backward(wgrad_stream=wg)
-        # top-MLP gradients reduce on the second communicator while the
-        # interaction / bottom backward and the reverse exchange run: issued
-        # from the weight-gradient stream, so only the allreduce waits for
-        # the last weight gradient
-        wg.wait_event(self._mark(cur))  # the head's / data gradients' side too
-        with torch.cuda.stream(wg):
-            h_top = ex.allreduce_async(e.grads[e.split_at:])
+        top_grads = (mark(wg), mark(cur))
         e.phase_b_interaction_backward()
-        ex.backward(e.gsend, e.grecv)
-        # owned-table fold + row update on the side stream, concurrently
-        # with the bottom MLP backward
-        got = torch.cuda.Event()
-        got.record(cur)
-        self.side.wait_event(got)
-        e.apply_sparse(self.side)
-        applied = torch.cuda.Event()
-        applied.record(self.side)
+        if not single:
+            comm.wait_event(mark(cur))
+            with torch.cuda.stream(comm):
+                ex.backward(e.gsend, e.grecv)
+            got = mark(comm)
+            for ev in top_grads:
+                comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                ex.allreduce(e.grads[e.split_at:])
+        else:
+            got = mark(cur)
+        # owned-table fold + row update on the side stream, concurrently with
+        # the bottom MLP backward
+        side.wait_event(got)
+        e.apply_sparse(side)
+        e.resolve_errors(side)
+        applied = mark(side)
         e.phase_b_bottom_backward(wgrad_stream=wg)
-        wg.wait_event(self._mark(cur))
-        with torch.cuda.stream(wg):
-            h_bot = ex.allreduce_async(e.grads[:e.split_at])
-        h_top.wait()
-        h_bot.wait()
-        e.sgd_dense()
+        if not single:
+            comm.wait_event(mark(wg))
+            comm.wait_event(mark(cur))
+            with torch.cuda.stream(comm):
+                ex.allreduce(e.grads[:e.split_at])
+            cur.wait_event(mark(comm))
+            e.sgd_dense()
+        else:
+            cur.wait_event(mark(wg))   # the fused updates of the weight gradients
         cur.wait_event(applied)
 
     @staticmethod

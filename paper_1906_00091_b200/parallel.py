@@ -20,11 +20,13 @@ import torch
 
 from .model import DlrmConfig, DlrmModel
 from .optim import Sgd
+from .pipeline import StagedDense
+from .timing import NullTimer, add_seconds
 from .trainer import StepEngine, StepResult
 
 __all__ = [
     "DevicePlan", "ShuffleSlice", "CommLog", "StepResult", "partition_tables",
-    "shard_bounds", "make_plan", "butterfly_shuffle", "inverse_shuffle",
+    "shard_bounds", "make_plan", "partition_tables_by_traffic", "butterfly_shuffle", "inverse_shuffle",
     "allreduce", "allreduce_max", "train_step", "evaluate", "format_comm_report",
     "ParallelTrainer",
 ]
@@ -85,10 +87,56 @@ def shard_bounds(batch_size: int, num_devices: int) -> list:
     return out
 
 
-def make_plan(config: DlrmConfig, batch_size: int, num_devices: int) -> DevicePlan:
-    sizes = [m * config.sparse_dim for m in config.embedding_sizes]
-    plan = DevicePlan(num_devices, partition_tables(sizes, num_devices),
-                      shard_bounds(batch_size, num_devices))
+def partition_tables_by_traffic(traffic, table_bytes, num_devices: int,
+                                capacity_bytes: float | None = None) -> list:
+    """Greedy heaviest-traffic-first: each table to the device with the least
+    per-step traffic so far (ties: lowest id) among those whose memory can
+    still hold it.  A table's owner pays for its lookups and for its pooled
+    rows in the all-to-all every step, whatever its row count; the
+    reference's size-balanced plan can give one GPU most of the (small)
+    tables — 19 of 26 on one of 8 GPUs at the Criteo shapes — and with it
+    most of the lookup and exchange work (SURVEY §7 hard part 5)."""
+    if num_devices < 1:
+        raise ValueError("need at least one device")
+    if len(traffic) != len(table_bytes):
+        raise ValueError("one traffic figure per table")
+    load = [0.0] * num_devices
+    mem = [0.0] * num_devices
+    owner = [0] * len(traffic)
+    for t in sorted(range(len(traffic)), key=lambda t: (-traffic[t], -table_bytes[t], t)):
+        fits = [d for d in range(num_devices)
+                if capacity_bytes is None or mem[d] + table_bytes[t] <= capacity_bytes]
+        if not fits:
+            raise ValueError(f"table {t} ({table_bytes[t]} bytes) fits on no device")
+        dev = min(fits, key=lambda d: (load[d], d))
+        owner[t] = dev
+        load[dev] += traffic[t]
+        mem[dev] += table_bytes[t]
+    return owner
+
+
+def make_plan(config: DlrmConfig, batch_size: int, num_devices: int,
+              policy: str = "size", pooling=None, capacity_bytes: float | None = None
+              ) -> DevicePlan:
+    """The reference plan (``policy="size"``: greedy on table sizes,
+    bit-identical to ref parallel.py:116-122) or ``policy="traffic"``:
+    greedy on per-step traffic — lookups (``pooling[t]`` indices per bag,
+    default 1) plus the pooled row exchanged — within ``capacity_bytes`` of
+    table memory per device (default: no limit)."""
+    d = config.sparse_dim
+    sizes = [m * d for m in config.embedding_sizes]
+    if policy == "size":
+        owner = partition_tables(sizes, num_devices)
+    elif policy == "traffic":
+        pool = [1.0] * len(sizes) if pooling is None else [float(p) for p in pooling]
+        if len(pool) != len(sizes):
+            raise ValueError("one pooling factor per table")
+        traffic = [batch_size * d * 4 * (p + 1.0) for p in pool]
+        owner = partition_tables_by_traffic(traffic, [4.0 * x for x in sizes], num_devices,
+                                            capacity_bytes)
+    else:
+        raise ValueError(f"unknown plan policy {policy!r}")
+    plan = DevicePlan(num_devices, owner, shard_bounds(batch_size, num_devices))
     plan.validate()
     return plan
 
@@ -200,22 +248,27 @@ def format_comm_report(comm: CommLog) -> str:
 # single-device training step  (ref parallel.py:250-287)
 
 def _engine_for(model: DlrmModel, batch: int, batches, optimizer,
-                weighted: bool) -> StepEngine:
+                weighted: bool, caps=None) -> StepEngine:
+    """The model's cached step engine if it fits (batch, update rule,
+    weighting, index capacities; ``caps``: exactly these capacities, the
+    layout of a staged batch), else a new one."""
     eng = getattr(model, "_engine", None)
     nnz = [sb.nnz for sb in batches]
     kind = optimizer.name
     eps = float(getattr(optimizer, "eps", 1e-10))
-    if (eng is not None and eng.B == batch and eng.lr == float(optimizer.lr)
+    fits = (eng is not None and (caps is None or list(eng.caps) == list(caps))
+            and all(n <= c for n, c in zip(nnz, eng.caps)))
+    if (fits and eng.B == batch and eng.lr == float(optimizer.lr)
             and eng.optimizer == kind and (kind != "adagrad" or eng.eps == eps)
-            and eng.weighted == weighted
-            and all(n <= c for n, c in zip(nnz, eng.caps))):
+            and eng.weighted == weighted):
         if isinstance(optimizer, _EngineSpec):
             return eng
         _bind_optimizer(eng, optimizer, model)
         return eng
-    caps = [max(n, batch) for n in nnz]
-    if eng is not None:  # grow geometrically so graphs are rarely rebuilt
-        caps = [max(c, int(1.25 * old)) for c, old in zip(caps, eng.caps)]
+    if caps is None:
+        caps = [max(n, batch) for n in nnz]
+        if eng is not None:  # grow geometrically so graphs are rarely rebuilt
+            caps = [max(c, int(1.25 * old)) for c, old in zip(caps, eng.caps)]
     old_owner = getattr(eng, "opt_owner", None) if eng is not None else None
     old_owner = old_owner() if old_owner is not None else None
     eng = StepEngine(model, batch, caps, lr=optimizer.lr, weighted=weighted,
@@ -319,10 +372,28 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
             raise ValueError(
                 f"sparse batch {t} has {sb.num_segments} segments, batch is {b}")
     weighted = any(sb.weights is not None for sb in batches)
-    eng = _engine_for(model, b, batches, optimizer, weighted)
-    eng.load(dense_x, [sb.offsets for sb in batches],
-             [sb.indices for sb in batches], labels,
-             [sb.weights for sb in batches] if weighted else None)
+    if isinstance(dense_x, StagedDense):
+        # a Prefetcher batch: already packed and on the device; one D2D copy
+        # of its block into the engine's input set
+        L = dense_x._layout
+        eng = _engine_for(model, b, batches, optimizer, L.weighted, caps=L.caps)
+        dense_x.consume(eng.input_sets[eng._set]["block"])
+    else:
+        eng = _engine_for(model, b, batches, optimizer, weighted)
+        eng.load(dense_x, [sb.offsets for sb in batches],
+                 [sb.indices for sb in batches], labels,
+                 [sb.weights for sb in batches] if weighted else None)
+    if timer is not None and (hasattr(timer, "seconds") or hasattr(timer, "add")) \
+            and not isinstance(timer, NullTimer):
+        # operator attribution (ref parallel.py:254-285): device time per
+        # stage from CUDA events, credited to the reference's categories
+        ms = eng.run_timed(use_graph)
+        per = {c: 0.0 for c in ("bottom_mlp", "embedding_lookup", "interaction",
+                                "top_mlp", "loss", "optimizer")}
+        for stage, v in ms.items():
+            per[eng.CATEGORY[stage]] += v / 1e3
+        add_seconds(timer, per)
+        return eng.result()
     if eng.graph is None and use_graph and eng.eager_runs >= 1:
         eng.capture()
     if eng.graph is not None:
@@ -330,8 +401,6 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
     else:
         eng.run()
         eng.eager_runs += 1
-    if timer is not None and hasattr(timer, "seconds"):
-        timer.seconds.setdefault("train_step", 0.0)
     return eng.result()
 
 
@@ -467,31 +536,45 @@ class ParallelTrainer:
                    [batches[t].offsets for t in own],
                    [batches[t].indices for t in own],
                    [batches[t].weights for t in own] if weighted else None)
-        for e in self.engines:
-            e.phase_a()
-        self.ex.forward_all([e.send for e in self.engines],
-                            [e.recv for e in self.engines])
+        sec = _Sections(timer)
+        with sec("embedding_lookup"):
+            for e in self.engines:
+                e.phase_a()
+                e.resolve_errors()
+        with sec("shuffle"):
+            self.ex.forward_all([e.send for e in self.engines],
+                                [e.recv for e in self.engines])
         moved = sum(4 * n for r, L in enumerate(self.layouts)
                     for dst, n in enumerate(L.send_split) if dst != r)
         self.comm.add(step, "butterfly_shuffle", moved, G)
-        for e in self.engines:
-            e.phase_b_forward()
-            e.phase_b_top_backward()
-            e.phase_b_interaction_backward()
-        self.ex.backward_all([e.gsend for e in self.engines],
-                             [e.grecv for e in self.engines])
+        with sec("device_compute"):
+            for e in self.engines:
+                e.phase_b_forward()
+                e.phase_b_top_backward()
+                e.phase_b_interaction_backward()
+        with sec("shuffle"):
+            self.ex.backward_all([e.gsend for e in self.engines],
+                                 [e.grecv for e in self.engines])
         self.comm.add(step, "grad_reverse_shuffle", moved, G)
-        for e in self.engines:
-            e.phase_b_bottom_backward()
-            e.publish_error()
-        self.ex.allreduce_all([e.stats for e in self.engines])
-        self.comm.add(step, "loss_gather", 12 * (G - 1), G)
-        self.ex.allreduce_all([e.grads for e in self.engines])
-        self.comm.add(step, "grad_allreduce",
-                      2 * (G - 1) * 4 * self.engines[0].grads.numel(), G)
-        for e in self.engines:
-            e.adopt_global_error()
-            e.phase_c()
+        with sec("device_compute"):
+            for e in self.engines:
+                e.phase_b_bottom_backward()
+                e.publish_error()
+        with sec("allreduce"):
+            self.ex.allreduce_all([e.stats for e in self.engines])
+            self.comm.add(step, "loss_gather", 12 * (G - 1), G)
+            self.ex.allreduce_all([e.grads for e in self.engines])
+            self.comm.add(step, "grad_allreduce",
+                          2 * (G - 1) * 4 * self.engines[0].grads.numel(), G)
+        with sec("embedding_lookup"):
+            for e in self.engines:
+                e.adopt_global_error()
+                e.prepare_sparse_backward()
+                e.apply_sparse()
+        with sec("optimizer"):
+            for e in self.engines:
+                e.sgd_dense()
+        sec.credit()
         if float(self.engines[0].stats[2].item()) > 0:
             for r, e in enumerate(self.engines):
                 err = e.local_error()
@@ -502,3 +585,39 @@ class ParallelTrainer:
         st = self.engines[0].stats.cpu()
         probs = torch.cat([e.prob for e in self.engines])
         return StepResult(float(st[0]) / n_total, float(st[1]) / n_total, probs)
+
+
+class _Sections:
+    """Device time of named host-side sections (CUDA events on the current
+    stream) credited to a StageTimer once the step is done."""
+
+    def __init__(self, timer):
+        self.on = timer is not None and not isinstance(timer, NullTimer) and \
+            (hasattr(timer, "add") or hasattr(timer, "seconds"))
+        self.timer, self.evs = timer, []
+
+    def __call__(self, name):
+        sections = self
+
+        class _Ctx:
+            def __enter__(self):
+                if sections.on:
+                    self.e0 = torch.cuda.Event(enable_timing=True)
+                    self.e0.record()
+
+            def __exit__(self, *exc):
+                if sections.on and exc[0] is None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    sections.evs.append((name, self.e0, e1))
+                return False
+        return _Ctx()
+
+    def credit(self):
+        if not self.on or not self.evs:
+            return
+        self.evs[-1][2].synchronize()
+        per = {}
+        for name, a, b in self.evs:
+            per[name] = per.get(name, 0.0) + a.elapsed_time(b) / 1e3
+        add_seconds(self.timer, per)

@@ -1,0 +1,281 @@
+"""Input pipeline of the training step: one step's inputs as ONE contiguous
+block (one host->device copy per step), packed from the reference's host
+arrays by worker threads and copied to the device ahead of the step.
+
+The reference feeds ``train_step`` numpy arrays (dense rows, per-table
+offsets / indices, labels; ref ``cli.py:294-314``, ``parallel.py:250-287``).
+Here:
+
+* ``InputLayout`` is the byte layout of a step's inputs for a fixed batch
+  size and per-table index capacity: ``[x (B x ceil4(dense)) f32 | labels f32
+  | offsets (T x (B+1)) i64 | indices (sum of capacities) i64 | weights f32]``,
+  16-byte aligned sections.  The step engine's input sets, packed pinned host
+  blocks and the prefetcher's device ring all use it, so moving a batch is a
+  single ``copy_``.
+* ``Prefetcher`` wraps an iterator of host batches: worker threads pack each
+  batch into a reused pinned block (the large copies release the GIL and run
+  in parallel), a copy stream moves it into a device ring slot, and the
+  iteration yields ``(dense_x, batches, labels)`` handles that ``train_step``
+  accepts in place of the arrays (same call, same result).  The step then
+  needs one device-to-device copy of the landed block.
+"""
+
+from __future__ import annotations
+
+import queue
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import torch
+
+__all__ = ["InputLayout", "Prefetcher", "StagedDense", "StagedSparse", "StagedLabels"]
+
+
+def _ceil4(n: int) -> int:
+    return (n + 3) // 4 * 4
+
+
+class InputLayout:
+    """Sections of one step's input block (see the module docstring)."""
+
+    def __init__(self, batch: int, num_tables: int, dense_dim: int, capacities,
+                 weighted: bool = False):
+        self.B, self.T, self.k0 = int(batch), int(num_tables), int(dense_dim)
+        self.caps = [max(1, int(c)) for c in capacities]
+        if len(self.caps) != self.T:
+            raise ValueError("one capacity per table")
+        self.weighted = bool(weighted)
+        self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
+        a16 = lambda n: (n + 15) // 16 * 16
+        B, T, ncap = self.B, self.T, int(self.cap_base[-1])
+        self.sections = {}
+        o = 0
+        for name, nbytes in (("x", B * _ceil4(self.k0) * 4), ("labels", B * 4),
+                             ("offsets", T * (B + 1) * 8), ("indices", ncap * 8),
+                             ("iweights", ncap * 4 if self.weighted else 0)):
+            self.sections[name] = (o, nbytes)
+            o = a16(o + nbytes)
+        self.nbytes = o
+
+    def key(self):
+        return (self.B, self.T, self.k0, tuple(self.caps), self.weighted)
+
+    # ------------------------------------------------------------------
+    def views(self, blk: torch.Tensor) -> dict:
+        """Typed torch views of a block (host or device)."""
+        B, T, ncap = self.B, self.T, int(self.cap_base[-1])
+
+        def view(name, dtype, shape):
+            o, n = self.sections[name]
+            if n == 0:
+                return None
+            return blk[o:o + n].view(dtype).view(*shape)
+        return {"block": blk,
+                "x": view("x", torch.float32, (B, _ceil4(self.k0))),
+                "labels": view("labels", torch.float32, (B,)),
+                "offsets": view("offsets", torch.int64, (T, B + 1)),
+                "indices": view("indices", torch.int64, (ncap,)),
+                "iweights": view("iweights", torch.float32, (ncap,))}
+
+    def _np(self, arr: np.ndarray, name, dtype, shape):
+        o, n = self.sections[name]
+        return arr[o:o + n].view(dtype).reshape(shape)
+
+    def check(self, indices, weights=None):
+        for t in range(self.T):
+            n = int(np.asarray(indices[t]).shape[0])
+            if n > self.caps[t]:
+                raise OverflowError(f"table {t}: {n} indices exceed capacity {self.caps[t]}")
+        if weights is not None and any(w is not None for w in weights) and not self.weighted:
+            raise ValueError("weighted bags need a weighted input layout")
+
+    def pack(self, blk: torch.Tensor, dense, offsets, indices, labels, weights=None,
+             pool: ThreadPoolExecutor | None = None) -> torch.Tensor:
+        """Write one batch of host arrays into the (pinned) host block ``blk``
+        (reused; returns it).  With ``pool`` the dense rows (in row slabs) and
+        every table's offsets / indices are copied by the pool's threads."""
+        self.check(indices, weights)
+        a = blk.numpy()
+        B, T = self.B, self.T
+        x = self._np(a, "x", np.float32, (B, _ceil4(self.k0)))
+        offs = self._np(a, "offsets", np.int64, (T, B + 1))
+        idx = self._np(a, "indices", np.int64, (int(self.cap_base[-1]),))
+        wv = self._np(a, "iweights", np.float32, (int(self.cap_base[-1]),)) \
+            if self.weighted else None
+        dense = np.asarray(dense)
+        if dense.shape != (B, self.k0):
+            raise ValueError(f"dense input {dense.shape} != {(B, self.k0)}")
+        jobs = []
+
+        def dense_rows(lo, hi):
+            np.copyto(x[lo:hi, :self.k0], dense[lo:hi], casting="unsafe")
+
+        def table(t):
+            np.copyto(offs[t], np.asarray(offsets[t]), casting="unsafe")
+            i = np.asarray(indices[t])
+            cb = int(self.cap_base[t])
+            np.copyto(idx[cb:cb + i.shape[0]], i, casting="unsafe")
+            if wv is not None:
+                w = None if weights is None else weights[t]
+                if w is None:
+                    wv[cb:cb + i.shape[0]] = 1.0
+                else:
+                    np.copyto(wv[cb:cb + i.shape[0]], np.asarray(w), casting="unsafe")
+
+        slabs = 4 if pool is not None and B >= 256 else 1
+        step = (B + slabs - 1) // slabs
+        for lo in range(0, B, step):
+            jobs.append((dense_rows, (lo, min(B, lo + step))))
+        for t in range(T):
+            jobs.append((table, (t,)))
+        if pool is None:
+            for fn, args in jobs:
+                fn(*args)
+        else:
+            for f in [pool.submit(fn, *args) for fn, args in jobs]:
+                f.result()
+        np.copyto(self._np(a, "labels", np.float32, (B,)), np.asarray(labels), casting="unsafe")
+        return blk
+
+    def new_host_block(self) -> torch.Tensor:
+        blk = torch.zeros(self.nbytes, dtype=torch.uint8).pin_memory()
+        if self.weighted:
+            self.views(blk)["iweights"].fill_(1.0)
+        return blk
+
+
+# ----------------------------------------------------------------------------
+# staged-batch handles (what a Prefetcher yields in place of the arrays)
+
+class _Slot:
+    def __init__(self, layout: InputLayout, device):
+        self.host = layout.new_host_block()
+        self.dev = torch.empty(layout.nbytes, dtype=torch.uint8, device=device)
+        self.h2d_done = torch.cuda.Event()   # host block may be repacked
+        self.ready = torch.cuda.Event()      # device block holds the batch
+        self.consumed = torch.cuda.Event()   # the step copied it out
+        self.consumed_set = False
+
+
+class StagedDense:
+    """Stands for the dense rows of a staged batch (``shape`` like the array)."""
+
+    def __init__(self, slot: _Slot, layout: InputLayout, pf: "Prefetcher"):
+        self._slot, self._layout, self._pf = slot, layout, pf
+        self.shape = (layout.B, layout.k0)
+
+    def consume(self, engine_block: torch.Tensor, stream=None):
+        """Copy the landed block into the engine's input block on ``stream``
+        (after the H2D copy) and release the ring slot."""
+        s = stream or torch.cuda.current_stream()
+        s.wait_event(self._slot.ready)
+        with torch.cuda.stream(s):
+            engine_block.copy_(self._slot.dev, non_blocking=True)
+        self._slot.consumed.record(s)
+        self._slot.consumed_set = True
+        self._pf._release(self._slot)
+
+
+class StagedSparse:
+    """Stands for one table's SparseBatch of a staged batch (the attributes
+    train_step validates: segments, nnz, weights)."""
+
+    def __init__(self, num_segments: int, nnz: int, weighted: bool):
+        self.num_segments, self.nnz = num_segments, nnz
+        self.weights = True if weighted else None
+
+
+class StagedLabels:
+    def __init__(self, n):
+        self.shape = (n,)
+
+
+class Prefetcher:
+    """Iterate ``(dense_x, batches, labels)`` staged handles over host batches.
+
+    ``source`` yields ``(dense, offsets_list, indices_list, labels)`` numpy
+    tuples, or objects with those attributes (``rng.HostBatch``).
+    ``capacities`` bounds each table's index count (the layout is static so
+    the step engine can replay one CUDA graph); default: the largest count of
+    the first batch + 25%.  ``depth`` ring slots are in flight; ``threads``
+    pack each batch in parallel."""
+
+    def __init__(self, source, batch_size: int, num_tables: int, dense_dim: int,
+                 capacities=None, depth: int = 3, threads: int = 8, weighted: bool = False,
+                 device=None):
+        self._src = iter(source)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self._first = None
+        if capacities is None:
+            self._first = self._next_host()
+            if self._first is None:
+                raise ValueError("empty source")
+            capacities = [max(batch_size, int(1.25 * np.asarray(i).shape[0]) + 1)
+                          for i in self._first[2]]
+        self.layout = InputLayout(batch_size, num_tables, dense_dim, capacities, weighted)
+        self._pool = ThreadPoolExecutor(max(1, int(threads)))
+        self._free = queue.Queue()
+        self._ready = queue.Queue(maxsize=depth)
+        for _ in range(max(2, int(depth))):
+            self._free.put(_Slot(self.layout, self.device))
+        self._stop = False
+        self._worker = threading.Thread(target=self._run, daemon=True)
+        self._worker.start()
+
+    def _next_host(self):
+        try:
+            b = next(self._src)
+        except StopIteration:
+            return None
+        if hasattr(b, "dense"):
+            return (b.dense, b.offsets, b.indices, b.labels, getattr(b, "weights", None))
+        return tuple(b) + ((None,) if len(b) == 4 else ())
+
+    def _run(self):
+        torch.cuda.set_device(self.device)
+        stream = torch.cuda.Stream(device=self.device)
+        try:
+            while not self._stop:
+                hb = self._first if self._first is not None else self._next_host()
+                self._first = None
+                if hb is None:
+                    break
+                slot = self._free.get()
+                if slot.consumed_set:
+                    stream.wait_event(slot.consumed)   # the step copied it out
+                slot.h2d_done.synchronize()             # the host block is free
+                dense, offs, idx, labels, weights = hb
+                self.layout.pack(slot.host, dense, offs, idx, labels, weights, self._pool)
+                with torch.cuda.stream(stream):
+                    slot.dev.copy_(slot.host, non_blocking=True)
+                    slot.h2d_done.record(stream)
+                    slot.ready.record(stream)
+                nnz = [int(np.asarray(i).shape[0]) for i in idx]
+                self._ready.put((slot, nnz, weights is not None))
+        except BaseException as e:  # surface worker errors to the consumer
+            self._ready.put(e)
+            return
+        self._ready.put(None)
+
+    def _release(self, slot):
+        self._free.put(slot)
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        item = self._ready.get()
+        if item is None:
+            self._ready.put(None)
+            raise StopIteration
+        if isinstance(item, BaseException):
+            raise item
+        slot, nnz, weighted = item
+        L = self.layout
+        dense = StagedDense(slot, L, self)
+        return dense, [StagedSparse(L.B, n, weighted) for n in nnz], StagedLabels(L.B)
+
+    def close(self):
+        self._stop = True
+        self._pool.shutdown(wait=False)

@@ -37,6 +37,7 @@ import torch
 from . import _lib
 from .embedding import LookupIndexError, SparseBatch
 from .model import DlrmModel, ceil4
+from .pipeline import InputLayout
 
 __all__ = ["StepEngine", "StepResult"]
 
@@ -124,24 +125,17 @@ class StepEngine:
                 tab.weights = v
 
         # ---- inputs: one contiguous block per input set, laid out exactly
-        # like a packed host batch (pack_host_batch) so a step's inputs move
-        # with ONE copy; views x / labels / offsets / indices (/ weights)
+        # like a packed host batch (pipeline.InputLayout) so a step's inputs
+        # move with ONE copy; views x / labels / offsets / indices (/ weights)
         self.k0 = cfg.dense_dim
-        self.cap_base = np.concatenate([[0], np.cumsum(self.caps)]).astype(np.int64)
-        a16 = lambda n: (n + 15) // 16 * 16
-        lay = {}
-        o = 0
-        for name, nbytes in (("x", B * ceil4(self.k0) * 4), ("labels", B * 4),
-                             ("offsets", T * (B + 1) * 8),
-                             ("indices", int(self.cap_base[-1]) * 8),
-                             ("iweights", int(self.cap_base[-1]) * 4 if weighted else 0)):
-            lay[name] = (o, nbytes)
-            o = a16(o + nbytes)
-        self.block_layout, self.block_bytes = lay, o
+        self.input_layout = InputLayout(B, T, self.k0, self.caps, weighted)
+        self.cap_base = self.input_layout.cap_base
+        self.block_layout = self.input_layout.sections
+        self.block_bytes = self.input_layout.nbytes
         self.input_sets = []
         for _ in range(max(1, int(input_sets))):
-            blk = torch.zeros(o, dtype=torch.uint8, device=dev)
-            v = self._views(blk)
+            blk = torch.zeros(self.block_bytes, dtype=torch.uint8, device=dev)
+            v = self.input_layout.views(blk)
             if weighted:
                 v["iweights"].fill_(1.0)
             self.input_sets.append(v)
@@ -229,25 +223,13 @@ class StepEngine:
         self.use_set(0)
         self._build_descs()
         self.graph = None
+        self.timed_graphs = {}
+        self._timed_runs = {}
         self.eval_graphs = {}
         self._eval_runs = 0
         self.launches_per_step = None
 
     # ------------------------------------------------------------------
-    def _views(self, blk):
-        B, T, lay = self.B, self.T, self.block_layout
-        def view(name, dtype, shape):
-            o, n = lay[name]
-            if n == 0:
-                return None
-            return blk[o:o + n].view(dtype).view(*shape)
-        return {"block": blk,
-                "x": view("x", torch.float32, (B, ceil4(self.k0))),
-                "labels": view("labels", torch.float32, (B,)),
-                "offsets": view("offsets", torch.int64, (T, B + 1)),
-                "indices": view("indices", torch.int64, (int(self.cap_base[-1]),)),
-                "iweights": view("iweights", torch.float32, (int(self.cap_base[-1]),))}
-
     def _make_descs(self, v):
         d = self.d
         descs = []
@@ -271,26 +253,13 @@ class StepEngine:
         self._descs, self._descs_p = v["descs"]
         self.graph = self.graphs.get(k)
 
-    def pack_host_batch(self, dense, offsets, indices, labels, weights=None):
-        """One pinned host buffer in the input-block layout (done once per
-        batch by the data pipeline; a step then needs a single H2D copy)."""
-        blk = torch.zeros(self.block_bytes, dtype=torch.uint8).pin_memory()
-        v = self._views(blk)
-        v["x"][:, :self.k0].copy_(torch.as_tensor(np.asarray(dense, np.float32)))
-        v["labels"].copy_(torch.as_tensor(np.asarray(labels, np.float32)))
-        for t in range(self.T):
-            v["offsets"][t].copy_(torch.as_tensor(np.asarray(offsets[t], np.int64)))
-            i = np.asarray(indices[t], np.int64)
-            if i.size > self.caps[t]:
-                raise OverflowError(f"table {t}: {i.size} indices exceed capacity "
-                                    f"{self.caps[t]}")
-            cb = int(self.cap_base[t])
-            v["indices"][cb:cb + i.size].copy_(torch.as_tensor(i))
-            if self.weighted:
-                w = np.ones(i.size, np.float32) if weights is None or weights[t] is None \
-                    else np.asarray(weights[t], np.float32)
-                v["iweights"][cb:cb + i.size].copy_(torch.as_tensor(w))
-        return blk
+    def pack_host_batch(self, dense, offsets, indices, labels, weights=None, out=None,
+                        pool=None):
+        """The batch in the input-block layout in pinned host memory (``out``:
+        a block to reuse, e.g. from a ring; ``pool``: a thread pool for the
+        copies), so a step needs a single H2D copy."""
+        blk = out if out is not None else self.input_layout.new_host_block()
+        return self.input_layout.pack(blk, dense, offsets, indices, labels, weights, pool)
 
     def stage(self, packed: torch.Tensor, k: int = 0, stream=None):
         """Copy a packed batch (pinned host or device) into input set k."""
@@ -358,12 +327,8 @@ class StepEngine:
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
-            sh = _lib.stream_handle(self.side)
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
-                 P(self.emb_ws), self.emb_ws_bytes, sh)
-            # the keys pass records every bad position: resolve the values
-            # here, off the critical path
-            self._resolve(sh)
+                 P(self.emb_ws), self.emb_ws_bytes, _lib.stream_handle(self.side))
             done = torch.cuda.Event()
             done.record(self.side)
             return done
@@ -403,8 +368,15 @@ class StepEngine:
             self.wg_stream.wait_event(ev)
             call("dlrm_linear_bwd_weight_upd", *args, wg)
 
+        looked_up = None
         if emb_side:
-            emb_fwd(fork(self.fwd_stream))
+            fh = fork(self.fwd_stream)
+            emb_fwd(fh)
+            looked_up = torch.cuda.Event()
+            looked_up.record(self.fwd_stream)
+            # the offending index values (if any) from the batch that ran:
+            # resolved on the lookup stream, which only rejoins at the end
+            self._resolve(fh)
 
         # bottom MLP forward; the last layer writes feature 0 of Z
         mark("bottom_mlp_fwd")
@@ -420,9 +392,10 @@ class StepEngine:
         # pooled lookups -> features 1..T of Z
         mark("embedding_fwd")
         if emb_side:
-            join(self.fwd_stream)
+            main.wait_event(looked_up)
         else:
             emb_fwd(s)
+            self._resolve(s)
         if self.prep_at == "after_fwd":
             prep_done = fork_prepare()
         # interaction -> R
@@ -527,6 +500,8 @@ class StepEngine:
                       None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
         # sparse backward fused with the row-wise SGD update
         mark("embedding_bwd_sgd")
+        if looked_up is not None:
+            join(self.fwd_stream)
         if wg is not None:
             join(self.wg_stream)  # the next step reads the updated weights
         if apply_done is not None:
@@ -535,12 +510,71 @@ class StepEngine:
         if prep_done is None:
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,
                  P(self.emb_ws), self.emb_ws_bytes, s)
-            self._resolve(s)
         else:
             main.wait_event(prep_done)
         call("dlrm_emb_bwd_apply", P(self.W_all), d, self._descs_p, self.T, B,
              P(self.gZ), nf * d, ue, ef, self.total_rows, P(self.emb_ws),
              self.emb_ws_bytes, s)
+
+    # reference operator category of each stage (ref parallel.py:254-285;
+    # the fused updates have no stage of their own, see timing.py)
+    CATEGORY = {"bottom_mlp_fwd": "bottom_mlp", "embedding_fwd": "embedding_lookup",
+                "interaction_fwd": "interaction", "top_mlp_fwd": "top_mlp",
+                "loss_head": "loss", "top_mlp_bwd": "top_mlp",
+                "interaction_bwd": "interaction", "bottom_mlp_bwd": "bottom_mlp",
+                "embedding_bwd_sgd": "embedding_lookup"}
+
+    def run_timed(self, use_graph: bool = True) -> dict:
+        """One training step with CUDA-event marks at the stage boundaries
+        (the stages serialised on one stream, same kernels, same results);
+        returns {stage: ms}.  From the second call per input set on, a
+        captured copy of the marked step is replayed (event-record nodes in
+        the graph), so host launch overhead does not enter the times."""
+        k = self._set
+        entry = self.timed_graphs.get(k)
+
+        def make_mark(evs, external):
+            def mark(name):
+                e = None
+                if external:
+                    try:
+                        e = torch.cuda.Event(enable_timing=True, external=True)
+                    except TypeError:
+                        e = None
+                if e is None:
+                    e = torch.cuda.Event(enable_timing=True)
+                e.record(torch.cuda.current_stream())
+                evs.append((name, e))
+            return mark
+
+        if entry is None and use_graph and self._timed_runs.get(k, 0) >= 1:
+            evs = []
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            try:
+                mark = make_mark(evs, True)
+                with _lib.capture_guard(), torch.cuda.graph(g):
+                    self.launch(mark=mark)
+                    mark("end")
+                entry = (g, evs)
+            except Exception:
+                torch.cuda.synchronize()
+                entry = False   # event nodes unavailable: eager marks from now on
+            self.timed_graphs[k] = entry
+        if entry:
+            g, evs = entry
+            g.replay()
+        else:
+            evs = []
+            mark = make_mark(evs, False)
+            self.launch(mark=mark)
+            mark("end")
+            self._timed_runs[k] = self._timed_runs.get(k, 0) + 1
+        evs[-1][1].synchronize()
+        out = {}
+        for (name, e), (_, nxt) in zip(evs[:-1], evs[1:]):
+            out[name] = out.get(name, 0.0) + e.elapsed_time(nxt)
+        return out
 
     # ------------------------------------------------------------------
     def capture(self):

@@ -42,10 +42,31 @@ def test_reference_arm_line():
 
 
 def test_reference_arm_other_ranks_exit_quietly():
-    r = _run(["--impl", "reference", "--config", "c1", "--steps", "2"],
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--gpus", "2"],
              env={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}, timeout=120)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip() == ""
+
+
+def test_world_size_must_match_gpus():
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "2", "--gpus", "4"],
+             env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"}, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+def test_gpus_n_launches_n_ranks_itself():
+    """`bench.py --gpus 2` (no WORLD_SIZE) re-launches itself under
+    torch.distributed.run: two ranks, rank 0 alone prints the line."""
+    e = {k: v for k, v in os.environ.items()
+         if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "c1", "--steps", "2", "--warmup", "1", "--gpus", "2"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["impl"] == "reference"
 
 
 def test_our_arm_needs_the_gpu():

@@ -81,7 +81,7 @@ def _worker(rank, world, port, tables, batch, d, q):
         plan = DevicePlan(world, partition_tables([m * d for m in tables], world),
                           shard_bounds(batch, world))
         L = ExchangeLayout(plan, rank, d)
-        ex = NcclExchange(L, None, dist.new_group(list(range(world))))
+        ex = NcclExchange(L)
         full, grads = reference_data(plan, d)
         recv = torch.zeros(max(L.recv_numel, 1))
         ex.forward(pack_send(L, full), recv[:L.recv_numel])

@@ -96,7 +96,8 @@ def test_bad_index_raises_with_device_and_mutates_nothing(golden):
         assert np.array_equal(x, y)
 
 
-def test_hybrid_trainer_nccl_one_process(golden):
+@pytest.mark.parametrize("force", [False, True])
+def test_hybrid_trainer_nccl_one_process(golden, force):
     """HybridTrainer over a real NCCL communicator (one process, one GPU):
     the all-to-alls, the overlapped allreduces, the no-sync step and the
     deferred error check run through the multi-process code path and give
@@ -117,8 +118,10 @@ def test_hybrid_trainer_nccl_one_process(golden):
         model = build(c)
         plan = make_plan(model.config, c["batch"], 1)
         caps = [max(len(hb.indices[t]) for hb in batches) for t in range(len(c["tables"]))]
-        tr = HybridTrainer(model, plan, 0, caps, lr=c["lr"],
-                           ar_group=dist.new_group([0]))
+        # force: the multi-rank path (collectives on the comm stream, unfused
+        # updates after the gradient allreduce) with a one-rank communicator;
+        # else the one-rank path (no collectives, fused updates)
+        tr = HybridTrainer(model, plan, 0, caps, lr=c["lr"], force_exchange=force)
         ref_model = build(c)
         opt = Sgd(c["lr"])
         for k, hb in enumerate(batches):
@@ -138,6 +141,8 @@ def test_hybrid_trainer_nccl_one_process(golden):
             sparse = [SparseBatch(o, i) for o, i in zip(hb.offsets, hb.indices)]
             s = train_step(ref_model, hb.dense.astype(np.float32), sparse, hb.labels, opt)
             assert abs(r.loss - s.loss) <= 1e-6 * abs(s.loss), (k, r.loss, s.loss)
+            if not force:   # the same kernels as the fused step, in the same order
+                assert r.loss == s.loss
         # a graph holding NCCL work must be released before the communicator
         tr.graph = None
         del tr

@@ -103,3 +103,91 @@ def test_random_source_fixed_and_variable():
         lens = np.diff(o)
         assert lens.min() >= 1 and lens.max() <= 4 and o[-1] == i.size
         assert i.min() >= 0 and i.max() < m
+
+
+def test_stage_timer_api():
+    # ref timing.py:9-36
+    import time
+    from paper_1906_00091_b200.timing import NullTimer, StageTimer, add_seconds
+    t = StageTimer()
+    with t.section("a"):
+        time.sleep(0.01)
+    t.add("b", 0.5)
+    add_seconds(t, {"b": 0.25, "c": 1.0})
+    assert t.seconds["a"] >= 0.01 and t.seconds["b"] == 0.75 and t.seconds["c"] == 1.0
+    assert abs(t.total() - sum(t.seconds.values())) < 1e-12
+    n = NullTimer()
+    with n.section("x"):
+        pass
+    add_seconds(n, {"x": 1.0})
+    assert n.total() == 0.0
+
+    class RefLike:  # the reference's StageTimer has only .seconds / .section
+        def __init__(self):
+            self.seconds = {}
+    r = RefLike()
+    add_seconds(r, {"loss": 0.5})
+    add_seconds(r, {"loss": 0.5})
+    assert r.seconds == {"loss": 1.0}
+
+
+def test_input_layout_pack_serial_and_threaded():
+    """One step's inputs as one block (pipeline.InputLayout): every section
+    round-trips, the threaded pack equals the serial one, capacities bound."""
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+    from paper_1906_00091_b200.pipeline import InputLayout
+    from paper_1906_00091_b200.rng import RandomBatchSource
+    src = RandomBatchSource([50, 70, 90], 13, 300, 5, False, seed=3)
+    hb = src.next_batch()
+    caps = [len(i) + 7 for i in hb.indices]
+    for weighted in (False, True):
+        L = InputLayout(300, 3, 13, caps, weighted)
+        w = [np.linspace(0.5, 1.5, len(i)) for i in hb.indices] if weighted else None
+        a = torch.zeros(L.nbytes, dtype=torch.uint8)
+        b = torch.zeros(L.nbytes, dtype=torch.uint8)
+        L.pack(a, hb.dense, hb.offsets, hb.indices, hb.labels, w)
+        with ThreadPoolExecutor(4) as pool:
+            L.pack(b, hb.dense, hb.offsets, hb.indices, hb.labels, w, pool)
+        assert torch.equal(a, b)
+        v = L.views(a)
+        assert np.array_equal(v["x"][:, :13].numpy(), hb.dense.astype(np.float32))
+        assert np.array_equal(v["labels"].numpy(), hb.labels.astype(np.float32))
+        for t in range(3):
+            assert np.array_equal(v["offsets"][t].numpy(), hb.offsets[t])
+            cb = int(L.cap_base[t])
+            assert np.array_equal(v["indices"][cb:cb + len(hb.indices[t])].numpy(), hb.indices[t])
+            if weighted:
+                assert np.array_equal(v["iweights"][cb:cb + len(hb.indices[t])].numpy(),
+                                      w[t].astype(np.float32))
+        assert L.sections["x"][0] == 0 and all(o % 16 == 0 for o, _ in L.sections.values())
+    L = InputLayout(300, 3, 13, [5, 5, 5])
+    with pytest.raises(OverflowError):
+        L.pack(torch.zeros(L.nbytes, dtype=torch.uint8), hb.dense, hb.offsets, hb.indices,
+               hb.labels)
+
+
+def test_traffic_balanced_plan():
+    """policy="traffic": equal-traffic tables spread evenly whatever their
+    sizes (the reference plan gives one of 8 GPUs 19 of the 26 Criteo-Kaggle
+    tables); memory capacity is respected; the default stays the reference
+    plan."""
+    from bench import KAGGLE
+    from paper_1906_00091_b200.parallel import partition_tables_by_traffic
+    cfg = DlrmConfig(KAGGLE, 16, [13, 512, 256, 64, 16], [512, 256, 1])
+    ref = make_plan(cfg, 2048 * 8, 8)
+    counts = np.bincount(ref.table_assignment, minlength=8)
+    assert counts.max() == 19
+    tp = make_plan(cfg, 2048 * 8, 8, policy="traffic")
+    counts = np.bincount(tp.table_assignment, minlength=8)
+    assert counts.max() - counts.min() <= 1 and counts.sum() == 26
+    assert make_plan(cfg, 2048 * 8, 8).table_assignment == ref.table_assignment
+    # capacity: two big tables may not share a device
+    own = partition_tables_by_traffic([1, 1, 1, 1], [10, 10, 1, 1], 2, capacity_bytes=11)
+    assert own[0] != own[1]
+    with pytest.raises(ValueError):
+        partition_tables_by_traffic([1, 1], [10, 10], 1, capacity_bytes=15)
+    # heavier pooling attracts fewer co-owned tables
+    cfg2 = DlrmConfig([100] * 4, 8, [4, 8], [4, 1])
+    p2 = make_plan(cfg2, 64, 2, policy="traffic", pooling=[100, 1, 1, 1])
+    assert p2.table_assignment.count(p2.table_assignment[0]) == 1
