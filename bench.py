@@ -531,7 +531,8 @@ def run_ours(args, c, rank, world, dist):
                     "ms_per_step": e2e_api["ms"] / K,
                     "path": "train_step(model, dense, batches, labels, Sgd) on Prefetcher "
                             "batches packed from the reference's numpy arrays; loss read "
-                            "back every step", "loss_last": e2e_api["loss_last"]},
+                            "back every step", "loss_last": e2e_api["loss_last"],
+                    "input_wait_ms_per_step": e2e_api["input_wait_ms"]},
             "e2e_engine": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d_bytes,
                            "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms / K,
                            "path": "StepEngine: pre-packed pinned blocks, H2D of step s+1 "
@@ -573,8 +574,11 @@ def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
     torch.cuda.synchronize()
     e0.record(stream)
     loss = None
+    waited = 0.0
     for _ in range(K):
+        t0 = time.perf_counter()
         d, b, l = next(it)
+        waited += time.perf_counter() - t0
         loss = train_step(model, d, b, l, opt).loss
     e1.record(stream)
     torch.cuda.synchronize()
@@ -584,7 +588,8 @@ def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    return {"ms": ms, "h2d_bytes": int(pf.layout.nbytes), "loss_last": loss}
+    return {"ms": ms, "h2d_bytes": int(pf.layout.nbytes), "loss_last": loss,
+            "input_wait_ms": waited * 1e3 / K}
 
 
 def rank_batches(c, plan, rank, P, seed):

@@ -717,6 +717,15 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
 
 bool tc_enabled() { return g_tc_mode == 0; }
 
+bool tma_encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
+                   int64_t ld_elems, int box_inner, int box_outer, int swizzle) {
+  if (!aligned16(base) || (ld_elems % 4) != 0) return false;
+  const CUtensorMapSwizzle swz = swizzle == 1   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle == 2 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return encode(map, base, inner, outer, ld_elems, box_inner, box_outer, swz);
+}
+
 namespace {
 // split-K clusters of a forward / data-gradient GEMM: partial tiles reduced
 // over DSMEM, then the normal epilogue

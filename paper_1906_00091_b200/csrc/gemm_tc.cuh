@@ -3,6 +3,8 @@
 // the tensor-core kernels take; otherwise the SIMT path runs.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace dlrm {
@@ -10,6 +12,12 @@ namespace dlrm {
 // false after dlrm_gemm_mode(1): every tensor-core kernel (GEMMs and the
 // interaction) is replaced by its SIMT fp32 counterpart (A/B tests)
 bool tc_enabled();
+
+// 2D fp32 tensor map (row-major, ld_elems per row) for TMA loads of
+// box_inner x box_outer boxes; swizzle 0 none, 1 128B (K-major MMA tiles),
+// 2 128B with 32-byte atoms (MN-major tf32 tiles).  False if not encodable.
+bool tma_encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
+                   int64_t ld_elems, int box_inner, int box_outer, int swizzle);
 
 bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw,
                       const float* Y, int64_t ldy, int64_t M, int64_t N,
