@@ -560,8 +560,11 @@ def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
         while True:
             yield hbs[s % len(hbs)]
             s += 1
+    # 4 packing threads: measured best on the 16-core GPU hosts (more threads
+    # contend with the stepping thread: 0.57 / 0.74 / 0.86 ms per step at
+    # 4 / 8 / 16, scripts/e2e_prof.py)
     pf = Prefetcher(source(), B, T, cfg.dense_dim, capacities=caps, depth=3,
-                    threads=min(8, max(1, (os.cpu_count() or 2) // 2)))
+                    threads=min(4, max(1, (os.cpu_count() or 2) // 4)))
     it = iter(pf)
     opt = Sgd(0.1)
     for _ in range(warmup + 2):   # eager step, graph capture, warm-up

@@ -329,6 +329,33 @@ int64_t dlrm_criteo_parse(const char* text, int64_t nbytes, const int64_t* vocab
  * no key, digest bytes read little-endian. */
 uint64_t dlrm_blake2b64(const void* data, int64_t nbytes);
 
+/* ---- input pipeline: the reference's random source (host code) ---------
+ * Variable-length bags of the reference's random batches (dlrmkit
+ * datagen.py:79-96 through cli.py:294-314), bit-identical to numpy:
+ * per table t and sample j a length uniform in [1, k] then that many row
+ * indices uniform in [0, rows[t]), drawn from numpy's Philox stream whose
+ * state (Generator.bit_generator.state: counter[4], key[2], buffer[4],
+ * buffer_pos, has_uint32, uinteger) is passed in `state` and advanced in
+ * place.  offsets_out: [nt][batch + 1] (CSR, terminal entry included);
+ * indices_out: [nt][batch * k] (the first nnz_out[t] of each row live).
+ * rows[t] < 2^32.  Host pointers.  Returns 0, or 1 for bad arguments. */
+int dlrm_random_bags(uint64_t* state, const int64_t* rows, int32_t nt, int64_t batch, int64_t k,
+                     int64_t* offsets_out, int64_t* indices_out, int64_t* nnz_out);
+
+/* One batch of the reference's host arrays packed into a step's input block
+ * (the layout of paper_1906_00091_b200.pipeline.InputLayout; sec[] = byte
+ * offsets of the x, labels, offsets, indices and per-index-weight sections,
+ * the last -1 when unweighted): dense float64 rows -> fp32 (pitch ldx
+ * floats), labels float64 -> fp32, offsets / indices int64 copied (table t's
+ * indices at slot cap_base[t]), weights float64 -> fp32 (NULL table entry:
+ * ones).  Runs on nthreads native threads.  Host pointers; 0 ok, 1 bad
+ * arguments (an index count above its capacity included). */
+int dlrm_pack_batch(uint8_t* dst, const int64_t* sec, int64_t batch, int64_t k0, int64_t ldx,
+                    int32_t nt, const int64_t* cap_base, const double* dense, int64_t ld_dense,
+                    const double* labels, const int64_t* const* offsets,
+                    const int64_t* const* indices, const int64_t* nnz,
+                    const double* const* weights, int32_t nthreads);
+
 /* Count of this library's kernel launches since load (for bench.py). */
 int64_t dlrm_launch_count(void);
 const char* dlrm_last_error(void);

@@ -95,7 +95,7 @@ _SIZE_FNS = {
 # every symbol include/dlrm_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = sorted(list(_SIGS) + list(_SIZE_FNS) + [
     "dlrm_launch_count", "dlrm_last_error", "dlrm_build_info", "dlrm_criteo_parse",
-    "dlrm_blake2b64"])
+    "dlrm_blake2b64", "dlrm_random_bags", "dlrm_pack_batch"])
 
 _lib = None
 
@@ -122,6 +122,11 @@ def lib():
                                         _i64, _vp, _i32]
         L.dlrm_criteo_parse.restype = _i64
         L.dlrm_blake2b64.argtypes, L.dlrm_blake2b64.restype = [_vp, _i64], C.c_uint64
+        L.dlrm_random_bags.argtypes = [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]
+        L.dlrm_random_bags.restype = _i32
+        L.dlrm_pack_batch.argtypes = [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp,
+                                      _vp, _vp, _vp, _vp, _i32]
+        L.dlrm_pack_batch.restype = _i32
         L.dlrm_last_error.restype = C.c_char_p
         L.dlrm_build_info.restype = C.c_char_p
         _lib = L

@@ -96,6 +96,9 @@ class InputLayout:
         (reused; returns it).  With ``pool`` the dense rows (in row slabs) and
         every table's offsets / indices are copied by the pool's threads."""
         self.check(indices, weights)
+        if self._pack_native(blk, dense, offsets, indices, labels, weights,
+                             pool._max_workers if pool is not None else 1):
+            return blk
         a = blk.numpy()
         B, T = self.B, self.T
         x = self._np(a, "x", np.float32, (B, _ceil4(self.k0)))
@@ -137,6 +140,50 @@ class InputLayout:
                 f.result()
         np.copyto(self._np(a, "labels", np.float32, (B,)), np.asarray(labels), casting="unsafe")
         return blk
+
+    def _pack_native(self, blk, dense, offsets, indices, labels, weights, threads) -> bool:
+        """``dlrm_pack_batch`` (native threads, no GIL) when the arrays have
+        the reference's dtypes (float64 dense / labels / weights, int64
+        offsets / indices); False to use the numpy path."""
+        try:
+            import ctypes as C
+            from . import _lib
+            L = _lib.lib()
+        except Exception:
+            return False
+        dense = np.asarray(dense)
+        labels = np.asarray(labels)
+        offs = [np.asarray(o) for o in offsets]
+        idx = [np.asarray(i) for i in indices]
+        ws = None if weights is None else [None if w is None else np.asarray(w) for w in weights]
+        ok = (dense.dtype == np.float64 and dense.ndim == 2 and dense.strides[1] == 8
+              and dense.shape == (self.B, self.k0) and labels.dtype == np.float64
+              and labels.shape == (self.B,) and labels.strides[0] == 8
+              and all(o.dtype == np.int64 and o.flags.c_contiguous and o.shape == (self.B + 1,)
+                      for o in offs)
+              and all(i.dtype == np.int64 and i.flags.c_contiguous for i in idx)
+              and (ws is None or all(w is None or (w.dtype == np.float64 and w.flags.c_contiguous)
+                                     for w in ws)))
+        if not ok:
+            return False
+        T = self.T
+        p = lambda arr: arr.ctypes.data
+        sec = np.array([self.sections["x"][0], self.sections["labels"][0],
+                        self.sections["offsets"][0], self.sections["indices"][0],
+                        self.sections["iweights"][0] if self.weighted else -1], np.int64)
+        P = C.c_void_p * T
+        optr = P(*[p(o) for o in offs])
+        iptr = P(*[p(i) if i.size else 0 for i in idx])
+        nnz = np.array([i.shape[0] for i in idx], np.int64)
+        wptr = P(*[p(w) if w is not None else 0 for w in ws]) if ws is not None else None
+        rc = L.dlrm_pack_batch(C.c_void_p(blk.data_ptr()), C.c_void_p(p(sec)), self.B, self.k0,
+                               _ceil4(self.k0), T, C.c_void_p(p(self.cap_base)),
+                               C.c_void_p(p(dense)), dense.strides[0] // 8, C.c_void_p(p(labels)),
+                               C.cast(optr, C.c_void_p), C.cast(iptr, C.c_void_p),
+                               C.c_void_p(p(nnz)),
+                               C.cast(wptr, C.c_void_p) if wptr is not None else None,
+                               int(max(1, threads)))
+        return rc == 0
 
     def new_host_block(self) -> torch.Tensor:
         blk = torch.zeros(self.nbytes, dtype=torch.uint8).pin_memory()
@@ -202,7 +249,7 @@ class Prefetcher:
     pack each batch in parallel."""
 
     def __init__(self, source, batch_size: int, num_tables: int, dense_dim: int,
-                 capacities=None, depth: int = 3, threads: int = 8, weighted: bool = False,
+                 capacities=None, depth: int = 3, threads: int = 4, weighted: bool = False,
                  device=None):
         self._src = iter(source)
         self.device = device or torch.device("cuda", torch.cuda.current_device())

@@ -223,6 +223,7 @@ class StepEngine:
         self.use_set(0)
         self._build_descs()
         self.graph = None
+        self._res_host = None
         self.timed_graphs = {}
         self._timed_runs = {}
         self.eval_graphs = {}
@@ -760,10 +761,20 @@ class StepEngine:
                                            tab.num_rows)
 
     def result(self) -> StepResult:
-        self.check_errors()
-        st = self.stats.cpu()
-        return StepResult(float(st[0]) / self.B, float(st[1]) / self.B,
-                          self.prob.clone())
+        """StepResult of the last step: the error flag and the loss / correct
+        sums come back with ONE synchronisation (two async copies into a
+        pinned buffer); raises LookupIndexError after a bad index."""
+        if self._res_host is None:
+            self._res_host = torch.zeros(4, dtype=torch.float32).pin_memory()
+        s = torch.cuda.current_stream()
+        h = self._res_host
+        h[2:3].view(torch.int32).copy_(self.err_flag, non_blocking=True)
+        h[0:2].copy_(self.stats, non_blocking=True)
+        probs = self.prob.clone()
+        s.synchronize()
+        if int(h[2:3].view(torch.int32)[0]):
+            self.check_errors()
+        return StepResult(float(h[0]) / self.B, float(h[1]) / self.B, probs)
 
 
 def _to_dev(a, dtype, dev):

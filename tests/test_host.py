@@ -191,3 +191,21 @@ def test_traffic_balanced_plan():
     cfg2 = DlrmConfig([100] * 4, 8, [4, 8], [4, 1])
     p2 = make_plan(cfg2, 64, 2, policy="traffic", pooling=[100, 1, 1, 1])
     assert p2.table_assignment.count(p2.table_assignment[0]) == 1
+
+
+def test_native_random_bags_bit_identical_to_numpy():
+    """dlrm_random_bags replays numpy's Philox / Lemire draws: the native
+    variable-length bags equal the Python loop's (ref datagen.py:79-96),
+    including 1-row ranges, rows near 2^32 and the state left for the
+    labels and the next batch."""
+    from paper_1906_00091_b200.rng import RandomBatchSource
+    for tabs, k in (([10 ** 6] * 3, 100), ([7, 5, 9], 3), ([30, 10 ** 9, 2 ** 31 + 5, 2 ** 32 - 1], 7),
+                    ([1000, 1], 1)):
+        a = RandomBatchSource(tabs, 13, 300, k, False, seed=3)
+        b = RandomBatchSource(tabs, 13, 300, k, False, seed=3)
+        b.native = False
+        for _ in range(3):
+            x, y = a.next_batch(), b.next_batch()
+            assert np.array_equal(x.dense, y.dense) and np.array_equal(x.labels, y.labels)
+            for o1, o2, i1, i2 in zip(x.offsets, y.offsets, x.indices, y.indices):
+                assert np.array_equal(o1, o2) and np.array_equal(i1, i2)
