@@ -5,32 +5,25 @@
 //   interact           218-242  out = [z0 | z_i . z_j for i < j, row-major]
 //   interact_backward  245-268  g_i = [i==0] gout[:, :d] + sum_{j!=i} g_ij z_j
 //
-// Both directions stack S samples' feature rows into one R = S*nf row tile
-// (S chosen so the tile and its operands fit TMEM / shared memory) and run
-// ONE 128-row MMA chain per tile; only the S diagonal nf x nf blocks of the
-// products are used (the tensor pipe has ample headroom at these sizes: the
-// op is HBM-bound).  Operands are split x = hi + lo with hi =
-// x truncated to TF32 (what the tensor core reads of a raw fp32 operand) and
-// lo = nearest-TF32(x - hi); the dropped lo*lo term is 2^-22 relative.
+// Operands are split x = hi + lo with hi = x truncated to TF32 (what the
+// tensor core reads of a raw fp32 operand) and lo = nearest-TF32(x - hi);
+// the dropped lo*lo term is 2^-22 relative.  The tensor pipe has ample
+// headroom at these sizes (the op is HBM-bound), so both
+// directions spend MMA work on zero padding to keep the data movement simple.
 //
-// Forward, per tile (A and B both K-major over the embedding dim d):
-//   B = [Z | Z_lo] (2*Rp rows), A = Z (the raw rows are the hi operand)
-//   D = Z_hi [Z_hi | Z_lo]^T  ->  columns [0, Rp): hh_ij, [Rp, 2Rp): X_ij
-//   z_i . z_j = hh_ij + X_ij + X_ji      (X_ji = z_j,hi . z_i,lo)
-// so one N = 2Rp MMA per k-step gives all three 3xTF32 products.
+// Forward: S samples' feature rows stacked into one R = S*nf row tile, ONE
+// 128-row MMA chain per tile over the embedding dim (A = [Z_hi ; Z_lo] rows
+// in TMEM, B = the raw rows), keeping only the S diagonal nf x nf blocks:
+//   z_i . z_j = hh_ij + Y_ij + Y_ji   (Y_ij = z_i,lo . z_j,hi).
 //
-// Backward, per tile (A = the block-diagonal symmetric pair-gradient matrix
-// M = G + G^T in TMEM, K-major; B = Z, MN-major, rows = stacked features):
-//   D = [M_hi Z_hi | M_hi Z_lo + M_lo Z_hi]  (hh chain and the small terms in
-//   separate TMEM columns, added in the epilogue), then g_0 += gout[:, :d] and
-//   the bottom MLP's ReLU mask on feature 0 (training step only).
+// Backward: per sample D = Z^T M (M = G + G^T, zero diagonal) with the
+// embedding dim on the TMEM lanes, so each warp store of the epilogue is 32
+// consecutive floats of one gradient row; see interact_tc_bwd_kernel.
 //
 // Feature f of sample b is read at feat[f] + b*stride[f] (the pooled-embedding
-// buffer or the all-to-all receive buffer in place), with 16-byte cp.async
-// into the swizzled operand layouts.  One persistent CTA per SM:
-//   warps 0-3  epilogue (TMEM lane quarters); backward: also build A in TMEM
-//   warps 4-7  loaders (cp.async) + lo split
-//   warp  8    TMEM allocator + MMA issuer (one thread)
+// buffer or the all-to-all receive buffer in place): by TMA when the features
+// are the rows of one [batch * nf, d] matrix, else by 16-byte cp.async.  One
+// persistent CTA per SM, warp-specialised (roles listed at each kernel).
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -56,20 +49,15 @@ constexpr int IA_EPI = 128;      // epilogue warps 0-3
 constexpr uint32_t IA_TMEM_COLS = 512;
 constexpr size_t IA_SMEM_MAX = 220 * 1024;
 
-// host-computed tile geometry (passed by value)
+// host-computed forward tile geometry (passed by value)
 struct IaGeom {
   int nf, d, S, R, P;
-  int Pp;            // bwd: P rounded up to 4 (pair-gradient row pitch)
-  int Rp;            // fwd: R rounded up to 16 (B rows, MMA N; lo lanes of A at Rp)
-  int rows;          // fwd: rows per K-chunk region (= Rp)
-  int kchunks;       // fwd: ceil(d / 32)
+  int Rp;            // R rounded up to 16 (B rows, MMA N; lo lanes of A at Rp)
+  int rows;          // rows per K-chunk region (= Rp)
+  int kchunks;       // ceil(d / 32)
   int tma;           // 1: features are rows of one [batch * nf, d] matrix, loaded by TMA
-  int Kq;            // bwd: R rounded up to 16 (A slot columns)
-  int Kp;            // bwd: R rounded up to 8 (MMA K)
   int nst;           // stages
   uint32_t stage_bytes;
-  uint32_t b_bytes;  // bwd: operand bytes of a stage (the rest: pair gradients)
-  uint32_t a_base;   // bwd: TMEM column of the A slots
   uint32_t idesc;
 };
 
@@ -83,61 +71,8 @@ __device__ __forceinline__ void ia_pair(int p, int nf, int& i, int& j) {
   j = row + 1 + (p - base);
 }
 
-__device__ __forceinline__ float4 split_lo4(float4 v) {
-  return make_float4(
-      __uint_as_float(tf32_rna(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u))),
-      __uint_as_float(tf32_rna(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u))),
-      __uint_as_float(tf32_rna(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u))),
-      __uint_as_float(tf32_rna(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u))));
-}
-
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
-}
-
-// Loader pipeline over this CTA's tiles (blockIdx.x, + gridDim.x, ...):
-// issue(it, tile) starts the copies of local tile `it` (one cp.async group),
-// finish(it, tile) completes it once its group has landed; up to IA_AHEAD
-// later tiles stay in flight meanwhile (bounded by the stage count).
-#ifndef DLRM_IA_AHEAD
-#define DLRM_IA_AHEAD 3
-#endif
-constexpr int IA_AHEAD = DLRM_IA_AHEAD;
-
-// DLRM_IA_PROF builds (measurements only): clock64 time per role / phase of
-// the backward kernel, summed over CTAs, read with dlrm_ia_prof()
-#ifdef DLRM_IA_PROF
-__device__ unsigned long long g_ia_prof[32];
-#define IA_T0(n) const long long _t##n = clock64();
-#define IA_T1(n, k) prof[k] += (unsigned long long)(clock64() - _t##n);
-#else
-#define IA_T0(n)
-#define IA_T1(n, k)
-#endif
-
-template <class Issue, class Finish>
-__device__ __forceinline__ void ia_pipeline(int64_t ntiles, int nst, Issue issue, Finish finish) {
-  const int ahead = nst - 1 < IA_AHEAD ? nst - 1 : IA_AHEAD;
-  int issued = 0;
-  int64_t next = blockIdx.x;
-  for (; issued < ahead && next < ntiles; ++issued, next += gridDim.x) issue(issued, next);
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    // groups still allowed in flight: the ones issued after tile `it`
-    const int pending = issued - it - 1;
-    if (pending >= 3) cp_async_wait<3>();
-    else if (pending >= 2) cp_async_wait<2>();
-    else if (pending == 1) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    finish(it, tile);
-    // the next tile's copies only now: its stage is the one the MMA of an
-    // earlier tile read, and waiting for that MMA before finishing this tile
-    // would serialise the loaders with the tensor core
-    if (next < ntiles) {
-      issue(issued++, next);
-      next += gridDim.x;
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -364,343 +299,369 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
 }
 
 // ---------------------------------------------------------------------------
-// backward
+// backward (transposed form)
 //
-// Per tile of S samples (R rows, Kp = R rounded up to 8, Kq = to 16):
-//   A (TMEM, K-major) = [M_hi | M_lo], M = blockdiag over the samples of the
-//     symmetric pair-gradient matrix G + G^T (zero diagonal), built by the
-//     loader warps from the tile's gout[b, d + p];
-//   B (smem, MN-major, SWIZZLE_128B_BASE32B: 32-wide column chunks of Kp
-//     rows x 128 B, 32-byte atom a of row k at (a ^ (k & 3))) = [Z | Z_lo];
-//   D = M_lo Z_hi + M_hi Z_lo (first: the small terms, against a small
-//     accumulator) + M_hi Z_hi, one TMEM chain of d columns;
-// then g_0 += gout[b, :d] and the bottom MLP's ReLU mask on feature 0.
-// TMEM: D buffers [0, d) / [d, 2d), A slots [A_hi | A_lo] from a_base.
-// Roles: warps 0-3 epilogue (TMEM -> gradient rows, straight from
-// registers), 4-7 loaders (TMA or cp.async, lo split, A build; TMEM lane
-// quarters), 8 MMA issuer.
-__device__ __forceinline__ uint32_t mn_off(int k, int n) {
-  // byte offset of element (k, n) inside the chunk set (without chunk stride)
-  return uint32_t(k * 128 + ((((n & 31) >> 3) ^ (k & 3)) << 5) + ((n & 7) << 2));
+// g_i = [i==0] gout[:, :d] + sum_k M_ik z_k with M = G + G^T (zero diagonal)
+// is computed per sample as D = Z^T M (D[n][i] = g_i[n]): the embedding dim n
+// is the MMA's M dimension (TMEM lanes), so
+//   A (TMEM) = Z^T split hi / lo: lane n, column k = feature k of the sample
+//     (nfq = nf rounded up to 16 columns each, zero past nf), written by the
+//     splitter warps from the landed Z tile (plain row-major rows of d floats);
+//   B (smem, K-major 128B swizzle) = [M_hi ; M_lo] (2 nfq rows x 128 B per
+//     sample; pad rows / columns and the diagonal stay zero), built by the
+//     builder warps straight from gout[b, d + p];
+//   D = [A_hi M_hi^T | A_hi M_lo^T + A_lo M_hi^T]: one N = 2 nfq MMA and one
+//     N = nfq MMA per k-step, hh chain and small terms in separate columns;
+// and the epilogue writes row i of sample b from lane n: every warp store is
+// 32 consecutive floats of one gradient row.  For d < 128 the 128 / d
+// samples of a lane group share A's columns at different lanes; each sample
+// has its own B and D (the other lanes of its D are not read).
+// Roles: warps 0-7 epilogue (TMEM lane quarter, half of the lane groups),
+// 8-11 splitters (lane quarters), 12-15 builders, 16 MMA issuer + TMEM
+// allocator, 17 TMA / cp.async loader.
+constexpr int JB_EW = 8, JB_SPL = 8, JB_BLD = 12, JB_MMA = 16, JB_LD = 17;
+constexpr int JB_THREADS = 32 * (JB_LD + 1);
+constexpr int JB_BT = 32 * (JB_MMA - JB_BLD);  // builder threads
+constexpr int JB_MAXV = 8;    // pair gradients per builder thread per tile
+constexpr int JB_G0 = 4;      // gout[b, :d] values per builder thread per tile
+
+// DLRM_IA_PROF builds (measurements only): clock64 cycles each role's
+// first thread spends in each barrier wait, and its total, summed over CTAs
+// (read with dlrm_ia_prof; scripts/ia_prof.py)
+#ifdef DLRM_IA_PROF
+__device__ unsigned long long g_ia_prof[24];
+#define IB_WAIT(bar, par, k)                                   \
+  do {                                                         \
+    const long long t0_ = clock64();                           \
+    mbar_wait(bar, par);                                       \
+    prof[k] += (unsigned long long)(clock64() - t0_);          \
+  } while (0)
+#define IB_PROF_BEGIN const long long pt0_ = clock64();
+#define IB_PROF_END(k)                                                          \
+  if (lane == 0 && (warp == JB_LD || warp == JB_SPL || warp == JB_BLD ||       \
+                    warp == JB_MMA || warp == 0)) {                             \
+    prof[k] += (unsigned long long)(clock64() - pt0_);                        \
+    for (int i_ = 0; i_ < 24; ++i_)                                             \
+      if (prof[i_]) atomicAdd(&g_ia_prof[i_], prof[i_]);                        \
+  }
+#else
+#define IB_WAIT(bar, par, k) mbar_wait(bar, par)
+#define IB_PROF_BEGIN
+#define IB_PROF_END(k)
+#endif
+
+struct IbGeom {
+  int nf, d, P;
+  int gg;          // samples per TMEM lane group (128 / d)
+  int S, groups;   // samples per tile, lane groups per tile
+  int nst;         // Z stages
+  uint32_t zbytes; // Z stage bytes
+  uint32_t bbytes; // B bytes per sample (2 nfq rows x 128 B)
+  uint32_t a_base; // TMEM column of the A slots (after the two D buffers)
+  uint32_t tmem_cols;
+  uint32_t idesc2, idesc1;  // N = 2 nfq / N = nfq
+  int tma;
+};
+
+// byte offset of element (row, k) of a K-major SWIZZLE_128B tile
+__device__ __forceinline__ uint32_t sw128_off(int row, int k) {
+  return uint32_t(row * 128 + ((((k >> 2) ^ (row & 7)) << 4) | ((k & 3) << 2)));
 }
 
-constexpr int IB_EW = 8;                  // epilogue warps 0-7 (2 per lane quarter)
-constexpr int IB_LW = 8;                  // loader warps 8-15 (2 per lane quarter)
-constexpr int IB_MMA = IB_EW + IB_LW;     // MMA warp
-constexpr int IB_THREADS = 32 * (IB_MMA + 1);
-constexpr int IB_ET = 32 * IB_EW, IB_LT = 32 * IB_LW;
-
-__global__ void __launch_bounds__(IB_THREADS, 1)
+template <int NFQ>
+__global__ void __launch_bounds__(JB_THREADS, 1)
 interact_tc_bwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs,
-                       GradFeatureSet gs, IaGeom g, int64_t batch,
+                       GradFeatureSet gs, IbGeom g, int64_t batch,
                        const float* __restrict__ gout, int64_t ld_gout, int mask_f0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint8_t* stages = smem;
-  // feature 0's extra terms of the tile's samples (gout[b, :d] and z0 for
-  // the mask), prefetched by the epilogue warps: [2 buffers][S][2d]
-  float* gz = reinterpret_cast<float*>(smem + size_t(g.nst) * g.stage_bytes);
-  // the tile's symmetric pair-gradient matrices [R][mp] and the pair table
-  const int mp = g.nf + 1;
-  float* Ms = gz + size_t(2) * g.S * 2 * g.d;
-  int* pairs = reinterpret_cast<int*>(Ms + size_t(g.R) * mp);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(pairs + g.P) + 7) & ~uintptr_t(7));
-  uint64_t* land = bars;        // [nst] TMA landed (tx count)
-  uint64_t* empty = bars + 4;   // [nst] MMA done with the stage
-  uint64_t* afull = bars + 8;   // [2] A slot + B_lo ready (4 loader warps)
-  uint64_t* aempty = bars + 10; // [2] A slot consumed
-  uint64_t* dfull = bars + 12;  // [2] D buffer ready
-  uint64_t* dempty = bars + 14; // [2] D buffer drained (4 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint8_t* bslots = smem + size_t(g.nst) * g.zbytes;  // [2][S][bbytes]
+  const uint32_t bslot_bytes = uint32_t(g.S) * g.bbytes;
+  // per pair-gradient slot e = s * P + p of a tile: .x its offset in the
+  // tile's gout rows, .y the byte offsets of M[i][j] | M[j][i] << 16 in the
+  // sample's B (hi rows; the lo rows are NFQ * 128 bytes further)
+  uint2* btab = reinterpret_cast<uint2*>(bslots + size_t(2) * bslot_bytes);
+  // feature 0's extra terms of a tile (gout[b, :d] from the builders, z0 for
+  // the mask from the splitters), 4 tiles deep: [4][S][d] each
+  float* g0buf = reinterpret_cast<float*>(btab + g.S * g.P);
+  float* z0buf = g0buf + 4 * g.S * g.d;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(z0buf + 4 * g.S * g.d);
+  uint64_t* zfull = bars;         // [nst] Z tile landed
+  uint64_t* zempty = bars + 4;    // [nst] splitters done with the Z tile
+  uint64_t* afull = bars + 8;     // [2] A slot written (4 splitter warps)
+  uint64_t* bfull = bars + 10;    // [2] B slot written (2 builder warps)
+  uint64_t* opempty = bars + 12;  // [2] MMAs done with the A / B slots
+  uint64_t* dfull = bars + 14;    // [2] D buffer ready
+  uint64_t* dempty = bars + 16;   // [2] D buffer drained (8 epilogue warps)
+  uint64_t* gzfull = bars + 18;   // [4] g0 / z0 of a tile staged
+  uint64_t* gzempty = bars + 22;  // [4] the epilogue is done with them
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nf = g.nf, d = g.d, S = g.S, P = g.P, Pp = g.Pp;
+  const int nf = g.nf, d = g.d, S = g.S, P = g.P;
   const int64_t ntiles = ceil_div(batch, S);
-  const uint32_t lbo = uint32_t(g.Kp) * 128;  // column-chunk stride
-  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+  const uint32_t dcols = uint32_t(S) * 2 * NFQ;          // one D buffer
+  const uint32_t acols = uint32_t(g.groups) * 2 * NFQ;   // one A slot
+
+  for (int e = threadIdx.x; e < S * P; e += blockDim.x) {
+    const int s = e / P, p = e - s * P;
     int pi, pj;
     ia_pair(p, nf, pi, pj);
-    pairs[p] = (pi << 16) | pj;
+    const uint32_t base = uint32_t(s) * g.bbytes;
+    btab[e] = make_uint2(uint32_t(s * ld_gout + d + p),
+                         (base + sw128_off(pi, pj)) | ((base + sw128_off(pj, pi)) << 16));
   }
-
+  // B slots: zero once (pad rows / columns and the diagonal are never written)
+  for (uint32_t e = threadIdx.x; e < 2 * bslot_bytes / 16; e += blockDim.x)
+    reinterpret_cast<float4*>(bslots)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+  fence_async_smem();
   if (threadIdx.x == 0) {
     for (int s = 0; s < g.nst; ++s) {
-      mbar_init(&land[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&zfull[s], g.tma ? 1 : 32);
+      mbar_init(&zempty[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&afull[b], IB_LW);
-      mbar_init(&aempty[b], 1);
+      mbar_init(&afull[b], 4);
+      mbar_init(&bfull[b], JB_BT / 32);
+      mbar_init(&opempty[b], 1);
       mbar_init(&dfull[b], 1);
-      mbar_init(&dempty[b], IB_EW);
+      mbar_init(&dempty[b], JB_EW);
+    }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&gzfull[b], 4 + JB_BT / 32);
+      mbar_init(&gzempty[b], JB_EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == IB_MMA) tmem_alloc_warp(tmem_slot, IA_TMEM_COLS);
+  if (warp == JB_MMA) tmem_alloc_warp(tmem_slot, g.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
+#ifdef DLRM_IA_PROF
+  unsigned long long prof[24] = {0};
+#endif
+  IB_PROF_BEGIN
 
-  if (warp >= IB_EW && warp < IB_MMA) {
-    // ---- loaders (lane quarter q, half lh of the A columns)
-    const int t = threadIdx.x - IB_ET, lw = warp - IB_EW, q = lw & 3, lh = lw >> 2;
-    const int nv = d / 4;
-    // pair gradients by 16-byte cp.async (the padded row holds Pp floats)
-    const bool g16 = (reinterpret_cast<uintptr_t>(gout) % 16) == 0 && ld_gout % 4 == 0 &&
-                     d % 4 == 0 && ld_gout >= d + Pp;
-    const int i = 32 * q + lane;  // this thread's row of A
-    const uint32_t lane_off = uint32_t(32 * q) << 16;
-    unsigned long long prof[8] = {0};
-    IA_T0(all)
-    auto issue = [&](int it, int64_t tile) {
+  if (warp == JB_LD) {
+    // ---- loader: the tile's S * nf feature rows, row-major, d floats each
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int st = it % g.nst;
-      IA_T0(e)
-      if (it >= g.nst) mbar_wait(&empty[st], ((it / g.nst) - 1) & 1);
-      IA_T1(e, 0)
-      IA_T0(w)
-      uint8_t* base = stages + size_t(st) * g.stage_bytes;
-      float* gp = reinterpret_cast<float*>(base + g.b_bytes);
+      if (it >= g.nst) IB_WAIT(&zempty[st], ((it / g.nst) - 1) & 1, 0);
+      uint8_t* zs = stages + size_t(st) * g.zbytes;
       const int64_t b0 = tile * S;
-      const int ns = int(batch - b0 < S ? batch - b0 : S);
-      const int rv = ns * nf;
       if (g.tma) {
-        // Kp consecutive rows of the [batch * nf, d] matrix, one 32-column
-        // box each: rows past the tile hold the next samples' (finite)
-        // features, which meet zero columns of A; past the batch: zeros
-        if (t == 0) {
-          mbar_expect_tx(&land[st], uint32_t((d / 32) * lbo));
-          for (int c = 0; c < d / 32; ++c)
-            tma_load_2d(base + size_t(c) * lbo, &tmZ, &land[st], 32 * c, int(b0 * nf));
+        if (lane == 0) {  // rows past the batch: zeros
+          mbar_expect_tx(&zfull[st], uint32_t(S * nf * d * 4));
+          tma_load_2d(zs, &tmZ, &zfull[st], 0, int(b0 * nf));
         }
       } else {
-        // a 16-byte piece per lane (zero past the valid rows: A is zero
-        // there, and 0 * garbage could be NaN)
-        for (int r = lw; r < g.Kp; r += IB_LW) {
-          const bool ok = r < rv;
-          const int sm = ok ? r / nf : 0, f = ok ? r - sm * nf : 0;
-          const float* src = fs.feat[f] + (b0 + sm) * fs.stride[f];
-          for (int p = lane; p < nv; p += 32) {
-            const int n = 4 * p;
-            cp_async16(base + size_t(n >> 5) * lbo + mn_off(r, n), ok ? src + n : fs.feat[0], ok);
-          }
+        const int ns = int(batch - b0 < S ? batch - b0 : S);
+        const int nv = d / 4;
+        for (int e = lane; e < ns * nf * nv; e += 32) {
+          const int r = e / nv, p = e - r * nv, sm = r / nf, f = r - sm * nf;
+          cp_async16(zs + (size_t(r) * d + 4 * p) * 4, fs.feat[f] + (b0 + sm) * fs.stride[f] + 4 * p,
+                     true);
         }
+        cp_async_commit();
+        cp_async_wait<0>();
+        mbar_arrive(&zfull[st]);
       }
-      // pair gradients of the tile's samples
-      if (g16) {
-        const int pq = Pp / 4;
-        for (int e = t; e < ns * pq; e += IB_LT) {
-          const int sm = e / pq, c = e - sm * pq;
-          cp_async16(gp + sm * Pp + 4 * c, gout + (b0 + sm) * ld_gout + d + 4 * c, true);
-        }
-      } else {
-        for (int sm = 0; sm < ns; ++sm)
-          for (int e = t; e < P; e += IB_LT) gp[sm * Pp + e] = __ldg(gout + (b0 + sm) * ld_gout + d + e);
-      }
-      cp_async_commit();
-      IA_T1(w, 1)
-    };
-    auto finish = [&](int it, int64_t tile) {
+    }
+  } else if (warp >= JB_SPL && warp < JB_SPL + 4) {
+    // ---- splitters: A lane L = (sample L / d of the group, dim L % d)
+    const int q = warp - JB_SPL, L = 32 * q + lane, sl = L / d, n = L - sl * d;
+    const uint32_t lane_off = uint32_t(32 * q) << 16;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int st = it % g.nst, ab = it & 1;
-      uint8_t* base = stages + size_t(st) * g.stage_bytes;
-      const float* gp = reinterpret_cast<const float*>(base + g.b_bytes);
       const int64_t b0 = tile * S;
       const int ns = int(batch - b0 < S ? batch - b0 : S);
-      IA_T0(l)
-      if (g.tma) mbar_wait(&land[st], (it / g.nst) & 1);
-      IA_T1(l, 2)
-      IA_T0(b)
-      named_bar(1, IB_LT);
-      IA_T1(b, 3)
-      IA_T0(o)
-      // lo columns [d, 2d)
-      for (int r = lw; r < g.Kp; r += IB_LW)
-        for (int p = lane; p < nv; p += 32) {
-          const int n = 4 * p, nl = d + n;
-          const float4 v = *reinterpret_cast<const float4*>(base + size_t(n >> 5) * lbo + mn_off(r, n));
-          *reinterpret_cast<float4*>(base + size_t(nl >> 5) * lbo + mn_off(r, nl)) = split_lo4(v);
-        }
-      fence_async_smem();
-      IA_T1(o, 4)
-      // the tile's symmetric M_s = G_s + G_s^T (zero diagonal) in smem,
-      // row pitch mp, so that A row i reads its nf values contiguously
-      for (int e = t; e < ns * nf; e += IB_LT) Ms[(e / nf) * nf * mp + (e % nf) * (mp + 1)] = 0.f;
-      for (int e = t; e < ns * P; e += IB_LT) {
-        const int sm = e / P, p = e - sm * P, pr = pairs[p], pi = pr >> 16, pj = pr & 0xffff;
-        const float v = gp[sm * Pp + p];
-        Ms[(sm * nf + pi) * mp + pj] = v;
-        Ms[(sm * nf + pj) * mp + pi] = v;
-      }
-      named_bar(1, IB_LT);
-      // A row i: M_s[fi][fk] over this sample's block, split hi / lo (this
-      // warp: the 16-column groups of parity lh)
-      IA_T0(a)
-      if (it >= 2) mbar_wait(&aempty[ab], ((it - 2) >> 1) & 1);
-      IA_T1(a, 5)
-      IA_T0(c)
+      IB_WAIT(&zfull[st], (it / g.nst) & 1, 1);
+      if (it >= 2) IB_WAIT(&opempty[ab], ((it - 2) >> 1) & 1, 2);
       tc_fence_after();
-      const bool valid = i < ns * nf;
-      const int blk = (i / nf) * nf;
-      const float* mrow = Ms + size_t(i) * mp;
-      const uint32_t slot = tmem + lane_off + g.a_base + uint32_t(2 * g.Kq * ab);
-      for (int c0 = 16 * lh; c0 < g.Kq; c0 += 32) {
-        uint32_t hi[16], lo[16];
+      const float* zs = reinterpret_cast<const float*>(stages + size_t(st) * g.zbytes);
+      const uint32_t slot = tmem + lane_off + g.a_base + uint32_t(ab) * acols;
+      if (it >= 4) IB_WAIT(&gzempty[it & 3], ((it - 4) >> 2) & 1, 9);
+      float* z0s = z0buf + (it & 3) * S * d;
+      for (int gi = 0; gi < g.groups && gi * g.gg < ns; ++gi) {
+        const int s = gi * g.gg + sl;
+        if (s >= ns) continue;  // warp-uniform (d >= 32)
+        const float* zr = zs + size_t(s) * nf * d + n;
+        if (mask_f0) z0s[s * d + n] = zr[0];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int fk = c0 + k - blk;
-          const float m = (valid && fk >= 0 && fk < nf) ? mrow[fk] : 0.f;
-          hi[k] = __float_as_uint(m) & 0xFFFFE000u;
-          lo[k] = tf32_rna(m - __uint_as_float(hi[k]));
+        for (int c0 = 0; c0 < NFQ; c0 += 16) {
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float x = c0 + k < nf ? zr[(c0 + k) * d] : 0.f;
+            hi[k] = __float_as_uint(x) & 0xFFFFE000u;
+            lo[k] = tf32_rna(x - __uint_as_float(hi[k]));
+          }
+          tmem_st16(slot + uint32_t(gi * 2 * NFQ + c0), hi);
+          tmem_st16(slot + uint32_t(gi * 2 * NFQ + NFQ + c0), lo);
         }
-        tmem_st16(slot + uint32_t(c0), hi);
-        tmem_st16(slot + uint32_t(g.Kq + c0), lo);
       }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[ab]);
-      IA_T1(c, 6)
+      if (lane == 0) {
+        mbar_arrive(&zempty[st]);
+        mbar_arrive(&afull[ab]);
+        mbar_arrive(&gzfull[it & 3]);
+      }
+    }
+  } else if (warp >= JB_BLD && warp < JB_MMA) {
+    // ---- builders: [M_hi ; M_lo] of each sample from its pair gradients;
+    // two register sets, so one tile's gradients load while the previous
+    // tile's are stored
+    const int t = threadIdx.x - 32 * JB_BLD;
+    float va[JB_MAXV + JB_G0], vb[JB_MAXV + JB_G0];
+    auto load = [&](int64_t tile, float* v) {
+      const int64_t b0 = tile * S;
+      const int ns = int(batch - b0 < S ? batch - b0 : S);
+      const float* src = gout + b0 * ld_gout;
+#pragma unroll
+      for (int k = 0; k < JB_MAXV; ++k) {
+        const int e = t + JB_BT * k;
+        v[k] = e < ns * P ? __ldg(src + btab[e].x) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < JB_G0; ++k) {  // gout[b, :d]
+        const int e = t + JB_BT * k, sm = e / d;
+        v[JB_MAXV + k] = e < ns * d ? __ldg(src + sm * ld_gout + (e - sm * d)) : 0.f;
+      }
     };
-    ia_pipeline(ntiles, g.nst, issue, finish);
-    IA_T1(all, 7)
-#ifdef DLRM_IA_PROF
-    if (threadIdx.x == IB_ET)
-      for (int k = 0; k < 8; ++k) atomicAdd(&g_ia_prof[k], prof[k]);
-#endif
-  } else if (warp == IB_MMA) {
+    auto store = [&](int it, int64_t tile, const float* v) {
+      const int ab = it & 1;
+      const int64_t b0 = tile * S;
+      const int nsp = int(batch - b0 < S ? batch - b0 : S) * P;
+      if (it >= 2) IB_WAIT(&opempty[ab], ((it - 2) >> 1) & 1, 3);
+      uint8_t* bs = bslots + size_t(ab) * bslot_bytes;
+#pragma unroll
+      for (int k = 0; k < JB_MAXV; ++k) {
+        const int e = t + JB_BT * k;
+        if (e < nsp) {
+          const uint32_t o = btab[e].y, o1 = o & 0xffffu, o2 = o >> 16;
+          const uint32_t h = __float_as_uint(v[k]) & 0xFFFFE000u;
+          const uint32_t l = tf32_rna(v[k] - __uint_as_float(h));
+          *reinterpret_cast<uint32_t*>(bs + o1) = h;
+          *reinterpret_cast<uint32_t*>(bs + o2) = h;
+          *reinterpret_cast<uint32_t*>(bs + o1 + NFQ * 128) = l;
+          *reinterpret_cast<uint32_t*>(bs + o2 + NFQ * 128) = l;
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bfull[ab]);
+      if (it >= 4) IB_WAIT(&gzempty[it & 3], ((it - 4) >> 2) & 1, 10);
+      float* g0s = g0buf + (it & 3) * S * d;
+#pragma unroll
+      for (int k = 0; k < JB_G0; ++k) {
+        const int e = t + JB_BT * k;
+        if (e < nsp / P * d) g0s[e] = v[JB_MAXV + k];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gzfull[it & 3]);
+    };
+    int it = 0;
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) load(tile, va);
+    while (tile < ntiles) {
+      if (tile + gridDim.x < ntiles) load(tile + gridDim.x, vb);
+      store(it++, tile, va);
+      tile += gridDim.x;
+      if (tile >= ntiles) break;
+      if (tile + gridDim.x < ntiles) load(tile + gridDim.x, va);
+      store(it++, tile, vb);
+      tile += gridDim.x;
+    }
+  } else if (warp == JB_MMA) {
     // ---- MMA issuer
     if (lane == 0) {
-      const int ksteps = g.Kp / 8;
-      unsigned long long prof[8] = {0};
-      IA_T0(all)
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it % g.nst, ab = it & 1;
-        IA_T0(a)
-        mbar_wait(&afull[ab], (it >> 1) & 1);
-        IA_T1(a, 0)
-        IA_T0(d)
-        if (it >= 2) mbar_wait(&dempty[ab], ((it - 2) >> 1) & 1);
-        IA_T1(d, 1)
+        const int ab = it & 1;
+        const int64_t b0 = tile * S;
+        const int ns = int(batch - b0 < S ? batch - b0 : S);
+        IB_WAIT(&afull[ab], (it >> 1) & 1, 4);
+        IB_WAIT(&bfull[ab], (it >> 1) & 1, 5);
+        if (it >= 2) IB_WAIT(&dempty[ab], ((it - 2) >> 1) & 1, 6);
         tc_fence_after();
-        const uint32_t base = smem_u32(stages + size_t(st) * g.stage_bytes);
-        const uint32_t a_hi = tmem + g.a_base + uint32_t(2 * g.Kq * ab), a_lo = a_hi + g.Kq;
-        const uint32_t dt = tmem + uint32_t(d * ab);
-        const uint32_t lo_off = uint32_t(d / 32) * lbo + uint32_t(d % 32 ? 64 : 0);
-        // the small terms first, into a fresh accumulator, then hi x hi
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const uint32_t kb = base + uint32_t(ks * 1024);
-          mma_tf32_ts(dt, a_lo + uint32_t(8 * ks), smem_desc(kb, lbo, 512, 1), g.idesc,
-                      ks > 0 ? 1u : 0u);
-          mma_tf32_ts(dt, a_hi + uint32_t(8 * ks), smem_desc(kb + lo_off, lbo, 512, 1), g.idesc,
-                      1u);
+        const uint32_t bbase = smem_u32(bslots + size_t(ab) * bslot_bytes);
+        for (int s = 0; s < ns; ++s) {
+          const uint32_t a_hi = tmem + g.a_base + uint32_t(ab) * acols + uint32_t(s / g.gg) * 2 * NFQ;
+          const uint32_t dt = tmem + uint32_t(ab) * dcols + uint32_t(s) * 2 * NFQ;
+          const uint32_t bb = bbase + uint32_t(s) * g.bbytes;
+#pragma unroll
+          for (int ks = 0; ks < NFQ / 8; ++ks) {
+            const uint64_t bd = smem_desc(bb + uint32_t(32 * ks), 16, 1024, 2);
+            mma_tf32_ts(dt, a_hi + uint32_t(8 * ks), bd, g.idesc2, ks > 0 ? 1u : 0u);
+            mma_tf32_ts(dt + NFQ, a_hi + NFQ + uint32_t(8 * ks), bd, g.idesc1, 1u);
+          }
         }
-        for (int ks = 0; ks < ksteps; ++ks)
-          mma_tf32_ts(dt, a_hi + uint32_t(8 * ks),
-                      smem_desc(base + uint32_t(ks * 1024), lbo, 512, 1), g.idesc, 1u);
-        mma_commit(&empty[st]);
-        mma_commit(&aempty[ab]);
+        mma_commit(&opempty[ab]);
         mma_commit(&dfull[ab]);
       }
-      IA_T1(all, 7)
-#ifdef DLRM_IA_PROF
-      for (int k = 0; k < 8; ++k) atomicAdd(&g_ia_prof[8 + k], prof[k]);
-#endif
     }
-  } else {
-    // ---- epilogue (TMEM lane quarter q, half h of the columns): row i of D
-    // is feature fi of sample s; written straight from registers
-    const int q = warp & 3, h = warp >> 2, i = 32 * q + lane;
-    const int ecols = d >= 32 ? d / 2 : d;
+  } else if (warp < JB_EW) {
+    // ---- epilogue: lane L of D = dim n of sample (group gi, L / d); this
+    // warp takes the groups gi = h, h + 2
+    const int q = warp & 3, h = warp >> 2, L = 32 * q + lane, sl = L / d, n = L - sl * d;
     const uint32_t lane_off = uint32_t(32 * q) << 16;
-    const int sm = i / nf, fi = i - sm * nf;
-    const int nv = d / 4;
-    unsigned long long prof[8] = {0};
-    IA_T0(all)
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it & 1;
       const int64_t b0 = tile * S;
       const int ns = int(batch - b0 < S ? batch - b0 : S);
-      const bool valid = i < ns * nf;
-      IA_T0(p)
-      const int64_t b = b0 + (valid ? sm : 0);
-      float* dst = gs.feat[valid ? fi : 0] + b * gs.stride[valid ? fi : 0];
-      // gout[b, :d] / z0 of the tile's samples: the loads are in flight while
-      // the MMAs run, then land in this tile's buffer
-      float* gzb = gz + size_t(ab) * S * 2 * d;
-      float4 pre[2];
-      int npre = 0;
-      for (int e = threadIdx.x; e < ns * 2 * nv && npre < 2; e += IB_ET, ++npre) {
-        const int sm2 = e / (2 * nv), c = e - sm2 * 2 * nv;
-        pre[npre] = c < nv ? __ldg(reinterpret_cast<const float4*>(gout + (b0 + sm2) * ld_gout) + c)
-                           : __ldg(reinterpret_cast<const float4*>(fs.feat[0] + (b0 + sm2) *
-                                                                     fs.stride[0]) + (c - nv));
-      }
-      IA_T1(p, 0)
-      IA_T0(f)
-      mbar_wait(&dfull[ab], (it >> 1) & 1);
-      IA_T1(f, 1)
-      IA_T0(g)
-      npre = 0;
-      for (int e = threadIdx.x; e < ns * 2 * nv && npre < 2; e += IB_ET, ++npre)
-        reinterpret_cast<float4*>(gzb)[e] = pre[npre];
-      for (int e = threadIdx.x + 2 * IB_ET; e < ns * 2 * nv; e += IB_ET) {
-        const int sm2 = e / (2 * nv), c = e - sm2 * 2 * nv;
-        reinterpret_cast<float4*>(gzb)[e] =
-            c < nv ? __ldg(reinterpret_cast<const float4*>(gout + (b0 + sm2) * ld_gout) + c)
-                   : __ldg(reinterpret_cast<const float4*>(fs.feat[0] + (b0 + sm2) * fs.stride[0]) +
-                           (c - nv));
-      }
-      named_bar(2, IB_ET);
-      IA_T1(g, 2)
-      IA_T0(m)
-      const float* g0 = gzb + size_t(valid ? sm : 0) * 2 * d;
-      const float* z0 = g0 + d;
+      IB_WAIT(&dfull[ab], (it >> 1) & 1, 7);
+      IB_WAIT(&gzfull[it & 3], (it >> 2) & 1, 11);
+      const float* g0s = g0buf + (it & 3) * S * d;
+      const float* z0s = z0buf + (it & 3) * S * d;
       tc_fence_after();
-      if (32 * q < ns * nf) {
-        for (int c0 = h * ecols; c0 < (h + 1) * ecols && c0 < d; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16_issue(tmem + lane_off + uint32_t(d * ab + c0), v);
-          tmem_wait_ld();
-          if (valid) {
 #pragma unroll
-            for (int k = 0; k < 16; k += 4) {
-              float4 o = make_float4(__uint_as_float(v[k]), __uint_as_float(v[k + 1]),
-                                     __uint_as_float(v[k + 2]), __uint_as_float(v[k + 3]));
-              if (fi == 0) {
-                const float4 a = *reinterpret_cast<const float4*>(g0 + c0 + k);
-                o.x = a.x + o.x; o.y = a.y + o.y; o.z = a.z + o.z; o.w = a.w + o.w;
-                if (mask_f0) {
-                  const float4 zz = *reinterpret_cast<const float4*>(z0 + c0 + k);
-                  o.x *= zz.x > 0.f ? 1.f : 0.f; o.y *= zz.y > 0.f ? 1.f : 0.f;
-                  o.z *= zz.z > 0.f ? 1.f : 0.f; o.w *= zz.w > 0.f ? 1.f : 0.f;
-                }
-              }
-              *reinterpret_cast<float4*>(dst + c0 + k) = o;
+      for (int u = 0; u < 2; ++u) {
+        const int s = (h + 2 * u) * g.gg + sl;
+        if (h + 2 * u >= g.groups || s >= ns) continue;  // warp-uniform
+        const uint32_t dt = tmem + lane_off + uint32_t(ab) * dcols + uint32_t(s) * 2 * NFQ;
+        uint32_t hh[NFQ], sm[NFQ];
+#pragma unroll
+        for (int c0 = 0; c0 < NFQ; c0 += 16) {
+          tmem_ld16_issue(dt + uint32_t(c0), hh + c0);
+          tmem_ld16_issue(dt + uint32_t(NFQ + c0), sm + c0);
+        }
+        tmem_wait_ld();
+        const int64_t b = b0 + s;
+#pragma unroll
+        for (int f = 0; f < NFQ; ++f) {
+          if (f < nf) {
+            float v = __uint_as_float(hh[f]) + __uint_as_float(sm[f]);
+            if (f == 0) {
+              v = g0s[s * d + n] + v;
+              if (mask_f0) v *= z0s[s * d + n] > 0.f ? 1.f : 0.f;
             }
+            gs.feat[f][b * gs.stride[f] + n] = v;
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&dempty[ab]);
-      IA_T1(m, 3)
+      if (lane == 0) {
+        mbar_arrive(&dempty[ab]);
+        mbar_arrive(&gzempty[it & 3]);
+      }
     }
-    IA_T1(all, 7)
-#ifdef DLRM_IA_PROF
-    if (threadIdx.x == 0)
-      for (int k = 0; k < 8; ++k) atomicAdd(&g_ia_prof[16 + k], prof[k]);
-#endif
   }
+  IB_PROF_END(16 + (warp == JB_LD ? 0 : warp == JB_SPL ? 1 : warp == JB_BLD ? 2 : warp == JB_MMA ? 3 : 4))
   tc_fence_before();
   __syncthreads();
-  if (warp == IB_MMA) {
+  if (warp == JB_MMA) {
     tc_fence_after();
-    tmem_dealloc_warp(tmem, IA_TMEM_COLS);
+    tmem_dealloc_warp(tmem, g.tmem_cols);
   }
 }
 
@@ -728,27 +689,32 @@ bool fwd_geom(int nf, int d, IaGeom* g) {
   return true;
 }
 
-bool bwd_geom(int nf, int d, IaGeom* g) {
-  // the lo half of B starts at column d: a whole 32-column chunk, or (d = 16)
-  // the upper half of chunk 0, so one descriptor addresses it
-  if (nf < 2 || nf > 64 || d < 16 || d > 128 || (d % 32 && d != 16)) return false;
+bool bwd_geom(int nf, int d, IbGeom* g) {
+  // lanes = the embedding dim: d in {32, 64, 128}; nf <= 32 (one K block)
+  if (nf < 2 || nf > 32 || d < 32 || d > 128 || 128 % d) return false;
   const int P = nf * (nf - 1) / 2;
-  const uint32_t a_base = ceil_to(uint32_t(2 * d), 32);  // after the two D buffers
-  for (int S = 128 / nf; S >= 1; --S) {
-    const int R = S * nf, Kq = int(ceil_to(R, 16)), Kp = int(ceil_to(R, 8));
-    if (a_base + 4u * Kq > IA_TMEM_COLS) continue;
-    const uint32_t nchunk = (2 * d + 31) / 32;
-    const uint32_t b_bytes = nchunk * Kp * 128;
-    const int Pp = int(ceil_to(P, 4));
-    const uint32_t stage = ceil_to(b_bytes + uint32_t(S) * Pp * 4, 1024);
-    int nst = int((IA_SMEM_MAX - 1024 - 256 - size_t(16) * S * d - size_t(R) * (nf + 1) * 4 -
-                   size_t(P) * 4) / stage);
+  const int nfq = nf <= 16 ? 16 : 32, gg = 128 / d;
+  for (int S = 8; S >= 1; --S) {
+    const int groups = (S + gg - 1) / gg;
+    const uint32_t cols = uint32_t(2 * S * 2 * nfq + 2 * groups * 2 * nfq);
+    if (groups > 4 || cols > IA_TMEM_COLS || S * P > JB_BT * JB_MAXV || S * d > JB_BT * JB_G0 ||
+        S * 2 * nfq * 128 > 65536)
+      continue;
+    const uint32_t zbytes = ceil_to(uint32_t(S * nf * d * 4), 1024);
+    const uint32_t bbytes = uint32_t(2 * nfq * 128);
+    const size_t fixed = 1024 + size_t(2) * S * bbytes + size_t(S) * P * 8 + size_t(32) * S * d +
+                         32 * 8;
+    int nst = int((IA_SMEM_MAX - fixed) / zbytes);
     if (nst > 4) nst = 4;
     if (nst < 2) continue;
-    *g = IaGeom{};
-    g->nf = nf; g->d = d; g->S = S; g->R = R; g->P = P; g->Pp = Pp; g->Kq = Kq; g->Kp = Kp;
-    g->nst = nst; g->stage_bytes = stage; g->b_bytes = b_bytes; g->a_base = a_base;
-    g->idesc = instr_desc(d, false, true);
+    uint32_t tc = 32;
+    while (tc < cols) tc *= 2;
+    *g = IbGeom{};
+    g->nf = nf; g->d = d; g->P = P; g->gg = gg; g->S = S; g->groups = groups; g->nst = nst;
+    g->zbytes = zbytes; g->bbytes = bbytes; g->a_base = uint32_t(2 * S * 2 * nfq);
+    g->tmem_cols = tc;
+    g->idesc2 = instr_desc(2 * nfq, false, false);
+    g->idesc1 = instr_desc(nfq, false, false);
     return true;
   }
   return false;
@@ -758,9 +724,9 @@ size_t fwd_smem(const IaGeom& g) {
   return 1024 + size_t(g.nst) * g.stage_bytes + size_t(2) * g.R * g.nf * 4 + size_t(g.P) * 4 +
          8 + 24 * 8;
 }
-size_t bwd_smem(const IaGeom& g) {
-  return 1024 + size_t(g.nst) * g.stage_bytes + size_t(2) * g.S * 2 * g.d * 4 +
-         size_t(g.R) * (g.nf + 1) * 4 + size_t(g.P) * 4 + 8 + 24 * 8;
+size_t bwd_smem(const IbGeom& g) {
+  return 1024 + size_t(g.nst) * g.zbytes + size_t(2) * g.S * g.bbytes + size_t(g.S) * g.P * 8 +
+         size_t(32) * g.S * g.d + 32 * 8;
 }
 
 // features f at feat[0] + f*d with row stride nf*d (the training engine's
@@ -812,35 +778,34 @@ int interact_tc_fwd(const FeatureSet& fs, int nf, int64_t dim, int64_t batch, fl
 
 bool interact_tc_bwd_ok(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
                         const float* gout, int64_t ld_gout) {
-  IaGeom g;
+  IbGeom g;
   if (!tc_ia_enabled() || !bwd_geom(nf, int(dim), &g)) return false;
   if (reinterpret_cast<uintptr_t>(gout) % 16 || ld_gout % 4) return false;
   for (int f = 0; f < nf; ++f)
-    if (reinterpret_cast<uintptr_t>(fs.feat[f]) % 16 || fs.stride[f] % 4 ||
-        reinterpret_cast<uintptr_t>(gs.feat[f]) % 16 || gs.stride[f] % 4)
-      return false;
+    if (reinterpret_cast<uintptr_t>(fs.feat[f]) % 16 || fs.stride[f] % 4) return false;
+  (void)gs;  // gradient rows are written with 4-byte stores
   return true;
 }
 
 int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
                     int64_t batch, const float* gout, int64_t ld_gout, int mask_f0,
                     cudaStream_t s) {
-  IaGeom g;
+  IbGeom g;
   DLRM_REQUIRE(bwd_geom(nf, int(dim), &g), "interaction shape not supported by tcgen05 path");
   const size_t smem = bwd_smem(g);
-  static bool configured = false;
-  if (!configured) {
-    DLRM_CUDA(cudaFuncSetAttribute(interact_tc_bwd_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(IA_SMEM_MAX + 4096)));
-    configured = true;
+  auto k = nf <= 16 ? interact_tc_bwd_kernel<16> : interact_tc_bwd_kernel<32>;
+  static bool configured[2] = {false, false};
+  if (!configured[nf > 16]) {
+    DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(IA_SMEM_MAX + 4096)));
+    configured[nf > 16] = true;
   }
   CUtensorMap tm{};
   g.tma = uniform_rows(fs, nf, dim) &&
-          tma_encode_2d(&tm, fs.feat[0], dim, batch * nf, dim, 32, g.Kp, 2);
+          tma_encode_2d(&tm, fs.feat[0], dim, batch * nf, dim, int(dim), g.S * nf, 0);
   const int64_t ntiles = ceil_div(batch, g.S);
   const unsigned grid = unsigned(ntiles < kNumSMs ? ntiles : kNumSMs);
-  launch(interact_tc_bwd_kernel, grid, IB_THREADS, smem, s, tm, fs, gs, g, batch, gout, ld_gout,
-         mask_f0);
+  launch(k, grid, JB_THREADS, smem, s, tm, fs, gs, g, batch, gout, ld_gout, mask_f0);
   return check_launch("interact_tc_bwd_kernel");
 }
 
@@ -848,8 +813,8 @@ int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int6
 
 #ifdef DLRM_IA_PROF
 extern "C" int dlrm_ia_prof(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, dlrm::g_ia_prof, sizeof(unsigned long long) * 32);
-  static const unsigned long long zero[32] = {0};
+  cudaMemcpyFromSymbol(out, dlrm::g_ia_prof, sizeof(unsigned long long) * 24);
+  static const unsigned long long zero[24] = {0};
   cudaMemcpyToSymbol(dlrm::g_ia_prof, zero, sizeof(zero));
   return 0;
 }

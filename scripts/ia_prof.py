@@ -1,6 +1,7 @@
-"""Per-role phase times of the tcgen05 interaction backward (DLRM_IA_PROF
-builds: python scripts/build_variant.py prof -DDLRM_IA_PROF), in % of the
-role's kernel time, summed over CTAs."""
+"""Barrier-wait share per role of the tcgen05 interaction backward
+(DLRM_IA_PROF builds: python scripts/build_variant.py prof -DDLRM_IA_PROF;
+run with DLRM_B200_LIB=gpurun_var/prof/libdlrmb200.so): cycles each role's
+first thread spent in each wait, in % of that role's kernel time."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,7 +18,7 @@ fp = C.c_void_p(C.addressof(feats))
 gfeat = (C.c_void_p * nf)(*[gZ.data_ptr() + 4 * f * d for f in range(nf)])
 gstr = (C.c_int64 * nf)(*([nf * d] * nf))
 s = _lib.stream_handle()
-buf = (C.c_ulonglong * 32)()
+buf = (C.c_ulonglong * 24)()
 for rep in range(3):
     L.dlrm_ia_prof(buf)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -28,10 +29,12 @@ for rep in range(3):
     torch.cuda.synchronize()
 L.dlrm_ia_prof(buf)
 v = list(buf)
-print("kernel us", e0.elapsed_time(e1) * 1e3)
-names = {0: ["ld:empty", "ld:issue", "ld:land", "ld:bar", "ld:lo", "ld:aempty", "ld:Abuild"],
-         1: ["mma:afull", "mma:dempty"], 2: ["epi:prefetch", "epi:dfull", "epi:gzbar", "epi:tmem+st"]}
-for role, ns in names.items():
-    tot = v[8 * role + 7] or 1
-    for k, n in enumerate(ns):
-        print(f"{n:14s} {100.0 * v[8 * role + k] / tot:6.1f}%")
+print(f"nf={nf} d={d} B={B}: kernel {e0.elapsed_time(e1) * 1e3:.1f} us")
+roles = {"loader": (16, {0: "zempty"}), "splitter": (17, {1: "zfull", 2: "opempty", 9: "gzempty"}),
+         "builder": (18, {3: "opempty", 10: "gzempty"}),
+         "mma": (19, {4: "afull", 5: "bfull", 6: "dempty"}),
+         "epilogue": (20, {7: "dfull", 11: "gzfull"})}
+for role, (tot, waits) in roles.items():
+    t = v[tot] or 1
+    ws = ", ".join(f"{n} {100.0 * v[k] / t:5.1f}%" for k, n in waits.items())
+    print(f"  {role:9s} waits: {ws}   busy {100.0 - 100.0 * sum(v[k] for k in waits) / t:5.1f}%")

@@ -4,7 +4,7 @@ oracle (ref model.py:218-268) and the SIMT kernels.
 Tolerance (stated): normwise |got - ref|_max / |ref|_max <= 2e-6 for the
 pair dots and the feature gradients — 3xTF32 with the lo operands rounded to
 nearest TF32 (error ~2^-21 per product) and one TMEM accumulation chain of
-d/8 (forward) or R/8 (backward) steps.  Layout (which column holds which
+d/8 (forward) or nf/8 (backward, hh chain and small terms apart) steps.  Layout (which column holds which
 pair, z0 copy, zero padding) is checked bit-exactly with integer-valued
 features, where every dot is exact in any order.
 """
@@ -58,8 +58,9 @@ def test_forward_matches_oracle_and_simt(nf, d, b, strided):
 
 
 @pytest.mark.parametrize("nf,d,b", SHAPES)
-def test_backward_matches_oracle_and_simt(nf, d, b):
-    host, dev = feats_of(nf, d, b, nf * 7 + d * 3 + b, True)
+@pytest.mark.parametrize("strided", [False, True])
+def test_backward_matches_oracle_and_simt(nf, d, b, strided):
+    host, dev = feats_of(nf, d, b, nf * 7 + d * 3 + b, strided)
     P = nf * (nf - 1) // 2
     g = np.asarray(RngStream(b).normal(b, d + P), np.float32).astype(np.float64)
     gt = torch.tensor(g, dtype=torch.float32, device="cuda")
