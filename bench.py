@@ -414,6 +414,11 @@ def run_ours(args, c, rank, world, dist):
         ms = float(t.item())
     value = world * B * K / (ms / 1e3)
     eng.check_errors()
+    if args.quick:  # A/B experiments: the device-timed number only
+        if rank == 0:
+            print(json.dumps({"metric": "train samples/s", "value": value, "ms_per_step": ms / K,
+                              "config": {"workload": c["name"]}, "quick": True}), flush=True)
+        return
 
     # e2e: pinned host batch -> H2D on a copy stream into the input set the
     # previous step is NOT using, step graph on the compute stream, D2H of
@@ -748,6 +753,9 @@ def main():
                     help="table placement for N > 1: the reference's size-balanced plan or "
                          "the traffic-balanced one")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true",
+                    help="experiments: print only the device-timed step rate (no e2e, "
+                         "stage profile, rooflines or CPU baseline)")
     ap.add_argument("--cpu-batch", type=int, default=0,
                     help="batch of the CPU reference / baseline sample (0: the workload's)")
     args = ap.parse_args()

@@ -15,10 +15,12 @@
 // indices loaded coalesced by the sub-warp and broadcast with shuffles, 4 row
 // loads in flight per lane.
 #include <stdlib.h>
+#include <string.h>
 
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace dlrm {
 
@@ -1253,11 +1255,12 @@ struct WsLayout {
 WsLayout ws_layout(int64_t n, int64_t dim) {
   WsLayout L{};
   size_t sort_bytes = 0, scan_bytes = 0;
-  // keys_a/vals_a -> keys_b/vals_b (CUB keeps its ping-pong buffers in temp);
-  // sized for the widest key range
+  // keys_a/vals_a -> keys_b/vals_b (CUB, or radix.cu with DLRM_SORT=radix*,
+  // keeps its ping-pong buffers in temp); sized for the widest key range
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, int(n > 0 ? n : 1), 0, 32);
+  if (stable_sort_scratch(n) > sort_bytes) sort_bytes = stable_sort_scratch(n);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (uint32_t*)nullptr,
                                 (uint32_t*)nullptr, int(n > 0 ? n : 1));
   const size_t a = 256, e = align_up(size_t(n > 0 ? n : 1) * 4, a);
@@ -1320,6 +1323,12 @@ int sort_pairs(const TableSet& ts, int64_t nb, char* ws, const WsLayout& L, int6
       launch(emb_keys_kernel<1>, grid, 256, 0, s, ts, nb, n, bag_blocks, sentinel, ka, va, bag, by_bag_values(ts), err_pos, err_flag);
     if (int rc = check_launch("emb_keys_kernel")) return rc;
   }
+  // the hand-written radix sort (radix.cu) on request; the library onesweep
+  // sort measured faster inside the step (see radix.cu)
+  const char* alt = getenv("DLRM_SORT");
+  if (alt && strncmp(alt, "radix", 5) == 0)
+    return stable_sort_pairs(ka, va, kb, vb, n, end_bit, atoi(alt + 5) == 12 ? 12 : 8,
+                             ws + L.temp, s);
   size_t tb = L.temp_bytes;
   DLRM_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.temp, tb, ka, kb, va, vb, int(n), 0, end_bit, s));
   count_launch(end_bit / 8 + 2);

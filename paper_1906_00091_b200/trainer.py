@@ -215,6 +215,9 @@ class StepEngine:
         # weight-gradient stream; measured slower at c3 (0.431 vs 0.428 ms:
         # it delays the first weight gradient), so off by default
         self.head_split = os.environ.get("DLRM_HEAD_SPLIT", "0") == "1"
+        # measurement only (wrong results): leave stages out of the step to
+        # see how much of the step time each one holds (scripts/ablate.py)
+        self.ablate = set(filter(None, os.environ.get("DLRM_ABLATE", "").split(",")))
         self.fwd_stream = torch.cuda.Stream(device=dev)
         self.wg_stream = torch.cuda.Stream(device=dev)
 
@@ -350,12 +353,15 @@ class StepEngine:
         relu = _lib.ACT["relu"]
         ef = P(self.err_flag)
         call("dlrm_err_reset", P(self.err_pos), self.T, ef, s)
-        if self.prep_at == "start":
+        skip = self.ablate
+        if self.prep_at == "start" and "prep" not in skip:
             prep_done = fork_prepare()
         emb_side = self.emb_side and not profiling
         wg = fork(self.wg_stream) if self.wgrad_side and not profiling else None
 
         def emb_fwd(stream_handle):
+            if "lookup" in skip:
+                return
             call("dlrm_emb_fwd", P(self.W_all), d, self._descs_p, self.T, B,
                  P(self.Z), nf * d, P(self.err_pos), ef, stream_handle)
 
@@ -384,6 +390,8 @@ class StepEngine:
         a, lda = self.x, self.x.stride(0)
         for i in range(self.Lb):
             l = L[i]
+            if "bot" in skip:
+                break
             last = i == self.Lb - 1
             out, ldo = (self.Z, nf * d) if last else (self.bact[i], self.bact[i].stride(0))
             call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
@@ -401,13 +409,16 @@ class StepEngine:
             prep_done = fork_prepare()
         # interaction -> R
         mark("interaction_fwd")
-        call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
-             self.R.stride(0), self.R.shape[1], s)
+        if "ia_fwd" not in skip:
+            call("dlrm_interact_fwd", self._feats_p, nf, d, B, P(self.R),
+                 self.R.stride(0), self.R.shape[1], s)
         # top MLP (all but the N=1 head)
         mark("top_mlp_fwd")
         a, lda = self.R, self.R.stride(0)
         for i in range(self.Lt - 1):
             l = L[self.Lb + i]
+            if "top" in skip:
+                break
             out = self.tact[i]
             call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
                  P(out), out.stride(0), B, l.n_out, l.n_in, out.shape[1],
@@ -447,6 +458,8 @@ class StepEngine:
         mark("top_mlp_bwd")
         for i in range(self.Lt - 2, -1, -1):
             l = L[self.Lb + i]
+            if "top" in skip:
+                break
             gz = self.gtop[i]
             xin = self.R if i == 0 else self.tact[i - 1]
             dx = self.gR if i == 0 else self.gtop[i - 1]
@@ -458,15 +471,17 @@ class StepEngine:
                   None, 0, None, P(l.storage), l.ldw, P(l.bias), um, ef, ws, wsb)
         # interaction backward (bottom's last ReLU folded in for feature 0)
         mark("interaction_bwd")
-        call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
-             self.gR.stride(0), C.cast(self._gfeat, C.c_void_p),
-             C.cast(self._gstride, C.c_void_p), 1, s)
+        if "ia_bwd" not in skip:
+            call("dlrm_interact_bwd", self._feats_p, nf, d, B, P(self.gR),
+                 self.gR.stride(0), C.cast(self._gfeat, C.c_void_p),
+                 C.cast(self._gstride, C.c_void_p), 1, s)
         # The sparse backward apply needs only the feature gradients the
         # interaction backward just wrote: it runs on the side stream,
         # concurrently with the bottom MLP backward (the stage profile, which
         # times stages on one stream, keeps them in order).
         apply_done = None
-        if self.apply_side and prep_done is not None and profiling is False:
+        if (self.apply_side and prep_done is not None and profiling is False
+                and "apply" not in skip):
             ev = torch.cuda.Event()
             ev.record(main)
             self.side.wait_event(ev)
@@ -479,6 +494,8 @@ class StepEngine:
         mark("bottom_mlp_bwd")
         for i in range(self.Lb - 1, -1, -1):
             l = L[i]
+            if "bot" in skip:
+                break
             if i == self.Lb - 1:
                 gz, ldg = self.gZ, nf * d
             else:
@@ -507,6 +524,10 @@ class StepEngine:
             join(self.wg_stream)  # the next step reads the updated weights
         if apply_done is not None:
             main.wait_event(apply_done)  # join: the next step reads the tables
+            return
+        if "apply" in skip or "prep" in skip:
+            if prep_done is not None:  # "apply" alone keeps the prepare
+                main.wait_event(prep_done)
             return
         if prep_done is None:
             call("dlrm_emb_bwd_prepare", d, self._descs_p, self.T, B, self.total_rows,

@@ -234,3 +234,21 @@ def test_bwd_sgd_skips_update_on_error():
               _lib.ptr(torch.ones((B, d), device=dev)), d, 0.1, _lib.ptr(ef), 10,
               _lib.ptr(ws), wsb, s)
     assert torch.equal(W, before)
+
+
+@pytest.mark.parametrize("sort", ["radix8", "radix12"])
+@pytest.mark.parametrize("case", [(200000, 16, 2048, 60, "u"), (5000, 64, 300, 40, "u"),
+                                  (20000, 128, 256, 100, "z"), (3, 16, 4096, 1, "u")])
+def test_hand_written_radix_sort(sort, case, monkeypatch):
+    """The opt-in stable LSD radix sort (csrc/radix.cu, DLRM_SORT=radix8 /
+    radix12: 2-3 passes) gives the same bit-exact backward as the default;
+    200k rows = 18-bit keys (3 passes of 8 bits)."""
+    monkeypatch.setenv("DLRM_SORT", sort)
+    test_random_bags_bit_exact(*case)
+
+
+@pytest.mark.parametrize("sort", ["radix8", "radix12"])
+def test_hand_written_radix_sort_fused_step(sort, monkeypatch):
+    monkeypatch.setenv("DLRM_SORT", sort)
+    test_fused_multitable_fwd_and_bwd_sgd(64, "tiny", True)
+    test_fused_multitable_fwd_and_bwd_sgd(32, True, True)
