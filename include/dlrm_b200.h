@@ -303,9 +303,11 @@ int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* up
 
 /* ---- misc --------------------------------------------------------------- */
 
-/* Kernel selection (tests / A-B measurements): 0 = tcgen05 3xTF32 wherever
- * the shape and strides allow (default), 1 = SIMT fp32 only (MLP GEMMs and
- * the dot interaction). */
+/* Kernel selection (tests / A-B measurements): 0 = default (tcgen05 3xTF32
+ * GEMMs wherever the shape and strides allow; the dot interaction on the
+ * tensor cores where that is measured faster), 1 = SIMT fp32
+ * only (MLP GEMMs and the dot interaction), 2 = tensor cores wherever legal
+ * (the interaction at every size too). */
 int dlrm_gemm_mode(int32_t mode);
 
 /* ---- input pipeline: Criteo TSV ingestion (host code, multithreaded) ----

@@ -715,7 +715,8 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
 
 }  // namespace
 
-bool tc_enabled() { return g_tc_mode == 0; }
+bool tc_enabled() { return g_tc_mode != 1; }
+int tc_mode() { return g_tc_mode; }
 
 bool tma_encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t outer,
                    int64_t ld_elems, int box_inner, int box_outer, int swizzle) {

@@ -12,6 +12,8 @@ namespace dlrm {
 // false after dlrm_gemm_mode(1): every tensor-core kernel (GEMMs and the
 // interaction) is replaced by its SIMT fp32 counterpart (A/B tests)
 bool tc_enabled();
+// dlrm_gemm_mode: 0 default, 1 SIMT only, 2 tensor cores wherever legal
+int tc_mode();
 
 // 2D fp32 tensor map (row-major, ld_elems per row) for TMA loads of
 // box_inner x box_outer boxes; swizzle 0 none, 1 128B (K-major MMA tiles),

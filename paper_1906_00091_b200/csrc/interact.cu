@@ -18,12 +18,12 @@
 namespace dlrm {
 
 // tcgen05 path (interact_tc.cu): used whenever the shape / alignment allows
-bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t ld_out,
-                        const float* out);
+bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t batch,
+                        int64_t ld_out, const float* out);
 int interact_tc_fwd(const FeatureSet& fs, int nf, int64_t dim, int64_t batch, float* out,
                     int64_t ld_out, int64_t pad_to, cudaStream_t s);
 bool interact_tc_bwd_ok(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
-                        const float* gout, int64_t ld_gout);
+                        int64_t batch, const float* gout, int64_t ld_gout);
 int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
                     int64_t batch, const float* gout, int64_t ld_gout, int mask_f0,
                     cudaStream_t s);
@@ -308,7 +308,7 @@ extern "C" int dlrm_interact_fwd(const dlrm_features* feats, int32_t nf,
   bool v4;
   if (int rc = fill_features(fs, feats, nf, dim, &v4)) return rc;
   if (batch == 0) return 0;
-  if (interact_tc_fwd_ok(fs, nf, dim, ld_out, out))
+  if (interact_tc_fwd_ok(fs, nf, dim, batch, ld_out, out))
     return interact_tc_fwd(fs, nf, dim, batch, out, ld_out, pad_to, as_stream(stream));
   const int npairs = nf * (nf - 1) / 2;
   const size_t fixed = align_up(size_t(npairs) * 4, 16);
@@ -342,7 +342,7 @@ extern "C" int dlrm_interact_bwd(const dlrm_features* feats, int32_t nf,
   }
   v4 = v4 && reinterpret_cast<uintptr_t>(gout) % 16 == 0 && ld_gout % 4 == 0;
   if (batch == 0) return 0;
-  if (interact_tc_bwd_ok(fs, gs, nf, dim, gout, ld_gout))
+  if (interact_tc_bwd_ok(fs, gs, nf, dim, batch, gout, ld_gout))
     return interact_tc_bwd(fs, gs, nf, dim, batch, gout, ld_gout, relu_mask_f0,
                            as_stream(stream));
   const size_t extra = size_t(nf) * ((nf + 3) & ~3) * 4;

@@ -32,12 +32,12 @@
 
 namespace dlrm {
 
-bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t ld_out,
-                        const float* out);
+bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t batch,
+                        int64_t ld_out, const float* out);
 int interact_tc_fwd(const FeatureSet& fs, int nf, int64_t dim, int64_t batch, float* out,
                     int64_t ld_out, int64_t pad_to, cudaStream_t s);
 bool interact_tc_bwd_ok(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
-                        const float* gout, int64_t ld_gout);
+                        int64_t batch, const float* gout, int64_t ld_gout);
 int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
                     int64_t batch, const float* gout, int64_t ld_gout, int mask_f0,
                     cudaStream_t s);
@@ -45,7 +45,7 @@ int interact_tc_bwd(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int6
 namespace {
 using namespace tcu;
 
-constexpr int IA_EPI = 128;      // epilogue warps 0-3
+constexpr int IA_EPI = 128;      // forward epilogue warps 0-3
 constexpr uint32_t IA_TMEM_COLS = 512;
 constexpr size_t IA_SMEM_MAX = 220 * 1024;
 
@@ -71,9 +71,37 @@ __device__ __forceinline__ void ia_pair(int p, int nf, int& i, int& j) {
   j = row + 1 + (p - base);
 }
 
+__host__ __device__ constexpr uint32_t ceil_to32(int x) { return uint32_t((x + 31) & ~31); }
+
 __device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
+
+// DLRM_IA_PROF builds (measurements only): clock64 cycles each role's
+// first thread spends in each barrier wait, and its total, summed over CTAs
+// (read with dlrm_ia_prof; scripts/ia_prof.py)
+#ifdef DLRM_IA_PROF
+__device__ unsigned long long g_ia_prof[24];
+#define IB_WAIT(bar, par, k)                                   \
+  do {                                                         \
+    const long long t0_ = clock64();                           \
+    mbar_wait(bar, par);                                       \
+    prof[k] += (unsigned long long)(clock64() - t0_);          \
+  } while (0)
+#define IB_PROF_BEGIN const long long pt0_ = clock64();
+#define IB_PROF_END(cond, k)                                                    \
+  if (lane == 0 && (cond)) {                                                    \
+    prof[k] += (unsigned long long)(clock64() - pt0_);                        \
+    for (int i_ = 0; i_ < 24; ++i_)                                             \
+      if (prof[i_]) atomicAdd(&g_ia_prof[i_], prof[i_]);                        \
+  }
+#define IB_PROF_DECL unsigned long long prof[24] = {0};
+#else
+#define IB_WAIT(bar, par, k) mbar_wait(bar, par)
+#define IB_PROF_BEGIN
+#define IB_PROF_END(cond, k)
+#define IB_PROF_DECL
+#endif
 
 // ---------------------------------------------------------------------------
 // forward
@@ -325,31 +353,6 @@ constexpr int JB_BT = 32 * (JB_MMA - JB_BLD);  // builder threads
 constexpr int JB_MAXV = 8;    // pair gradients per builder thread per tile
 constexpr int JB_G0 = 4;      // gout[b, :d] values per builder thread per tile
 
-// DLRM_IA_PROF builds (measurements only): clock64 cycles each role's
-// first thread spends in each barrier wait, and its total, summed over CTAs
-// (read with dlrm_ia_prof; scripts/ia_prof.py)
-#ifdef DLRM_IA_PROF
-__device__ unsigned long long g_ia_prof[24];
-#define IB_WAIT(bar, par, k)                                   \
-  do {                                                         \
-    const long long t0_ = clock64();                           \
-    mbar_wait(bar, par);                                       \
-    prof[k] += (unsigned long long)(clock64() - t0_);          \
-  } while (0)
-#define IB_PROF_BEGIN const long long pt0_ = clock64();
-#define IB_PROF_END(k)                                                          \
-  if (lane == 0 && (warp == JB_LD || warp == JB_SPL || warp == JB_BLD ||       \
-                    warp == JB_MMA || warp == 0)) {                             \
-    prof[k] += (unsigned long long)(clock64() - pt0_);                        \
-    for (int i_ = 0; i_ < 24; ++i_)                                             \
-      if (prof[i_]) atomicAdd(&g_ia_prof[i_], prof[i_]);                        \
-  }
-#else
-#define IB_WAIT(bar, par, k) mbar_wait(bar, par)
-#define IB_PROF_BEGIN
-#define IB_PROF_END(k)
-#endif
-
 struct IbGeom {
   int nf, d, P;
   int gg;          // samples per TMEM lane group (128 / d)
@@ -441,9 +444,7 @@ interact_tc_bwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs,
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
-#ifdef DLRM_IA_PROF
-  unsigned long long prof[24] = {0};
-#endif
+  IB_PROF_DECL
   IB_PROF_BEGIN
 
   if (warp == JB_LD) {
@@ -656,7 +657,8 @@ interact_tc_bwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs,
       }
     }
   }
-  IB_PROF_END(16 + (warp == JB_LD ? 0 : warp == JB_SPL ? 1 : warp == JB_BLD ? 2 : warp == JB_MMA ? 3 : 4))
+  IB_PROF_END(warp == JB_LD || warp == JB_SPL || warp == JB_BLD || warp == JB_MMA || warp == 0,
+              16 + (warp == JB_LD ? 0 : warp == JB_SPL ? 1 : warp == JB_BLD ? 2 : warp == JB_MMA ? 3 : 4))
   tc_fence_before();
   __syncthreads();
   if (warp == JB_MMA) {
@@ -738,17 +740,27 @@ bool uniform_rows(const FeatureSet& fs, int nf, int64_t dim) {
   return true;
 }
 
-bool tc_ia_enabled() {
+// Default dispatch (scripts/ia_matrix.py, profiles/round2/ia_matrix.jsonl):
+// the SIMT kernels cost ~pairs x d FMAs per sample, the tensor-core ones
+// are bound by their per-tile data movement.  With many features (nf = 27,
+// d >= 64: Criteo-shaped) the tensor cores win at every batch (1.5-1.8x at
+// d = 128); with few (nf = 9, 36 pairs: the Big Basin shape) or narrow rows
+// (d = 32) the SIMT kernels are faster at every batch.  So: tensor cores
+// when nf (nf - 1) / 2 >= 100 and d >= 64; dlrm_gemm_mode(2) forces them,
+// DLRM_IA_SIMT (or mode 1) disables them.
+bool tc_ia_enabled(int nf, int64_t dim) {
   static const bool off = getenv("DLRM_IA_SIMT") != nullptr;
-  return !off && tc_enabled();
+  if (off || !tc_enabled()) return false;
+  return tc_mode() == 2 || (nf * (nf - 1) / 2 >= 100 && dim >= 64);
 }
 
 }  // namespace
 
-bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t ld_out,
-                        const float* out) {
+bool interact_tc_fwd_ok(const FeatureSet& fs, int nf, int64_t dim, int64_t batch,
+                        int64_t ld_out, const float* out) {
   IaGeom g;
-  if (!tc_ia_enabled() || !fwd_geom(nf, int(dim), &g)) return false;
+  (void)batch;
+  if (!tc_ia_enabled(nf, dim) || !fwd_geom(nf, int(dim), &g)) return false;
   if (reinterpret_cast<uintptr_t>(out) % 16 || ld_out % 4) return false;
   for (int f = 0; f < nf; ++f)
     if (reinterpret_cast<uintptr_t>(fs.feat[f]) % 16 || fs.stride[f] % 4) return false;
@@ -777,9 +789,10 @@ int interact_tc_fwd(const FeatureSet& fs, int nf, int64_t dim, int64_t batch, fl
 }
 
 bool interact_tc_bwd_ok(const FeatureSet& fs, const GradFeatureSet& gs, int nf, int64_t dim,
-                        const float* gout, int64_t ld_gout) {
+                        int64_t batch, const float* gout, int64_t ld_gout) {
   IbGeom g;
-  if (!tc_ia_enabled() || !bwd_geom(nf, int(dim), &g)) return false;
+  (void)batch;
+  if (!tc_ia_enabled(nf, dim) || !bwd_geom(nf, int(dim), &g)) return false;
   if (reinterpret_cast<uintptr_t>(gout) % 16 || ld_gout % 4) return false;
   for (int f = 0; f < nf; ++f)
     if (reinterpret_cast<uintptr_t>(fs.feat[f]) % 16 || fs.stride[f] % 4) return false;
