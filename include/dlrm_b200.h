@@ -309,6 +309,8 @@ int dlrm_update_dense(float* p, const float* g, int64_t n, const dlrm_update* up
  * only (MLP GEMMs and the dot interaction), 2 = tensor cores wherever legal
  * (the interaction at every size too). */
 int dlrm_gemm_mode(int32_t mode);
+/* the current kernel selection (dlrm_gemm_mode) */
+int dlrm_gemm_mode_get(void);
 
 /* ---- input pipeline: Criteo TSV ingestion (host code, multithreaded) ----
  * Replaces dlrmkit.datagen.parse_criteo / read_criteo (datagen.py:318-371)

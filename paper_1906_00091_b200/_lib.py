@@ -6,6 +6,7 @@ kernel is not a CUDA tensor, the call fails loudly.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 
@@ -95,7 +96,7 @@ _SIZE_FNS = {
 # every symbol include/dlrm_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = sorted(list(_SIGS) + list(_SIZE_FNS) + [
     "dlrm_launch_count", "dlrm_last_error", "dlrm_build_info", "dlrm_criteo_parse",
-    "dlrm_blake2b64", "dlrm_random_bags", "dlrm_pack_batch"])
+    "dlrm_blake2b64", "dlrm_random_bags", "dlrm_pack_batch", "dlrm_gemm_mode_get"])
 
 _lib = None
 
@@ -127,6 +128,7 @@ def lib():
         L.dlrm_pack_batch.argtypes = [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp,
                                       _vp, _vp, _vp, _vp, _i32]
         L.dlrm_pack_batch.restype = _i32
+        L.dlrm_gemm_mode_get.argtypes, L.dlrm_gemm_mode_get.restype = [], _i32
         L.dlrm_last_error.restype = C.c_char_p
         L.dlrm_build_info.restype = C.c_char_p
         _lib = L
@@ -135,6 +137,30 @@ def lib():
 
 class KernelError(RuntimeError):
     pass
+
+
+@contextlib.contextmanager
+def accurate_gemms(enable: bool):
+    """The enclosed launches and graph captures use the SIMT fp32 GEMMs and
+    interaction (``dlrm_gemm_mode(1)``) when ``enable`` and the caller left
+    the default mode; the caller's mode is restored.  Used by Adagrad steps:
+    Adagrad divides every gradient component by its own running magnitude,
+    so the error of tiny components — larger with 3xTF32's truncating
+    tensor-core accumulation than with fp32 FMA chains — reaches the weights
+    (DESIGN.md §2)."""
+    if not enable:
+        yield
+        return
+    L = lib()
+    prev = int(L.dlrm_gemm_mode_get())
+    if prev != 0:
+        yield
+        return
+    L.dlrm_gemm_mode(1)
+    try:
+        yield
+    finally:
+        L.dlrm_gemm_mode(prev)
 
 
 def call(name, *args):

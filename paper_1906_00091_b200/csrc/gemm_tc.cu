@@ -837,3 +837,5 @@ extern "C" int dlrm_gemm_mode(int32_t mode) {
   dlrm::g_tc_mode = mode;
   return 0;
 }
+
+extern "C" int dlrm_gemm_mode_get(void) { return dlrm::g_tc_mode; }

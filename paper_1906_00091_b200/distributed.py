@@ -280,6 +280,8 @@ class RankEngine:
         # update rule (SGD / Adagrad with same-layout accumulators)
         from .optim import update_rule
         self.optimizer = optimizer
+        # Adagrad: fp32 SIMT GEMMs (see _lib.accurate_gemms)
+        self.accurate = optimizer == "adagrad" and os.environ.get("DLRM_ADAGRAD_TC") != "1"
         if optimizer == "adagrad":
             self.params_acc = torch.zeros_like(self.params)
             self.W_acc = torch.zeros_like(self.W_own)
@@ -645,7 +647,7 @@ class HybridTrainer:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         try:
-            with _lib.capture_guard(), torch.cuda.graph(g):
+            with _lib.capture_guard(), torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self._issue()
         except Exception:
             self.graph = None
@@ -669,6 +671,10 @@ class HybridTrainer:
         return self.result()
 
     def _issue(self):
+        with _lib.accurate_gemms(self.engine.accurate):
+            self._issue_step()
+
+    def _issue_step(self):
         e, ex = self.engine, self.ex
         cur = torch.cuda.current_stream()
         comm, wg, side = self.comm_stream, self.wg_stream, self.side

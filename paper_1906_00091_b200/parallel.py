@@ -18,6 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _lib
 from .model import DlrmConfig, DlrmModel
 from .optim import Sgd
 from .pipeline import StagedDense
@@ -518,6 +519,11 @@ class ParallelTrainer:
                    default=0.0)
 
     def step(self, dense_x, batches, labels, timer=None) -> StepResult:
+        # Adagrad: fp32 SIMT GEMMs (see _lib.accurate_gemms)
+        with _lib.accurate_gemms(self.engines[0].accurate):
+            return self._step(dense_x, batches, labels, timer)
+
+    def _step(self, dense_x, batches, labels, timer=None) -> StepResult:
         plan = self.plan
         n_total = int(dense_x.shape[0])
         if n_total != plan.batch_size:

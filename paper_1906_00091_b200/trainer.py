@@ -189,6 +189,7 @@ class StepEngine:
         # Adagrad with accumulators laid out exactly like the parameters
         from .optim import update_rule
         self.optimizer, self.eps = optimizer, float(eps)
+        self.accurate = optimizer == "adagrad" and os.environ.get("DLRM_ADAGRAD_TC") != "1"
         if optimizer == "adagrad":
             self.params_acc = torch.zeros_like(self.params)
             self.W_acc = torch.zeros_like(self.W_all)
@@ -320,7 +321,13 @@ class StepEngine:
 
     def launch(self, stream=None, mark=None):
         """Issue the whole step on ``stream`` (default: current stream).
-        ``mark(stage)`` (profiling only) is called before each stage."""
+        ``mark(stage)`` (profiling only) is called before each stage.
+        Adagrad steps run the fp32 SIMT GEMMs (``_lib.accurate_gemms``;
+        ``DLRM_ADAGRAD_TC=1`` keeps the tensor cores)."""
+        with _lib.accurate_gemms(self.accurate):
+            return self._launch(stream, mark)
+
+    def _launch(self, stream=None, mark=None):
         profiling = mark is not None
         mark = mark or (lambda name: None)
         main = stream if stream is not None else torch.cuda.current_stream()
@@ -575,7 +582,7 @@ class StepEngine:
             g = torch.cuda.CUDAGraph()
             try:
                 mark = make_mark(evs, True)
-                with _lib.capture_guard(), torch.cuda.graph(g):
+                with _lib.capture_guard(), torch.cuda.graph(g, capture_error_mode="thread_local"):
                     self.launch(mark=mark)
                     mark("end")
                 entry = (g, evs)
@@ -606,7 +613,7 @@ class StepEngine:
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n0 = _lib.launch_count()
-        with _lib.capture_guard(), torch.cuda.graph(g):
+        with _lib.capture_guard(), torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.launch()
         self.launches_per_step = _lib.launch_count() - n0
         self.graph = g
@@ -634,7 +641,7 @@ class StepEngine:
         try:
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
-            with _lib.capture_guard(), torch.cuda.graph(graph):
+            with _lib.capture_guard(), torch.cuda.graph(graph, capture_error_mode="thread_local"):
                 self.launch(mark=mark)
                 mark("end")
         except Exception:
@@ -743,7 +750,7 @@ class StepEngine:
         if self._eval_runs >= 1:
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with _lib.capture_guard(), torch.cuda.graph(g):
+            with _lib.capture_guard(), torch.cuda.graph(g, capture_error_mode="thread_local"):
                 self.launch_eval()
             self.eval_graphs[self._set] = g
             g.replay()
