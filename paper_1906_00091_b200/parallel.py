@@ -355,12 +355,15 @@ def _bind_optimizer(eng, optimizer, model):
 
 
 def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
-               timer=None, use_graph: bool = True) -> StepResult:
+               timer=None, use_graph: bool = True, sync: bool = True) -> StepResult:
     """One forward/backward/SGD step over a mini-batch on the current GPU.
 
     Same contract as the reference: updates ``model`` in place and returns
     (loss, accuracy, probs); an out-of-range index raises LookupIndexError
-    and leaves every parameter untouched."""
+    and leaves every parameter untouched.  ``sync=False`` returns as soon as
+    the step is issued: the result's loss / accuracy (and a LookupIndexError
+    of this step) materialise when first read, so the host can stage the
+    next step while this one runs (``trainer.PendingStepResult``)."""
     if getattr(optimizer, "name", None) not in ("sgd", "adagrad"):
         raise ValueError(f"unsupported optimizer {optimizer!r}")
     cfg = model.config
@@ -402,7 +405,7 @@ def train_step(model: DlrmModel, dense_x, batches, labels, optimizer,
     else:
         eng.run()
         eng.eager_runs += 1
-    return eng.result()
+    return eng.result() if sync else eng.result_async()
 
 
 class _EngineSpec:

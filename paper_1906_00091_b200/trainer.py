@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 import torch
@@ -68,6 +69,32 @@ class StepResult:
 
     def __repr__(self):
         return f"StepResult(loss={self.loss:.6f}, accuracy={self.accuracy:.4f})"
+
+
+class PendingStepResult(StepResult):
+    """The StepResult of a step issued with ``sync=False``: ``loss`` and
+    ``accuracy`` are copied back asynchronously into a pinned ring slot and
+    materialise on first access (which waits for that step only); a bad
+    index raises LookupIndexError then, with the payload of THAT step.  Steps
+    issued after it are not rolled back (each skipped only its own updates
+    if its own batch was bad)."""
+
+    def __init__(self, engine: "StepEngine", slot: int, event, probs: torch.Tensor):
+        self._eng, self._slot, self._event, self.probs = engine, slot, event, probs
+        self._vals = None
+
+    def _materialise(self):
+        if self._vals is None:
+            self._vals = self._eng._settle(self)
+        return self._vals
+
+    @property
+    def loss(self) -> float:
+        return self._materialise()[0]
+
+    @property
+    def accuracy(self) -> float:
+        return self._materialise()[1]
 
 
 class StepEngine:
@@ -787,6 +814,55 @@ class StepEngine:
                     tab = self.model.tables[t]
                     raise LookupIndexError(tab.table_id, int(pos[t]), int(val[t]),
                                            tab.num_rows)
+
+    RING = 8  # pinned result slots of sync=False steps
+
+    def result_async(self) -> "PendingStepResult":
+        """The last step's result without a host synchronisation: loss /
+        correct sums, the error flag and the error payload are copied into a
+        pinned ring slot on the compute stream (PendingStepResult)."""
+        T = self.T
+        if getattr(self, "_ring", None) is None:
+            # per slot: [loss, correct, flag(int32), pad | err_pos[T] | err_val[T]]
+            self._ring = [torch.zeros(4 + 4 * T, dtype=torch.float32).pin_memory()
+                          for _ in range(self.RING)]
+            self._ring_owner = [None] * self.RING
+            self._ring_next = 0
+        k = self._ring_next
+        self._ring_next = (k + 1) % self.RING
+        old = self._ring_owner[k]
+        if old is not None:
+            old = old()
+            if old is not None:  # an unread result still owns the slot
+                old._materialise()
+        h = self._ring[k]
+        s = torch.cuda.current_stream()
+        h[2:3].view(torch.int32).copy_(self.err_flag, non_blocking=True)
+        h[0:2].copy_(self.stats, non_blocking=True)
+        h[4:4 + 2 * T].view(torch.int64).copy_(self.err_pos, non_blocking=True)
+        h[4 + 2 * T:4 + 4 * T].view(torch.int64).copy_(self.err_val, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        res = PendingStepResult(self, k, ev, self.prob.clone())
+        self._ring_owner[k] = weakref.ref(res)
+        return res
+
+    def _settle(self, res: "PendingStepResult"):
+        res._event.synchronize()
+        h, T = self._ring[res._slot], self.T
+        if self._ring_owner[res._slot] is not None and self._ring_owner[res._slot]() is res:
+            self._ring_owner[res._slot] = None
+        vals = (float(h[0]) / self.B, float(h[1]) / self.B)
+        if int(h[2:3].view(torch.int32)[0]):
+            res._vals = vals
+            pos = h[4:4 + 2 * T].view(torch.int64).numpy()
+            val = h[4 + 2 * T:4 + 4 * T].view(torch.int64).numpy()
+            for t in range(T):
+                if pos[t] != INT64_MAX:
+                    tab = self.model.tables[t]
+                    raise LookupIndexError(tab.table_id, int(pos[t]), int(val[t]),
+                                           tab.num_rows)
+        return vals
 
     def result(self) -> StepResult:
         """StepResult of the last step: the error flag and the loss / correct

@@ -1,9 +1,9 @@
-"""Summarise `ncu --set full` reports (scripts/round_ncu.sh) as the markdown
-table in profiles/<round>/ncu_full_c3.md and the per-kernel DRAM traffic JSON
-bench.py reads (profiles/ncu_traffic_c3.json).
+"""Summarise `ncu --set full` reports (scripts/round2_ncu.sh) as a markdown
+table for profiles/<round>/ and the per-kernel DRAM traffic JSON bench.py
+reads for the `roofline.traffic` field (profiles/ncu_traffic_<config>.json).
 
-    python scripts/ncu_summary.py gpurun_out/r1n4 profiles/round1/ncu_full_c3.md \
-        profiles/ncu_traffic_c3.json
+    python scripts/ncu_summary.py c3 profiles/round2/ncu_full_c3.md \
+        profiles/ncu_traffic_c3.json gpurun_out/r2n/c3_fold.ncu-rep ...
 """
 import csv, io, json, re, subprocess, sys
 
@@ -38,16 +38,18 @@ def short(name):
 
 
 def main():
-    src, md, js = sys.argv[1], sys.argv[2], sys.argv[3]
-    lines = ["# ncu --set full --clock-control none, c3 training step (scripts/round_ncu.sh)", "",
-             "Captured from `python scripts/profile_step.py --config c3 --steps 2` (eager step, "
-             f"second step's launches); raw reports in {src} (not committed); table by "
-             "`scripts/ncu_summary.py`.", "",
+    cfg, md, js, reps = sys.argv[1], sys.argv[2], sys.argv[3], sys.argv[4:]
+    lines = [f"# ncu --set full --clock-control none, {cfg} training step (scripts/round2_ncu.sh)",
+             "",
+             f"Captured from `python scripts/profile_step.py --config {cfg} --steps 2` (eager "
+             "step, second step's launches) after a clean plain run of the same command; "
+             "table by `scripts/ncu_summary.py`.  Cold-cache, serialised: compare shares and "
+             "traffic, not absolute step time.", "",
              "kernel | time us | DRAM read+write MB | " + " | ".join(c for c, _ in COLS[1:]) +
              " | grid x block", "---|" * (len(COLS) + 2) + "---"]
-    traffic, gemm = {}, []
-    for rep in ("full_fold", "full_fwd", "full_gemm"):
-        for r in rows_of(f"{src}/{rep}.ncu-rep"):
+    per = {}
+    for rep in reps:
+        for r in rows_of(rep):
             t = num(r["gpu__time_duration.sum"]) * TSCALE.get(r["gpu__time_duration.sum"][1], 1.0)
             dr = num(r["dram__bytes_read.sum"]) * SCALE.get(r["dram__bytes_read.sum"][1], 1)
             dw = num(r["dram__bytes_write.sum"]) * SCALE.get(r["dram__bytes_write.sum"][1], 1)
@@ -55,16 +57,11 @@ def main():
             vals = [f"{num(r[m]):.1f}" if m in r else "-" for _, m in COLS[1:]]
             lines.append(f"{k} | {t:.2f} | {(dr + dw) / 1e6:.1f} | " + " | ".join(vals) +
                          f" | {r['launch__grid_size'][0]} x {r['launch__block_size'][0]}")
-            base = re.sub(r"<.*", "", k)
-            if base == "tc_gemm_kernel":
-                gemm.append(dr + dw)
-            else:
-                traffic[base] = dr + dw
-    if gemm:
-        traffic["tc_gemm_kernel"] = sum(gemm) / len(gemm)
-    traffic["_source"] = ("ncu --set full --clock-control none (scripts/round_ncu.sh), c3 step, "
-                          "DRAM read+write bytes per launch; tc_gemm_kernel = mean of the "
-                          f"{len(gemm)} captured launches")
+            per.setdefault(re.sub(r"<.*", "", k), []).append(dr + dw)
+    traffic = {k: sum(v) / len(v) for k, v in per.items()}
+    traffic["_source"] = (f"ncu --set full --clock-control none (scripts/round2_ncu.sh), {cfg} "
+                          "step, DRAM read+write bytes per launch (mean over the captured "
+                          "launches of each kernel)")
     open(md, "w").write("\n".join(lines) + "\n")
     json.dump(traffic, open(js, "w"), indent=1)
     print("\n".join(lines))

@@ -181,3 +181,39 @@ def test_adagrad_state_belongs_to_the_optimizer(golden):
     train_step(m1, batches[3 % len(batches)].dense.astype(np.float32),
                sp(batches[3 % len(batches)]), batches[3 % len(batches)].labels, oa)
     assert not all(torch.equal(x, y) for x, y in zip(a_state, oa._table_state.values()))
+
+
+def test_async_results_match_sync_and_report_their_own_error(golden):
+    """train_step(sync=False): the results read after later steps were
+    issued equal the synchronous ones; a bad index in one step raises with
+    THAT step's payload when its result is read, and that step's update is
+    skipped while the steps around it apply."""
+    fx = golden("traj_c1s.npz")
+    c, batches = traj_inputs(fx)
+    sb = lambda hb, idx=None: [SparseBatch(o, i) for o, i in
+                               zip(hb.offsets, idx if idx is not None else hb.indices)]
+    ma, mb = build(c), build(c)
+    ra = [train_step(ma, hb.dense, sb(hb), hb.labels, Sgd(0.1)) for hb in batches]
+    pend = [train_step(mb, hb.dense, sb(hb), hb.labels, Sgd(0.1), sync=False) for hb in batches]
+    for x, y in zip(ra, pend):
+        assert x.loss == y.loss and x.accuracy == y.accuracy and torch.equal(x.probs, y.probs)
+    for a, b in zip(arrays(ma.bottom, ma.top, ma.tables), arrays(mb.bottom, mb.top, mb.tables)):
+        assert np.array_equal(a, b)
+    # a bad index in the middle step of three
+    m = build(c)
+    bad = [i.copy() for i in batches[1].indices]
+    bad[2][5] = c["tables"][2] + 77
+    p0 = train_step(m, batches[0].dense, sb(batches[0]), batches[0].labels, Sgd(0.1), sync=False)
+    p1 = train_step(m, batches[1].dense, sb(batches[1], bad), batches[1].labels, Sgd(0.1),
+                    sync=False)
+    p2 = train_step(m, batches[2].dense, sb(batches[2]), batches[2].labels, Sgd(0.1), sync=False)
+    assert p0.loss > 0 and p2.loss > 0
+    with pytest.raises(LookupIndexError) as e:
+        _ = p1.loss
+    assert (e.value.table_id, e.value.position, e.value.index) == (2, 5, c["tables"][2] + 77)
+    # same as running steps 0 and 2 synchronously (step 1 skipped its updates)
+    r = build(c)
+    train_step(r, batches[0].dense, sb(batches[0]), batches[0].labels, Sgd(0.1))
+    train_step(r, batches[2].dense, sb(batches[2]), batches[2].labels, Sgd(0.1))
+    for a, b in zip(arrays(m.bottom, m.top, m.tables), arrays(r.bottom, r.top, r.tables)):
+        assert np.array_equal(a, b)
