@@ -568,11 +568,11 @@ def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
         while True:
             yield hbs[s % len(hbs)]
             s += 1
-    # 4 packing threads: measured best on the 16-core GPU hosts (more threads
-    # contend with the stepping thread: 0.57 / 0.74 / 0.86 ms per step at
-    # 4 / 8 / 16, scripts/e2e_prof.py)
-    pf = Prefetcher(source(), B, T, cfg.dense_dim, capacities=caps, depth=3,
-                    threads=min(4, max(1, (os.cpu_count() or 2) // 4)))
+    # two packing workers x 4 native threads each (16-core GPU hosts: one
+    # c3 batch packs in 0.32 ms on 4 threads, scripts/pack_bench.py; two
+    # batches in flight keep the input ahead of the 0.4 ms step)
+    pf = Prefetcher(source(), B, T, cfg.dense_dim, capacities=caps, depth=4,
+                    threads=min(4, max(1, (os.cpu_count() or 2) // 4)), workers=2)
     it = iter(pf)
     opt = Sgd(0.1)
     for _ in range(warmup + 2):   # eager step, graph capture, warm-up

@@ -141,6 +141,8 @@ extern "C" int dlrm_random_bags(uint64_t* state, const int64_t* rows, int32_t nt
 // float64 -> fp32, per-table offsets / indices int64 (and weights float64 ->
 // fp32).  The copies run on `nthreads` native threads, without the Python
 // GIL (the Prefetcher's worker calls this through ctypes).
+#include <emmintrin.h>
+
 #include <algorithm>
 #include <thread>
 #include <vector>
@@ -165,7 +167,11 @@ extern "C" int dlrm_pack_batch(uint8_t* dst, const int64_t* sec /* x, labels, of
   int64_t* idx = reinterpret_cast<int64_t*>(dst + sec[3]);
   float* iw = sec[4] >= 0 ? reinterpret_cast<float*>(dst + sec[4]) : nullptr;
   const int nth = std::max(1, std::min(int(nthreads), 64));
-  // work items: dense row slabs, then tables
+  // work items: dense row slabs, then tables.  The block is written with
+  // streaming (non-temporal) stores: it is only read again by the H2D DMA,
+  // and regular stores would first read every destination line (the host's
+  // memory bandwidth is what the input pipeline is bound by, shared with
+  // that DMA).
   const int64_t slabs = std::min<int64_t>(nth, std::max<int64_t>(1, batch / 64));
   const int64_t items = slabs + nt;
   auto work = [&](int64_t it) {
@@ -174,15 +180,33 @@ extern "C" int dlrm_pack_batch(uint8_t* dst, const int64_t* sec /* x, labels, of
       for (int64_t r = r0; r < r1; ++r) {
         const double* s = dense + r * ld_dense;
         float* d = x + r * ldx;
-        for (int64_t c = 0; c < k0; ++c) d[c] = float(s[c]);
+        int64_t c = 0;
+        if ((reinterpret_cast<uintptr_t>(d) & 15) == 0)
+          for (; c + 4 <= k0; c += 4) {
+            const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(s + c));
+            const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(s + c + 2));
+            _mm_stream_ps(d + c, _mm_movelh_ps(lo, hi));
+          }
+        for (; c < k0; ++c) d[c] = float(s[c]);
       }
       if (it == 0)
         for (int64_t r = 0; r < batch; ++r) lab[r] = float(labels[r]);
+      _mm_sfence();
       return;
     }
     const int t = int(it - slabs);
     memcpy(offs + int64_t(t) * (batch + 1), offsets[t], size_t(batch + 1) * 8);
-    if (nnz[t] > 0) memcpy(idx + cap_base[t], indices[t], size_t(nnz[t]) * 8);
+    if (nnz[t] > 0) {
+      int64_t* d = idx + cap_base[t];
+      const int64_t* src = indices[t];
+      int64_t i = 0, n = nnz[t];
+      if ((reinterpret_cast<uintptr_t>(d) & 15) != 0 && n > 0) d[i] = src[i], ++i;
+      for (; i + 2 <= n; i += 2)
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i),
+                         _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i)));
+      for (; i < n; ++i) d[i] = src[i];
+      _mm_sfence();
+    }
     if (iw) {
       float* w = iw + cap_base[t];
       const double* src = weights ? weights[t] : nullptr;

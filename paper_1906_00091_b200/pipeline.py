@@ -245,12 +245,13 @@ class Prefetcher:
     tuples, or objects with those attributes (``rng.HostBatch``).
     ``capacities`` bounds each table's index count (the layout is static so
     the step engine can replay one CUDA graph); default: the largest count of
-    the first batch + 25%.  ``depth`` ring slots are in flight; ``threads``
-    pack each batch in parallel."""
+    the first batch + 25%.  ``depth`` ring slots are in flight; ``workers``
+    threads pack consecutive batches concurrently (each with ``threads``
+    native threads) and the batches are handed out in source order."""
 
     def __init__(self, source, batch_size: int, num_tables: int, dense_dim: int,
                  capacities=None, depth: int = 3, threads: int = 4, weighted: bool = False,
-                 device=None):
+                 device=None, workers: int = 2):
         self._src = iter(source)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self._first = None
@@ -263,12 +264,21 @@ class Prefetcher:
         self.layout = InputLayout(batch_size, num_tables, dense_dim, capacities, weighted)
         self._pool = ThreadPoolExecutor(max(1, int(threads)))
         self._free = queue.Queue()
-        self._ready = queue.Queue(maxsize=depth)
-        for _ in range(max(2, int(depth))):
+        nworkers = max(1, int(workers))
+        for _ in range(max(2, int(depth), nworkers + 1)):
             self._free.put(_Slot(self.layout, self.device))
+        # in-order hand-out: workers take (seq, batch) under _src_lock and
+        # publish results keyed by seq; __next__ waits for the next seq
+        self._src_lock = threading.Lock()
+        self._cv = threading.Condition()
+        self._done = {}
+        self._seq_in = 0
+        self._seq_out = 0
+        self._end = None  # seq of the end-of-source marker
         self._stop = False
-        self._worker = threading.Thread(target=self._run, daemon=True)
-        self._worker.start()
+        self._workers = [threading.Thread(target=self._run, daemon=True) for _ in range(nworkers)]
+        for w in self._workers:
+            w.start()
 
     def _next_host(self):
         try:
@@ -279,16 +289,39 @@ class Prefetcher:
             return (b.dense, b.offsets, b.indices, b.labels, getattr(b, "weights", None))
         return tuple(b) + ((None,) if len(b) == 4 else ())
 
+    def _publish(self, seq, item):
+        with self._cv:
+            self._done[seq] = item
+            self._cv.notify_all()
+
     def _run(self):
         torch.cuda.set_device(self.device)
         stream = torch.cuda.Stream(device=self.device)
-        try:
-            while not self._stop:
-                hb = self._first if self._first is not None else self._next_host()
+        while not self._stop:
+            slot = self._free.get()
+            if slot is None:
+                return
+            with self._src_lock:
+                seq = self._seq_in
+                if self._end is not None:
+                    self._free.put(slot)
+                    return
+                try:
+                    hb = self._first if self._first is not None else self._next_host()
+                except BaseException as e:  # surface source errors to the consumer
+                    self._end = seq
+                    self._seq_in += 1
+                    self._free.put(slot)
+                    self._publish(seq, e)
+                    return
                 self._first = None
+                self._seq_in += 1
                 if hb is None:
-                    break
-                slot = self._free.get()
+                    self._end = seq
+                    self._free.put(slot)
+                    self._publish(seq, None)
+                    return
+            try:
                 if slot.consumed_set:
                     stream.wait_event(slot.consumed)   # the step copied it out
                 slot.h2d_done.synchronize()             # the host block is free
@@ -299,11 +332,11 @@ class Prefetcher:
                     slot.h2d_done.record(stream)
                     slot.ready.record(stream)
                 nnz = [int(np.asarray(i).shape[0]) for i in idx]
-                self._ready.put((slot, nnz, weights is not None))
-        except BaseException as e:  # surface worker errors to the consumer
-            self._ready.put(e)
-            return
-        self._ready.put(None)
+                self._publish(seq, (slot, nnz, weights is not None))
+            except BaseException as e:
+                self._free.put(slot)
+                self._publish(seq, e)
+                return
 
     def _release(self, slot):
         self._free.put(slot)
@@ -312,9 +345,15 @@ class Prefetcher:
         return self
 
     def __next__(self):
-        item = self._ready.get()
+        with self._cv:
+            while self._seq_out not in self._done:
+                self._cv.wait()
+            item = self._done.pop(self._seq_out)
+            if item is None or isinstance(item, BaseException):
+                self._done[self._seq_out] = item  # stays at the end
+            else:
+                self._seq_out += 1
         if item is None:
-            self._ready.put(None)
             raise StopIteration
         if isinstance(item, BaseException):
             raise item
@@ -325,4 +364,6 @@ class Prefetcher:
 
     def close(self):
         self._stop = True
+        for _ in self._workers:
+            self._free.put(None)
         self._pool.shutdown(wait=False)

@@ -16,8 +16,8 @@ def gen():
     i = 0
     while True:
         yield hbs[i % 4]; i += 1
-pf = Prefetcher(gen(), 2048, 8, 512, capacities=caps, depth=int(os.environ.get("DEPTH", 3)),
-                threads=threads)
+pf = Prefetcher(gen(), 2048, 8, 512, capacities=caps, depth=int(os.environ.get("DEPTH", 4)),
+                threads=threads, workers=int(os.environ.get("WORKERS", 2)))
 it = iter(pf)
 opt = Sgd(0.1)
 for _ in range(6):
@@ -26,10 +26,12 @@ torch.cuda.synchronize()
 K = 100
 tn = tt = tl = 0.0
 prev = None
+evs = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
 t0 = time.perf_counter()
-for _ in range(K):
+for k in range(K):
     a = time.perf_counter(); d, b, l = next(it); tn += time.perf_counter() - a
     a = time.perf_counter(); r = train_step(model, d, b, l, opt, sync=False); tt += time.perf_counter() - a
+    evs[k].record()
     a = time.perf_counter()
     if prev is not None:
         _ = prev.loss
@@ -37,6 +39,9 @@ for _ in range(K):
     prev = r
 _ = prev.loss
 tot = time.perf_counter() - t0
-print(f"threads {threads}: step ms {tot / K * 1e3:.3f}; next() {tn / K * 1e3:.3f}, "
+torch.cuda.synchronize()
+gaps = [evs[k - 1].elapsed_time(evs[k]) for k in range(1, K)]
+print(f"device step-to-step ms: mean {sum(gaps) / len(gaps):.3f} min {min(gaps):.3f}")
+print(f"threads {threads} workers {os.environ.get('WORKERS', 2)}: step ms {tot / K * 1e3:.3f}; next() {tn / K * 1e3:.3f}, "
       f"train_step {tt / K * 1e3:.3f}, prev.loss {tl / K * 1e3:.3f}")
 pf.close()
