@@ -215,10 +215,14 @@ class StagedDense:
     def consume(self, engine_block: torch.Tensor, stream=None):
         """Copy the landed block into the engine's input block on ``stream``
         (after the H2D copy) and release the ring slot."""
-        s = stream or torch.cuda.current_stream()
+        cur = torch.cuda.current_stream()
+        s = stream or cur
         s.wait_event(self._slot.ready)
-        with torch.cuda.stream(s):
+        if s == cur:
             engine_block.copy_(self._slot.dev, non_blocking=True)
+        else:
+            with torch.cuda.stream(s):
+                engine_block.copy_(self._slot.dev, non_blocking=True)
         self._slot.consumed.record(s)
         self._slot.consumed_set = True
         self._pf._release(self._slot)

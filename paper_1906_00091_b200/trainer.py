@@ -206,12 +206,15 @@ class StepEngine:
         # concurrently with the weight-gradient stream: its own workspace
         self.lin_ws2 = torch.empty(lin, dtype=torch.uint8, device=dev)
         self.last_wgrad_main = os.environ.get("DLRM_LAST_WGRAD_MAIN", "1") != "0"
-        self.stats = torch.zeros(2, **f32)
-        self.err_pos = torch.empty(T, dtype=torch.int64, device=dev)
-        self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
-        # the offending index value per table, resolved on the device from the
-        # batch that ran (dlrm_err_resolve)
-        self.err_val = torch.zeros(T, dtype=torch.int64, device=dev)
+        # the step's host-visible results in ONE device block (one D2H copy
+        # per step): [loss sum, correct | error flag (int32), pad | error
+        # position per table (int64) | offending index value per table
+        # (int64, resolved on the device from the batch that ran)]
+        self.res_dev = torch.zeros(4 + 4 * T, **f32)
+        self.stats = self.res_dev[0:2]
+        self.err_flag = self.res_dev[2:3].view(torch.int32)
+        self.err_pos = self.res_dev[4:4 + 2 * T].view(torch.int64)
+        self.err_val = self.res_dev[4 + 2 * T:].view(torch.int64)
         # update rule fused into the step's kernels (ref optim.py): SGD, or
         # Adagrad with accumulators laid out exactly like the parameters
         from .optim import update_rule
@@ -837,10 +840,7 @@ class StepEngine:
                 old._materialise()
         h = self._ring[k]
         s = torch.cuda.current_stream()
-        h[2:3].view(torch.int32).copy_(self.err_flag, non_blocking=True)
-        h[0:2].copy_(self.stats, non_blocking=True)
-        h[4:4 + 2 * T].view(torch.int64).copy_(self.err_pos, non_blocking=True)
-        h[4 + 2 * T:4 + 4 * T].view(torch.int64).copy_(self.err_val, non_blocking=True)
+        h.copy_(self.res_dev, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(s)
         res = PendingStepResult(self, k, ev, self.prob.clone())
@@ -869,11 +869,10 @@ class StepEngine:
         sums come back with ONE synchronisation (two async copies into a
         pinned buffer); raises LookupIndexError after a bad index."""
         if self._res_host is None:
-            self._res_host = torch.zeros(4, dtype=torch.float32).pin_memory()
+            self._res_host = torch.zeros(4 + 4 * self.T, dtype=torch.float32).pin_memory()
         s = torch.cuda.current_stream()
         h = self._res_host
-        h[2:3].view(torch.int32).copy_(self.err_flag, non_blocking=True)
-        h[0:2].copy_(self.stats, non_blocking=True)
+        h.copy_(self.res_dev, non_blocking=True)
         probs = self.prob.clone()
         s.synchronize()
         if int(h[2:3].view(torch.int32)[0]):
