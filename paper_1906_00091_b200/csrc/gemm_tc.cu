@@ -573,6 +573,11 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
     return check_launch("tc_gemm_kernel");
   }
   // fused weight gradient: the split-K CTAs of a tile are one cluster
+  static bool nonportable = false;
+  if (splits > 8 && !nonportable) {
+    DLRM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    nonportable = true;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
@@ -616,11 +621,16 @@ int max_clusters(int cz) {
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) {
     cudaGetLastError();
-    n = kNumSMs / cz;
+    n = cz > 8 ? 0 : kNumSMs / cz;  // a non-portable size that does not fit: unused
   }
   cache[cz] = n;
   return n;
 }
+
+#ifndef DLRM_MAX_SPLIT
+#define DLRM_MAX_SPLIT 16
+#endif
+constexpr int kMaxSplit = DLRM_MAX_SPLIT;
 
 // Tile plan: the N tile and the split-K (cluster) size.
 struct TcPlan {
@@ -687,13 +697,17 @@ TcPlan cluster_plan(int64_t m_rows, int64_t n_grid, int64_t kt, int min_bn,
     if (bn < min_bn) continue;
     if (bn > 16 && n_grid <= bn / 2) continue;  // mostly empty tile
     const int64_t tiles = mt * ceil_div(n_grid, bn);
-    int64_t smax = kt / 4 < 8 ? kt / 4 : 8;
+    // up to 16 split-K CTAs per cluster (non-portable size above 8): the
+    // weight gradients of narrow layers over long batches (c4: 128 x 256
+    // outputs over K = 32768) have only a few output tiles
+    int64_t smax = kt / 4 < kMaxSplit ? kt / 4 : kMaxSplit;
     if (smax < 1) smax = 1;
     for (int64_t sp = 1; sp <= smax; ++sp) {
       const int cap_occ = bn == 128 ? max_clusters<A_MN, B_MN, 128>(int(sp))
                     : bn == 64  ? max_clusters<A_MN, B_MN, 64>(int(sp))
                     : bn == 32  ? max_clusters<A_MN, B_MN, 32>(int(sp))
                                 : max_clusters<A_MN, B_MN, 16>(int(sp));
+      if (cap_occ < 1) continue;
       // one_per_sm: narrow tiles sharing an SM also share its tensor core
       const int cap = one_per_sm && cap_occ > kNumSMs / int(sp) ? kNumSMs / int(sp) : cap_occ;
       const double waves = double(ceil_div(tiles, cap));

@@ -8,6 +8,8 @@ from paper_1906_00091_b200 import _lib
 def ceil4(n): return (n + 3) // 4 * 4
 B = int(os.environ.get("B", 2048))
 layers = [(512, 512), (512, 64), (100, 1024), (1024, 1024), (13, 512), (512, 256), (367, 512)]
+if os.environ.get("LAYERS") == "c4":  # B=32768 Terabyte-shaped MLPs
+    layers = [(480, 1024), (1024, 1024), (1024, 512), (512, 256), (13, 512), (512, 256), (256, 128)]
 res = []
 g = torch.Generator(device="cuda").manual_seed(0)
 for K, N in layers:
