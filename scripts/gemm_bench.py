@@ -11,6 +11,8 @@ layers = [(512, 512), (512, 64), (100, 1024), (1024, 1024), (13, 512), (512, 256
 if os.environ.get("LAYERS") == "c4":  # B=32768 Terabyte-shaped MLPs
     layers = [(480, 1024), (1024, 1024), (1024, 512), (512, 256), (13, 512), (512, 256), (256, 128)]
 res = []
+if os.environ.get("MODE"):
+    _lib.call("dlrm_gemm_mode", int(os.environ["MODE"]))
 g = torch.Generator(device="cuda").manual_seed(0)
 for K, N in layers:
     X = torch.randn((B, ceil4(K)), device="cuda", generator=g)
