@@ -700,7 +700,10 @@ TcPlan cluster_plan(int64_t m_rows, int64_t n_grid, int64_t kt, int min_bn,
     // up to 16 split-K CTAs per cluster (non-portable size above 8): the
     // weight gradients of narrow layers over long batches (c4: 128 x 256
     // outputs over K = 32768) have only a few output tiles
-    int64_t smax = kt / 4 < kMaxSplit ? kt / 4 : kMaxSplit;
+    // (16 only over long K — >= 256 k-blocks, c4's B = 32768; at B = 2048 the
+    // wider clusters measured no faster and cost a little at c2)
+    const int64_t lim = kt >= 256 ? kMaxSplit : (kMaxSplit < 8 ? kMaxSplit : 8);
+    int64_t smax = kt / 4 < lim ? kt / 4 : lim;
     if (smax < 1) smax = 1;
     for (int64_t sp = 1; sp <= smax; ++sp) {
       const int cap_occ = bn == 128 ? max_clusters<A_MN, B_MN, 128>(int(sp))
