@@ -1502,7 +1502,12 @@ extern "C" int dlrm_emb_fwd(const float* W_all, int64_t dim,
       if (cfg == 4) DLRM_STREAM(16, 32, 3, 8);
       if (cfg == 5) DLRM_STREAM(16, 16, 3, 8);
       if (cfg == 6) DLRM_STREAM(16, 16, 2, 8);
-      DLRM_STREAM(16, 16, 3, 16);
+      if (cfg == 10) DLRM_STREAM(16, 8, 4, 24);
+      if (cfg == 11) DLRM_STREAM(16, 8, 3, 32);
+      if (cfg == 9) DLRM_STREAM(16, 16, 3, 16);
+      // 24 warps x 2 slots of 16-row chunks (c3 step 0.4095 -> 0.4067 ms
+      // over two A/B runs; the round-1 default is cfg 9)
+      DLRM_STREAM(16, 16, 2, 24);
     }
     if (nv0 == 32) {
       // 512-byte rows: 16 warps of 8-row chunks (c4 pooling-1 lookup 263 ->
