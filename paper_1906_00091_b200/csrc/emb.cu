@@ -1064,13 +1064,16 @@ __global__ void seg_plan_kernel(FoldArgs fa, uint32_t max_runs, uint32_t max_seg
   if (threadIdx.x == blockDim.x - 1) seg_base[max_runs] = min(s_tot[threadIdx.x], max_segs);
 }
 
+#ifndef DLRM_SEG_U
+#define DLRM_SEG_U 16  // Zipf c5 point, d = 64: apply 127 -> 115 us; d = 128: 164 -> 157 us
+#endif
 template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
 seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
                 const uint32_t* seg_base, const uint32_t* seg_run, float* partial) {
   pdl_entry();
   constexpr int RPI = 32 / LPB;
-  constexpr int U = NV == 1 ? 4 : 2;
+  constexpr int U = NV == 1 ? DLRM_SEG_U : 2;  // U * RPI gradient rows in flight per warp
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPB, col = lane % LPB;
   const uint32_t nseg = seg_base[max_runs];
