@@ -1065,7 +1065,7 @@ __global__ void seg_plan_kernel(FoldArgs fa, uint32_t max_runs, uint32_t max_seg
 }
 
 #ifndef DLRM_SEG_U
-#define DLRM_SEG_U 16  // Zipf c5 point, d = 64: apply 127 -> 115 us; d = 128: 164 -> 157 us
+#define DLRM_SEG_U 32  // cap; Zipf c5 point d = 64: apply 127 -> 115 us (16 rows), d = 128: 164 -> 160 us
 #endif
 template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
@@ -1073,7 +1073,8 @@ seg_fold_kernel(FoldArgs fa, TableSet ts, int64_t dim, uint32_t max_runs,
                 const uint32_t* seg_base, const uint32_t* seg_run, float* partial) {
   pdl_entry();
   constexpr int RPI = 32 / LPB;
-  constexpr int U = NV == 1 ? DLRM_SEG_U : 2;  // U * RPI gradient rows in flight per warp
+  // U * RPI gradient rows in flight per warp: the whole 32-slot batch
+  constexpr int U = NV == 1 ? (32 / RPI < DLRM_SEG_U ? 32 / RPI : DLRM_SEG_U) : 2;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPB, col = lane % LPB;
   const uint32_t nseg = seg_base[max_runs];

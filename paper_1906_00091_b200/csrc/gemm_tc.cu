@@ -509,6 +509,266 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
+// Persistent variant for tile grids larger than the SMs (the B = 32768 MLPs):
+// one CTA per SM walks output tiles tile = blockIdx.x, + gridDim.x, ... (the
+// n tiles of an m row back to back, so the CTAs in flight share A rows in L2)
+// with the same producer / MMA / splitter roles as tc_gemm_kernel (BN = 128,
+// stage and A-slot counters running across tiles, so the producer fills the
+// next tile's stages while this tile finishes), plus 8 epilogue warps: they
+// drain the tile's [big | small] accumulators from TMEM into registers,
+// release TMEM to the MMA issuer (acc_empty) and only then do the smem
+// transpose and global stores — the next tile's MMAs overlap the stores.
+constexpr int P_EPI_WARPS = 8;
+constexpr int P_THREADS = THREADS + 32 * P_EPI_WARPS;
+
+template <bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(P_THREADS, 1)
+tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB, TcArgs args, int64_t n_tiles,
+                          int64_t tiles) {
+  constexpr int BN = 128;
+  constexpr uint32_t A_BYTES = BM * BK * 4;
+  constexpr uint32_t B_BYTES = BN * BK * 4;
+  constexpr uint32_t STAGE_BYTES = A_BYTES + 2 * B_BYTES;
+  constexpr uint32_t TMA_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t ACC_COLS = 2 * BN;  // one [big | small] pair
+  constexpr int ASLOTS = 4;
+  constexpr uint32_t TMEM_COLS = 512;
+  static_assert(ACC_COLS + 64 * ASLOTS <= TMEM_COLS, "TMEM overflow");
+  constexpr uint32_t IDESC = instr_desc(BN, false, B_MN);
+  constexpr uint32_t IDESC2 = instr_desc(2 * BN, false, B_MN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;                                // TSTAGES x STAGE_BYTES
+  float* etile = reinterpret_cast<float*>(smem + TSTAGES * STAGE_BYTES);  // [8 warps][32][20]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(etile + P_EPI_WARPS * 32 * 20);
+  uint64_t* full = bars;                               // TMA landed        [T]
+  uint64_t* empty_t = bars + TSTAGES;                  // MMA done, stage   [T]
+  uint64_t* conv = bars + 2 * TSTAGES;                 // A slot + B_lo set [L]
+  uint64_t* empty_l = bars + 2 * TSTAGES + ASLOTS;     // MMA done, A slot  [L]
+  uint64_t* acc_full = bars + 2 * TSTAGES + 2 * ASLOTS;  // tile accumulated
+  uint64_t* acc_empty = acc_full + 1;                    // accumulators drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nk = args.k_tiles;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty_t[s], 1);
+    }
+    for (int s = 0; s < ASLOTS; ++s) {
+      mbar_init(&conv[s], SPLIT_WARPS);
+      mbar_init(&empty_l[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, P_EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see tc_gemm_kernel)
+  pdl_wait();
+
+  if (warp == 0) {
+    // ---- TMA producer, k-blocks of all this CTA's tiles back to back
+    if (lane == 0) {
+      int g = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+        for (int it = 0; it < nk; ++it, ++g) {
+          const int s = g % TSTAGES;
+          if (g >= TSTAGES) mbar_wait(&empty_t[s], ((g / TSTAGES) - 1) & 1);
+          uint8_t* st = ring + s * STAGE_BYTES;
+          const int k0 = it * BK;
+          mbar_expect_tx(&full[s], TMA_BYTES);
+          if (A_MN && args.a3d) {
+            tma_load_3d(st, &tmA, &full[s], 0, k0, int(m0 / 32));
+          } else if (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c)
+              tma_load_2d(st + c * 32 * BK * 4, &tmA, &full[s], int(m0 + 32 * c), k0);
+          } else {
+            tma_load_2d(st, &tmA, &full[s], k0, int(m0));
+          }
+          uint8_t* sb = st + A_BYTES;
+          if (B_MN && args.b3d) {
+            tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
+          } else if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c)
+              tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
+          } else {
+            tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      int g = 0, ti = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+        // the epilogue warps have drained the previous tile's accumulators
+        if (ti >= 1) mbar_wait(acc_empty, (ti - 1) & 1);
+        tc_fence_after();
+        for (int it = 0; it < nk; ++it, ++g) {
+          const int t = g % TSTAGES, l = g % ASLOTS;
+          mbar_wait(&conv[l], (g / ASLOTS) & 1);
+          tc_fence_after();
+          const uint32_t b_hi = smem_u32(ring + t * STAGE_BYTES) + A_BYTES;
+          const uint32_t a_hi = tmem + ACC_COLS + uint32_t(64 * l);
+          const uint32_t a_lo = a_hi + 32;
+          const uint32_t big = tmem, small = tmem + uint32_t(BN);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
+            const uint32_t b_lbo = B_MN ? 32 * BK * 4 : 16, b_sbo = B_MN ? 512 : 1024;
+            const uint32_t b_lay = B_MN ? 1 : 2;
+            const uint64_t dbh = smem_desc(b_hi + bo, b_lbo, b_sbo, b_lay);
+            const uint32_t first = (it > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ts(big, a_hi + 8 * kk, dbh, IDESC2, first);  // [big | small] = A_hi x [B_hi | B_lo]
+            mma_tf32_ts(small, a_lo + 8 * kk, dbh, IDESC, 1u);    // small += A_lo x B_hi
+          }
+          mma_commit(&empty_t[t]);
+          mma_commit(&empty_l[l]);
+        }
+        mma_commit(acc_full);
+      }
+    }
+  } else if (warp < 2 + SPLIT_WARPS) {
+    // ---- splitter warps (2..9), as in tc_gemm_kernel
+    const int ct = threadIdx.x - 64;
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int arow = 32 * q + lane;
+    constexpr int B_F4 = int(B_BYTES / 16);
+    constexpr int NSPLIT = 32 * SPLIT_WARPS;
+    constexpr int NJ = (B_F4 + NSPLIT - 1) / NSPLIT;
+    const uint32_t a_taddr = tmem + (uint32_t(32 * q) << 16) + ACC_COLS + uint32_t(16 * h);
+    int g = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int it = 0; it < nk; ++it, ++g) {
+        const int t = g % TSTAGES, l = g % ASLOTS;
+        mbar_wait(&full[t], (g / TSTAGES) & 1);
+        if (g >= ASLOTS) mbar_wait(&empty_l[l], ((g / ASLOTS) - 1) & 1);
+        tc_fence_after();
+        const uint8_t* st = ring + t * STAGE_BYTES;
+        float x[16];
+        if (A_MN) {
+          const float* src = reinterpret_cast<const float*>(st + q * 32 * BK * 4);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int kr = 16 * h + i;
+            x[i] = src[kr * 32 + 8 * ((lane >> 3) ^ (kr & 3)) + (lane & 7)];
+          }
+        } else {
+          const float4* src = reinterpret_cast<const float4*>(st + arow * 128);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float4 v = src[(4 * h + c) ^ (arow & 7)];
+            x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+          }
+        }
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          hi[i] = __float_as_uint(x[i]) & 0xFFFFE000u;
+          lo[i] = lo_bits(x[i] - __uint_as_float(hi[i]));
+        }
+        const uint32_t slot = a_taddr + uint32_t(64 * l);
+        tmem_st16(slot, hi);
+        tmem_st16(slot + 32, lo);
+        const float4* src_b = reinterpret_cast<const float4*>(st + A_BYTES);
+        float4* dst_b = reinterpret_cast<float4*>(const_cast<uint8_t*>(st) + A_BYTES + B_BYTES);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int i = ct + NSPLIT * j;
+          if (B_F4 % NSPLIT == 0 || i < B_F4) {
+            const float4 v = src_b[i];
+            dst_b[i] = make_float4(__uint_as_float(lo_bits(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u))),
+                                   __uint_as_float(lo_bits(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u))),
+                                   __uint_as_float(lo_bits(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u))),
+                                   __uint_as_float(lo_bits(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u))));
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[l]);
+      }
+    }
+  } else {
+    // ---- epilogue warps (10..17): TMEM lane quarter q = warp % 4, column
+    // half by warp; the whole 32 x 64 block is drained into registers before
+    // the accumulators are released
+    const int ew = warp - 2 - SPLIT_WARPS;  // 0..7
+    const int q = warp & 3, half = ew >> 2;
+    float* tile_s = etile + ew * (32 * 20);
+    const GemmEpilogue& ep = args.ep;
+    constexpr int CW = BN / 2;  // 64 columns per warp
+    int ti = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++ti) {
+      const int64_t m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * BN;
+      mbar_wait(acc_full, ti & 1);
+      tc_fence_after();
+      float v[CW];
+      const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16) + uint32_t(half * CW);
+#pragma unroll
+      for (int c = 0; c < CW; c += 16) {
+        uint32_t rb[16], rs[16];
+        tmem_ld16_issue(lane_base + uint32_t(c), rb);
+        tmem_ld16_issue(lane_base + uint32_t(BN + c), rs);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[c + i] = __uint_as_float(rb[i]) + __uint_as_float(rs[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);  // the next tile's MMAs may start
+#pragma unroll
+      for (int c = 0; c < CW; c += 16) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(tile_s + lane * 20 + i) =
+              make_float4(v[c + i], v[c + i + 1], v[c + i + 2], v[c + i + 3]);
+        __syncwarp();
+        const int c4 = (lane & 3) * 4;
+#pragma unroll
+        for (int r = lane >> 2; r < 32; r += 8) {
+          const int64_t row = m0 + 32 * q + r;
+          if (row < args.M)
+            apply_epilogue4(ep, row, n0 + half * CW + c + c4, args.N,
+                            *reinterpret_cast<const float4*>(tile_s + r * 20 + c4), 0);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 int g_tc_mode = 0;  // 0: use tcgen05 where the shape allows; 1: never
@@ -568,6 +828,23 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   }
   const dim3 grid(unsigned(ceil_div(n_grid, BN)), unsigned(ceil_div(args.M, BM)),
                   unsigned(splits));
+  const int64_t tiles = int64_t(grid.x) * grid.y;
+  static const bool persist_ok = !getenv("DLRM_GEMM_PERSIST") ||
+                                 atoi(getenv("DLRM_GEMM_PERSIST")) != 0;
+  if (BN == 128 && !args.wf.on && splits == 1 && tiles > kNumSMs && persist_ok) {
+    // more tiles than SMs: persistent CTAs, the next tile's loads and MMAs
+    // overlap this tile's epilogue
+    auto kp = tc_gemm_persistent_kernel<A_MN, B_MN>;
+    const size_t psm = sm + size_t(P_EPI_WARPS) * 32 * 20 * 4;
+    static bool pconf = false;
+    if (!pconf) {
+      DLRM_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psm)));
+      pconf = true;
+    }
+    launch(kp, unsigned(tiles < kNumSMs ? tiles : kNumSMs), P_THREADS, psm, s, a, b, args,
+           int64_t(grid.x), tiles);
+    return check_launch("tc_gemm_persistent_kernel");
+  }
   if (!args.wf.on) {
     launch(k, grid, THREADS, sm, s, a, b, args);
     return check_launch("tc_gemm_kernel");

@@ -18,7 +18,9 @@ SHAPES = [(2048, 1024, 1024), (2048, 512, 512), (2048, 64, 512), (2048, 1024, 10
           (2048, 512, 13), (128, 512, 52), (64, 256, 367), (33, 30, 64), (300, 16, 64),
           (4096, 128, 479), (2048, 16, 64),
           # narrow layer inputs (the dense features): the slab weight gradient
-          (128, 512, 13), (32768, 512, 13), (2048, 300, 32), (1000, 7, 3), (5, 130, 16)]
+          (128, 512, 13), (32768, 512, 13), (2048, 300, 32), (1000, 7, 3), (5, 130, 16),
+          # more output tiles than SMs: the persistent kernel (partial tiles too)
+          (4096, 1024, 1024), (20000, 640, 480), (32768, 256, 512), (8200, 1000, 300)]
 
 
 def ceil4(n):
