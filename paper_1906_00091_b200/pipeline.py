@@ -367,7 +367,11 @@ class Prefetcher:
         return dense, [StagedSparse(L.B, n, weighted) for n in nnz], StagedLabels(L.B)
 
     def close(self):
+        """Stop the workers and wait for them (a worker inside the native
+        packer must not be torn down with the interpreter)."""
         self._stop = True
         for _ in self._workers:
             self._free.put(None)
+        for w in self._workers:
+            w.join(timeout=10.0)
         self._pool.shutdown(wait=False)
