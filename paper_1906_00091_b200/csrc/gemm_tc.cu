@@ -747,7 +747,9 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
               make_float4(v[c + i], v[c + i + 1], v[c + i + 2], v[c + i + 3]);
         __syncwarp();
         const int c4 = (lane & 3) * 4;
-#pragma unroll
+        // rolled: 4 inlined epilogues, not 16 (fully unrolled, the kernel's
+        // SASS doubled and the epilogue stalled on instruction fetch)
+#pragma unroll 1
         for (int r = lane >> 2; r < 32; r += 8) {
           const int64_t row = m0 + 32 * q + r;
           if (row < args.M)

@@ -20,7 +20,9 @@ SHAPES = [(2048, 1024, 1024), (2048, 512, 512), (2048, 64, 512), (2048, 1024, 10
           # narrow layer inputs (the dense features): the slab weight gradient
           (128, 512, 13), (32768, 512, 13), (2048, 300, 32), (1000, 7, 3), (5, 130, 16),
           # more output tiles than SMs: the persistent kernel (partial tiles too)
-          (4096, 1024, 1024), (20000, 640, 480), (32768, 256, 512), (8200, 1000, 300)]
+          (4096, 1024, 1024), (20000, 640, 480), (32768, 256, 512), (8200, 1000, 300),
+          # one wave just short of the SMs (ragged rows / columns / K too)
+          (2000, 1000, 1000), (1500, 1024, 2048), (2048, 640, 700)]
 
 
 def ceil4(n):
@@ -124,3 +126,19 @@ def test_tensor_core_path_differs_from_simt():
     e_simt = maxnorm_err(y_simt.cpu(), ref.cpu())
     print(f"K=1024 normwise error: tcgen05 3xTF32 {e_tc:.2e}, SIMT fp32 {e_simt:.2e}")
     assert e_tc < 2e-5  # TC fp32 accumulation is ~6x looser than FFMA chains
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 1024, 1024), (4096, 1000, 1000)])
+def test_gemm_is_deterministic(M, N, K):
+    """Each output element is one fixed-order reduction: repeated calls (the
+    one-wave kernel and the persistent one) are bitwise equal."""
+    X = torch.zeros((M, ceil4(K)), device="cuda")
+    X[:, :K] = rand((M, K), 13)
+    W = torch.zeros((N, ceil4(K)), device="cuda")
+    W[:, :K] = rand((N, K), 14, K ** -0.5)
+    b = rand((N,), 15)
+    _lib.call("dlrm_gemm_mode", 0)
+    ys = [linear_fwd(X, W, b, N, K, 0) for _ in range(3)]
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    ref = X[:, :K].double() @ W[:, :K].double().T + b.double()
+    assert maxnorm_err(ys[0][:, :N].cpu(), ref.cpu()) < TOL
