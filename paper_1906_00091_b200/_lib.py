@@ -135,6 +135,29 @@ def lib():
     return _lib
 
 
+PYLIB_PATH = os.path.join(_HERE, "libdlrmpy.so")
+_pylib = None
+
+
+def pylib():
+    """libdlrmpy.so (csrc/pyhost.c: batch packing straight from the Python
+    arrays, buffer protocol in C, GIL released around dlrm_pack_batch),
+    loaded with ctypes.PyDLL; None when it was not built."""
+    global _pylib
+    if _pylib is None:
+        lib()
+        if not os.path.exists(PYLIB_PATH):
+            _pylib = False
+        else:
+            L = C.PyDLL(PYLIB_PATH)
+            f = L.dlrm_pack_batch_py
+            po = C.py_object
+            f.argtypes = [po, po, po, po, po, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _i32]
+            f.restype = C.c_int
+            _pylib = L
+    return _pylib or None
+
+
 class KernelError(RuntimeError):
     pass
 

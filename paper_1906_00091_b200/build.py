@@ -66,13 +66,33 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
+    relinked = force or jobs or _stale(LIB, objs)
+    if relinked:
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link of libdlrmb200.so failed")
+    _build_pyhost(force or relinked)
     return LIB
+
+
+def _build_pyhost(force: bool) -> None:
+    """libdlrmpy.so: the Python-facing packing entry (csrc/pyhost.c), a
+    plain C shared object against the interpreter's headers, linked to
+    libdlrmb200.so next to it."""
+    import sysconfig
+    src = os.path.join(CSRC, "pyhost.c")
+    out = os.path.join(PKG, "libdlrmpy.so")
+    if not force and not _stale(out, [src, LIB] + _headers()):
+        return
+    cmd = ["gcc", "-O2", "-shared", "-fPIC", "-Wall", f"-I{sysconfig.get_paths()['include']}",
+           f"-I{os.path.join(ROOT, 'include')}", src, "-o", out, f"-L{PKG}", "-ldlrmb200",
+           "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError("build of libdlrmpy.so failed")
 
 
 if __name__ == "__main__":

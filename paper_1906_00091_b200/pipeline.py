@@ -29,6 +29,8 @@ from concurrent.futures import ThreadPoolExecutor
 import numpy as np
 import torch
 
+from . import _lib
+
 __all__ = ["InputLayout", "Prefetcher", "StagedDense", "StagedSparse", "StagedLabels"]
 
 
@@ -57,6 +59,12 @@ class InputLayout:
             self.sections[name] = (o, nbytes)
             o = a16(o + nbytes)
         self.nbytes = o
+        # the native packer's section offsets and capacity prefix (kept alive
+        # with the layout: their addresses go to C on every batch)
+        self._sec = np.array([self.sections["x"][0], self.sections["labels"][0],
+                              self.sections["offsets"][0], self.sections["indices"][0],
+                              self.sections["iweights"][0] if self.weighted else -1], np.int64)
+        self._cap_base_ptr = self.cap_base.ctypes.data
 
     def key(self):
         return (self.B, self.T, self.k0, tuple(self.caps), self.weighted)
@@ -95,9 +103,22 @@ class InputLayout:
         """Write one batch of host arrays into the (pinned) host block ``blk``
         (reused; returns it).  With ``pool`` the dense rows (in row slabs) and
         every table's offsets / indices are copied by the pool's threads."""
+        threads = pool._max_workers if pool is not None else 1
+        if weights is not None and any(w is not None for w in weights) and not self.weighted:
+            raise ValueError("weighted bags need a weighted input layout")
+        PL = _lib.pylib()
+        if PL is not None:
+            # validation, pointers and packing in C (no per-table Python)
+            rc = PL.dlrm_pack_batch_py(dense, labels, offsets, indices, weights,
+                                       blk.data_ptr(), self._sec.ctypes.data, self.B, self.k0,
+                                       _ceil4(self.k0), self.T, self._cap_base_ptr,
+                                       int(max(1, threads)))
+            if rc == 0:
+                return blk
+            if rc >= 2:
+                self.check(indices, weights)  # raises the OverflowError
         self.check(indices, weights)
-        if self._pack_native(blk, dense, offsets, indices, labels, weights,
-                             pool._max_workers if pool is not None else 1):
+        if self._pack_native(blk, dense, offsets, indices, labels, weights, threads):
             return blk
         a = blk.numpy()
         B, T = self.B, self.T

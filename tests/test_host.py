@@ -167,6 +167,59 @@ def test_input_layout_pack_serial_and_threaded():
                hb.labels)
 
 
+def test_pack_paths_agree():
+    """The C-side packer (libdlrmpy.so: buffer protocol, no per-table
+    Python) writes the same block as the ctypes path and the numpy path,
+    for the reference dtypes, weighted bags with unweighted tables, a
+    strided dense view, and inputs it must hand back to numpy (float32
+    dense, int32 indices); capacities still raise OverflowError."""
+    import torch
+    from paper_1906_00091_b200 import _lib
+    from paper_1906_00091_b200.pipeline import InputLayout
+    from paper_1906_00091_b200.rng import RandomBatchSource
+    assert _lib.pylib() is not None, "libdlrmpy.so not built"
+    src = RandomBatchSource([50, 70, 90, 40], 13, 200, 6, False, seed=5)
+    hb = src.next_batch()
+    caps = [len(i) + 3 for i in hb.indices]
+    wide = np.zeros((200, 20))
+    wide[:, 3:16] = hb.dense
+    cases = [
+        (hb.dense, hb.offsets, hb.indices, None, False),
+        (hb.dense, hb.offsets, hb.indices,
+         [np.linspace(0.5, 1.5, len(i)) if t % 2 == 0 else None
+          for t, i in enumerate(hb.indices)], True),
+        (wide[:, 3:16], hb.offsets, hb.indices, None, False),
+        (hb.dense.astype(np.float32), hb.offsets, hb.indices, None, False),
+        (hb.dense, hb.offsets, [i.astype(np.int32) for i in hb.indices], None, False),
+    ]
+    PL = _lib.pylib()
+    for k, (dense, offs, idx, w, weighted) in enumerate(cases):
+        L = InputLayout(200, 4, 13, caps, weighted)
+        a, c = (torch.zeros(L.nbytes, dtype=torch.uint8) for _ in range(2))
+        if weighted:
+            for blk in (a, c):
+                L.views(blk)["iweights"].fill_(1.0)
+        rc = PL.dlrm_pack_batch_py(dense, hb.labels, offs, idx, w, a.data_ptr(),
+                                   L._sec.ctypes.data, 200, 13, 16, 4, L._cap_base_ptr, 2)
+        assert rc == (0 if k < 3 else 1)  # the last two go back to numpy
+        L.pack(a, dense, offs, idx, hb.labels, w)
+        pl, _lib._pylib = _lib._pylib, False  # the ctypes / numpy paths
+        try:
+            L.pack(c, dense, offs, idx, hb.labels, w)
+        finally:
+            _lib._pylib = pl
+        assert torch.equal(a, c)
+        v = L.views(a)
+        assert np.array_equal(v["x"][:, :13].numpy(), np.asarray(dense, np.float32))
+        for t in range(4):
+            cb = int(L.cap_base[t])
+            assert np.array_equal(v["indices"][cb:cb + len(idx[t])].numpy(), idx[t])
+    L = InputLayout(200, 4, 13, [5] * 4)
+    with pytest.raises(OverflowError):
+        L.pack(torch.zeros(L.nbytes, dtype=torch.uint8), hb.dense, hb.offsets, hb.indices,
+               hb.labels)
+
+
 def test_traffic_balanced_plan():
     """policy="traffic": equal-traffic tables spread evenly whatever their
     sizes (the reference plan gives one of 8 GPUs 19 of the 26 Criteo-Kaggle
