@@ -22,7 +22,10 @@ SHAPES = [(2048, 1024, 1024), (2048, 512, 512), (2048, 64, 512), (2048, 1024, 10
           # more output tiles than SMs: the persistent kernel (partial tiles too)
           (4096, 1024, 1024), (20000, 640, 480), (32768, 256, 512), (8200, 1000, 300),
           # one wave just short of the SMs (ragged rows / columns / K too)
-          (2000, 1000, 1000), (1500, 1024, 2048), (2048, 640, 700)]
+          (2000, 1000, 1000), (1500, 1024, 2048), (2048, 640, 700),
+          # narrow inputs over long batches: the SIMT skinny forward / weight
+          # gradient (ragged column counts, padding columns)
+          (9000, 130, 5), (8200, 7, 16), (16384, 600, 13)]
 
 
 def ceil4(n):
