@@ -1006,6 +1006,13 @@ TcPlan cluster_plan(int64_t m_rows, int64_t n_grid, int64_t kt, int min_bn,
 
 // Fused weight gradient: m = N (MN-major gZ), n = K, k = M.
 TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
+  // DLRM_WGRAD_PLAN="bn,splits": measurement override
+  if (const char* e = getenv("DLRM_WGRAD_PLAN")) {
+    int bn = 0, sp = 0;
+    if (sscanf(e, "%d,%d", &bn, &sp) == 2 && (bn == 32 || bn == 64 || bn == 128) && sp >= 1 &&
+        sp <= kMaxSplit)
+      return TcPlan{bn, sp};
+  }
   return cluster_plan<true, true>(N, K, ceil_div(M, BK), 32);
 }
 
