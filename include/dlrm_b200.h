@@ -204,6 +204,23 @@ int dlrm_linear_bwd_data(const float* gZ, int64_t ldg, const float* W,
                          float* dX, int64_t ldx, int64_t M, int64_t N,
                          int64_t K, dlrm_stream_t stream);
 
+/* The same two GEMMs with the weights' TF32 low parts precomputed:
+ * W_lo = dlrm_tf32_split_lo(W) in W's layout (the engine refreshes it once
+ * per step for all layers).  The tensor-core kernels then load B_lo by TMA
+ * instead of converting it per output tile; results are bitwise those of
+ * dlrm_linear_fwd / dlrm_linear_bwd_data.  W_lo = NULL: the plain calls. */
+int dlrm_linear_fwd_wlo(const float* X, int64_t ldx, const float* W,
+                        const float* W_lo, int64_t ldw, const float* b, float* Y,
+                        int64_t ldy, int64_t M, int64_t N, int64_t K,
+                        int64_t pad_n, int32_t act, dlrm_stream_t stream);
+int dlrm_linear_bwd_data_wlo(const float* gZ, int64_t ldg, const float* W,
+                             const float* W_lo, int64_t ldw, const float* mask,
+                             int64_t ldm, float* dX, int64_t ldx, int64_t M,
+                             int64_t N, int64_t K, dlrm_stream_t stream);
+/* lo[i] = tf32(x[i] - x[i] with its low 13 mantissa bits cleared), n a
+ * multiple of 4, 16-byte aligned buffers. */
+int dlrm_tf32_split_lo(const float* x, float* lo, int64_t n, dlrm_stream_t stream);
+
 size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N, int64_t K);
 
 /* dW = gZ^T X (N x K), db = column sums of gZ (ref mlp_backward,

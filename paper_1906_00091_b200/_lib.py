@@ -74,6 +74,11 @@ _SIGS = {
                         _i64, _i64, _i32, _vp],
     "dlrm_linear_bwd_data": [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                              _i64, _i64, _i64, _vp],
+    "dlrm_linear_fwd_wlo": [_vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _i64,
+                            _i64, _i64, _i32, _vp],
+    "dlrm_linear_bwd_data_wlo": [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
+                                 _i64, _i64, _i64, _vp],
+    "dlrm_tf32_split_lo": [_vp, _vp, _i64, _vp],
     "dlrm_linear_bwd_weight": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp,
                                _i64, _vp, _vp, _i64, _vp, _f32, _vp, _vp,
                                _sz, _vp],

@@ -95,6 +95,8 @@ struct TcArgs {
   GemmEpilogue ep;
   int a3d, b3d;  // MN-major operand described as a 3D tensor: one TMA box per tile
   WgradFuse wf;
+  int blo;  // 1: B_lo comes from memory (third tensor map, same geometry as B) instead of
+            // being converted from B_hi by the splitter warps
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -104,6 +106,23 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
       : "memory");
+}
+
+// B tile of one k-block (BN columns at n0, BK k-rows at k0) into dst
+template <bool B_MN, int BN>
+__device__ __forceinline__ void load_b_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                            bool b3d, int64_t n0, int k0) {
+  if (B_MN && b3d) {
+    tma_load_3d(dst, map, bar, 0, k0, int(n0 / 32));
+  } else if (B_MN) {
+#pragma unroll
+    for (int c = 0; c < BN / 32; ++c)
+      tma_load_2d(dst + c * 32 * BK * 4, map, bar, int(n0 + 32 * c), k0);
+    if (BN % 32)  // BN == 16: a single 16-wide box
+      tma_load_2d(dst, map, bar, int(n0), k0);
+  } else {
+    tma_load_2d(dst, map, bar, k0, int(n0));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -226,7 +245,7 @@ __device__ __forceinline__ void wgrad_cluster_reduce(const TcArgs& args, const u
 template <bool A_MN, bool B_MN, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               TcArgs args) {
+               const __grid_constant__ CUtensorMap tmBl, TcArgs args) {
   constexpr bool FUSE = BN >= 32;            // BN = 16 (MN-major 64-byte boxes): 3 MMAs
   constexpr uint32_t A_BYTES = BM * BK * 4;  // 16 KB
   constexpr uint32_t B_BYTES = BN * BK * 4;
@@ -310,7 +329,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (it >= TSTAGES) mbar_wait(&empty_t[s], ((it / TSTAGES) - 1) & 1);
         uint8_t* st = ring + s * STAGE_BYTES;
         const int k0 = (kt0 + it) * BK;
-        mbar_expect_tx(&full[s], TMA_BYTES);
+        mbar_expect_tx(&full[s], TMA_BYTES + (args.blo ? B_BYTES : 0u));
         if (A_MN && args.a3d) {
           tma_load_3d(st, &tmA, &full[s], 0, k0, int(m0 / 32));
         } else if (A_MN) {
@@ -320,18 +339,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         } else {
           tma_load_2d(st, &tmA, &full[s], k0, int(m0));
         }
-        uint8_t* sb = st + A_BYTES;
-        if (B_MN && args.b3d) {
-          tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
-        } else if (B_MN) {
-#pragma unroll
-          for (int c = 0; c < BN / 32; ++c)
-            tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
-          if (BN % 32)  // BN == 16: a single 16-wide box
-            tma_load_2d(sb, &tmB, &full[s], int(n0), k0);
-        } else {
-          tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
-        }
+        load_b_tile<B_MN, BN>(st + A_BYTES, &tmB, &full[s], args.b3d, n0, k0);
+        if (args.blo) load_b_tile<B_MN, BN>(st + A_BYTES + B_BYTES, &tmBl, &full[s], args.b3d, n0, k0);
       }
     }
   } else if (warp == 1) {
@@ -427,7 +436,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int i = ct + NSPLIT * j;
-        if (B_F4 % NSPLIT == 0 || i < B_F4) {
+        if (!args.blo && (B_F4 % NSPLIT == 0 || i < B_F4)) {
           const float4 v = src_b[i];
           dst_b[i] = make_float4(__uint_as_float(lo_bits(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u))),
                                  __uint_as_float(lo_bits(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u))),
@@ -524,7 +533,8 @@ constexpr int P_THREADS = THREADS + 32 * P_EPI_WARPS;
 template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(P_THREADS, 1)
 tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, TcArgs args, int64_t n_tiles,
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmBl, TcArgs args, int64_t n_tiles,
                           int64_t tiles) {
   constexpr int BN = 128;
   constexpr uint32_t A_BYTES = BM * BK * 4;
@@ -594,7 +604,7 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
           if (g >= TSTAGES) mbar_wait(&empty_t[s], ((g / TSTAGES) - 1) & 1);
           uint8_t* st = ring + s * STAGE_BYTES;
           const int k0 = it * BK;
-          mbar_expect_tx(&full[s], TMA_BYTES);
+          mbar_expect_tx(&full[s], TMA_BYTES + (args.blo ? B_BYTES : 0u));
           if (A_MN && args.a3d) {
             tma_load_3d(st, &tmA, &full[s], 0, k0, int(m0 / 32));
           } else if (A_MN) {
@@ -604,16 +614,9 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
           } else {
             tma_load_2d(st, &tmA, &full[s], k0, int(m0));
           }
-          uint8_t* sb = st + A_BYTES;
-          if (B_MN && args.b3d) {
-            tma_load_3d(sb, &tmB, &full[s], 0, k0, int(n0 / 32));
-          } else if (B_MN) {
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              tma_load_2d(sb + c * 32 * BK * 4, &tmB, &full[s], int(n0 + 32 * c), k0);
-          } else {
-            tma_load_2d(sb, &tmB, &full[s], k0, int(n0));
-          }
+          load_b_tile<B_MN, BN>(st + A_BYTES, &tmB, &full[s], args.b3d, n0, k0);
+          if (args.blo)
+            load_b_tile<B_MN, BN>(st + A_BYTES + B_BYTES, &tmBl, &full[s], args.b3d, n0, k0);
         }
       }
     }
@@ -696,7 +699,7 @@ tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA,
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
           const int i = ct + NSPLIT * j;
-          if (B_F4 % NSPLIT == 0 || i < B_F4) {
+          if (!args.blo && (B_F4 % NSPLIT == 0 || i < B_F4)) {
             const float4 v = src_b[i];
             dst_b[i] = make_float4(__uint_as_float(lo_bits(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u))),
                                    __uint_as_float(lo_bits(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u))),
@@ -819,8 +822,8 @@ constexpr size_t smem_bytes(int bn) {
 }
 
 template <bool A_MN, bool B_MN, int BN>
-int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
-              int splits, cudaStream_t s) {
+int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& bl,
+              const TcArgs& args, int64_t n_grid, int splits, cudaStream_t s) {
   auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
   const size_t sm = smem_bytes(BN);
   static bool configured = false;
@@ -843,12 +846,12 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
       DLRM_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psm)));
       pconf = true;
     }
-    launch(kp, unsigned(tiles < kNumSMs ? tiles : kNumSMs), P_THREADS, psm, s, a, b, args,
+    launch(kp, unsigned(tiles < kNumSMs ? tiles : kNumSMs), P_THREADS, psm, s, a, b, bl, args,
            int64_t(grid.x), tiles);
     return check_launch("tc_gemm_persistent_kernel");
   }
   if (!args.wf.on) {
-    launch(k, grid, THREADS, sm, s, a, b, args);
+    launch(k, grid, THREADS, sm, s, a, b, bl, args);
     return check_launch("tc_gemm_kernel");
   }
   // fused weight gradient: the split-K CTAs of a tile are one cluster
@@ -871,7 +874,7 @@ int launch_bn(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, in
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k, a, b, args);
+  cudaLaunchKernelEx(&cfg, k, a, b, bl, args);
   return check_launch("tc_gemm_kernel(cluster)");
 }
 
@@ -918,13 +921,13 @@ struct TcPlan {
 };
 
 template <bool A_MN, bool B_MN>
-int launch(const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args, int64_t n_grid,
-           int bn, int splits, cudaStream_t s) {
+int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& bl, const TcArgs& args,
+           int64_t n_grid, int bn, int splits, cudaStream_t s) {
   switch (bn) {
-    case 16: return launch_bn<A_MN, B_MN, 16>(a, b, args, n_grid, splits, s);
-    case 32: return launch_bn<A_MN, B_MN, 32>(a, b, args, n_grid, splits, s);
-    case 64: return launch_bn<A_MN, B_MN, 64>(a, b, args, n_grid, splits, s);
-    default: return launch_bn<A_MN, B_MN, 128>(a, b, args, n_grid, splits, s);
+    case 16: return launch_bn<A_MN, B_MN, 16>(a, b, bl, args, n_grid, splits, s);
+    case 32: return launch_bn<A_MN, B_MN, 32>(a, b, bl, args, n_grid, splits, s);
+    case 64: return launch_bn<A_MN, B_MN, 64>(a, b, bl, args, n_grid, splits, s);
+    default: return launch_bn<A_MN, B_MN, 128>(a, b, bl, args, n_grid, splits, s);
   }
 }
 
@@ -1016,7 +1019,37 @@ TcPlan weight_plan(int64_t M, int64_t N, int64_t K) {
   return cluster_plan<true, true>(N, K, ceil_div(M, BK), 32);
 }
 
+__global__ void __launch_bounds__(256) split_lo_kernel(const float4* __restrict__ x,
+                                                       float4* __restrict__ lo, int64_t n4) {
+  pdl_entry();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    lo[i] = make_float4(__uint_as_float(lo_bits(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u))),
+                        __uint_as_float(lo_bits(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u))),
+                        __uint_as_float(lo_bits(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u))),
+                        __uint_as_float(lo_bits(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u))));
+  }
+}
+
 }  // namespace
+
+// DLRM_GEMM_BLO=0: the splitter converts B_lo per tile even when W_lo is given
+bool blo_enabled() {
+  static const bool on = !getenv("DLRM_GEMM_BLO") || atoi(getenv("DLRM_GEMM_BLO")) != 0;
+  return on;
+}
+
+int tc_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s) {
+  DLRM_REQUIRE(n % 4 == 0 && aligned16(x) && aligned16(lo), "split_lo needs float4 rows");
+  const int64_t n4 = n / 4;
+  int64_t blocks = ceil_div(n4, 256);
+  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+  if (blocks < 1) return 0;
+  launch(split_lo_kernel, unsigned(blocks), 256, 0, s, reinterpret_cast<const float4*>(x),
+         reinterpret_cast<float4*>(lo), n4);
+  return check_launch("split_lo_kernel");
+}
 
 bool tc_enabled() { return g_tc_mode != 1; }
 int tc_mode() { return g_tc_mode; }
@@ -1051,7 +1084,7 @@ bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw, 
 
 int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, const float* b,
                   float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K, int64_t n_grid,
-                  int act, cudaStream_t s) {
+                  int act, cudaStream_t s, const float* W_lo) {
   // split-K over a thread-block cluster when the tile grid alone cannot
   // fill the SMs (bias / ReLU applied after the DSMEM reduction)
   const TcPlan pl = cluster_plan<false, false>(M, n_grid, ceil_div(K, BK), 16, true);
@@ -1067,7 +1100,12 @@ int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw, cons
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
   if (used > 1) a.wf = cluster_epilogue();
-  return launch<false, false>(ma, mb, a, n_grid, bn, used, s);
+  CUtensorMap ml = mb;
+  if (W_lo && blo_enabled() && bn >= 32) {
+    DLRM_REQUIRE(map_operand(&ml, W_lo, false, N, K, ldw, bn), "tensor map encoding failed (W_lo)");
+    a.blo = 1;
+  }
+  return launch<false, false>(ma, mb, ml, a, n_grid, bn, used, s);
 }
 
 bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
@@ -1080,7 +1118,7 @@ bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W, int64_t
 
 int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw,
                        const float* mask, int64_t ldm, float* dX, int64_t ldx, int64_t M,
-                       int64_t N, int64_t K, cudaStream_t s) {
+                       int64_t N, int64_t K, cudaStream_t s, const float* W_lo) {
   // dX (M x K) = gZ (M x N) W (N x K): GEMM n = K (MN-major in W), k = N
   const TcPlan pl = cluster_plan<false, true>(M, K, ceil_div(N, BK), 32, true);
   const int bn = pl.bn;
@@ -1096,7 +1134,12 @@ int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W, int64_t ldw
   a.k_tiles_per_split = int(ceil_div(a.k_tiles, pl.splits));
   const int used = int(ceil_div(a.k_tiles, a.k_tiles_per_split));
   if (used > 1) a.wf = cluster_epilogue();
-  return launch<false, true>(ma, mb, a, K, bn, used, s);
+  CUtensorMap ml = mb;
+  if (W_lo && blo_enabled() && bn >= 32) {
+    DLRM_REQUIRE(map_operand(&ml, W_lo, true, K, N, ldw, bn), "tensor map encoding failed (W_lo)");
+    a.blo = 1;
+  }
+  return launch<false, true>(ma, mb, ml, a, K, bn, used, s);
 }
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X, int64_t ldx,
@@ -1131,7 +1174,7 @@ int tc_linear_bwd_weight(const float* gZ, int64_t ldg, const float* X, int64_t l
   a.wf = WgradFuse{1, (db || b_upd) ? 1 : 0, dW, lddw, W_upd, ldw, db, b_upd, u, err_flag,
                    vec ? 1 : 0};
 
-  return launch<true, true>(ma, mb, a, K, bn, used, s);
+  return launch<true, true>(ma, mb, mb, a, K, bn, used, s);
 }
 
 }  // namespace dlrm

@@ -24,9 +24,12 @@ bool tma_encode_2d(CUtensorMap* map, const float* base, int64_t inner, int64_t o
 bool tc_linear_fwd_ok(const float* X, int64_t ldx, const float* W, int64_t ldw,
                       const float* Y, int64_t ldy, int64_t M, int64_t N,
                       int64_t K, int64_t n_grid);
+// W_lo (optional): lo_tf32(W - hi(W)) in W's layout (dlrm_tf32_split_lo),
+// loaded by TMA instead of being converted per tile
 int tc_linear_fwd(const float* X, int64_t ldx, const float* W, int64_t ldw,
                   const float* b, float* Y, int64_t ldy, int64_t M, int64_t N,
-                  int64_t K, int64_t n_grid, int act, cudaStream_t s);
+                  int64_t K, int64_t n_grid, int act, cudaStream_t s,
+                  const float* W_lo = nullptr);
 
 bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W,
                            int64_t ldw, const float* dX, int64_t ldx, int64_t M,
@@ -34,7 +37,11 @@ bool tc_linear_bwd_data_ok(const float* gZ, int64_t ldg, const float* W,
 int tc_linear_bwd_data(const float* gZ, int64_t ldg, const float* W,
                        int64_t ldw, const float* mask, int64_t ldm, float* dX,
                        int64_t ldx, int64_t M, int64_t N, int64_t K,
-                       cudaStream_t s);
+                       cudaStream_t s, const float* W_lo = nullptr);
+// lo[i] = lo_tf32(x[i] - hi(x[i])): the B_lo operand the GEMM splitter would
+// make, for weights reused by many GEMM tiles
+int tc_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s);
+bool blo_enabled();
 
 bool tc_linear_bwd_weight_ok(const float* gZ, int64_t ldg, const float* X,
                              int64_t ldx, int64_t M, int64_t N, int64_t K);

@@ -449,11 +449,11 @@ linear_n1_kernel(const float* __restrict__ X, int64_t ldx, const float* __restri
 }  // namespace
 }  // namespace dlrm
 
-extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
-                               int64_t ldw, const float* b, float* Y,
-                               int64_t ldy, int64_t M, int64_t N, int64_t K,
-                               int64_t pad_n, int32_t act,
-                               dlrm_stream_t stream) {
+namespace dlrm {
+namespace {
+int linear_fwd(const float* X, int64_t ldx, const float* W, const float* W_lo, int64_t ldw,
+               const float* b, float* Y, int64_t ldy, int64_t M, int64_t N, int64_t K,
+               int64_t pad_n, int32_t act, dlrm_stream_t stream) {
   DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldx >= K && ldw >= K && ldy >= N,
                "bad linear_fwd shape");
   DLRM_REQUIRE(act == DLRM_ACT_IDENTITY || act == DLRM_ACT_RELU, "bad activation");
@@ -471,9 +471,53 @@ extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
       (reinterpret_cast<uintptr_t>(Y) % 16) == 0 && skinny_v_enabled())
     return skinny_fwd(X, ldx, W, ldw, b, Y, ldy, M, N, K, ng, act, s);
   if (tc_linear_fwd_ok(X, ldx, W, ldw, Y, ldy, M, N, K, ng))
-    return tc_linear_fwd(X, ldx, W, ldw, b, Y, ldy, M, N, K, ng, act, s);
+    return tc_linear_fwd(X, ldx, W, ldw, b, Y, ldy, M, N, K, ng, act, s, W_lo);
   GemmEpilogue ep{EPI_BIAS_ACT, act, Y, ldy, b, nullptr, 0, ng, M};
   return gemm_simt(X, ldx, 1, W, ldw, 1, M, N, K, 1, ep, ng, s);
+}
+
+int linear_bwd_data(const float* gZ, int64_t ldg, const float* W, const float* W_lo,
+                    int64_t ldw, const float* mask, int64_t ldm, float* dX, int64_t ldx,
+                    int64_t M, int64_t N, int64_t K, dlrm_stream_t stream) {
+  DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldw >= K && ldx >= K,
+               "bad linear_bwd_data shape");
+  if (M == 0) return 0;
+  cudaStream_t s = as_stream(stream);
+  if (tc_linear_bwd_data_ok(gZ, ldg, W, ldw, dX, ldx, M, N, K))
+    return tc_linear_bwd_data(gZ, ldg, W, ldw, mask, ldm, dX, ldx, M, N, K, s, W_lo);
+  GemmEpilogue ep{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M};
+  // dX(M x K) = gZ(M x N) W(N x K): A(m,k') = gZ[m*ldg+k'], B(k',n') = W[k'*ldw+n']
+  return gemm_simt(gZ, ldg, 1, W, 1, ldw, M, K, N, 1, ep, K, s);
+}
+}  // namespace
+}  // namespace dlrm
+
+extern "C" int dlrm_linear_fwd(const float* X, int64_t ldx, const float* W,
+                               int64_t ldw, const float* b, float* Y,
+                               int64_t ldy, int64_t M, int64_t N, int64_t K,
+                               int64_t pad_n, int32_t act,
+                               dlrm_stream_t stream) {
+  return dlrm::linear_fwd(X, ldx, W, nullptr, ldw, b, Y, ldy, M, N, K, pad_n, act, stream);
+}
+
+extern "C" int dlrm_linear_fwd_wlo(const float* X, int64_t ldx, const float* W,
+                                   const float* W_lo, int64_t ldw, const float* b, float* Y,
+                                   int64_t ldy, int64_t M, int64_t N, int64_t K,
+                                   int64_t pad_n, int32_t act, dlrm_stream_t stream) {
+  return dlrm::linear_fwd(X, ldx, W, W_lo, ldw, b, Y, ldy, M, N, K, pad_n, act, stream);
+}
+
+extern "C" int dlrm_linear_bwd_data_wlo(const float* gZ, int64_t ldg, const float* W,
+                                        const float* W_lo, int64_t ldw, const float* mask,
+                                        int64_t ldm, float* dX, int64_t ldx, int64_t M,
+                                        int64_t N, int64_t K, dlrm_stream_t stream) {
+  return dlrm::linear_bwd_data(gZ, ldg, W, W_lo, ldw, mask, ldm, dX, ldx, M, N, K, stream);
+}
+
+extern "C" int dlrm_tf32_split_lo(const float* x, float* lo, int64_t n,
+                                  dlrm_stream_t stream) {
+  DLRM_REQUIRE(n >= 0, "bad split_lo size");
+  return dlrm::tc_split_lo(x, lo, n, dlrm::as_stream(stream));
 }
 
 extern "C" int dlrm_linear_bwd_data(const float* gZ, int64_t ldg,
@@ -481,15 +525,7 @@ extern "C" int dlrm_linear_bwd_data(const float* gZ, int64_t ldg,
                                     const float* mask, int64_t ldm, float* dX,
                                     int64_t ldx, int64_t M, int64_t N,
                                     int64_t K, dlrm_stream_t stream) {
-  DLRM_REQUIRE(M >= 0 && N >= 1 && K >= 1 && ldg >= N && ldw >= K && ldx >= K,
-               "bad linear_bwd_data shape");
-  if (M == 0) return 0;
-  cudaStream_t s = as_stream(stream);
-  if (tc_linear_bwd_data_ok(gZ, ldg, W, ldw, dX, ldx, M, N, K))
-    return tc_linear_bwd_data(gZ, ldg, W, ldw, mask, ldm, dX, ldx, M, N, K, s);
-  GemmEpilogue ep{EPI_MASK, 0, dX, ldx, nullptr, mask, ldm, K, M};
-  // dX(M x K) = gZ(M x N) W(N x K): A(m,k') = gZ[m*ldg+k'], B(k',n') = W[k'*ldw+n']
-  return gemm_simt(gZ, ldg, 1, W, 1, ldw, M, K, N, 1, ep, K, s);
+  return dlrm::linear_bwd_data(gZ, ldg, W, nullptr, ldw, mask, ldm, dX, ldx, M, N, K, stream);
 }
 
 extern "C" size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N,

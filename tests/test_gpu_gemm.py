@@ -145,3 +145,38 @@ def test_gemm_is_deterministic(M, N, K):
     assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
     ref = X[:, :K].double() @ W[:, :K].double().T + b.double()
     assert maxnorm_err(ys[0][:, :N].cpu(), ref.cpu()) < TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 1024, 1024), (2048, 64, 512), (4096, 1000, 300),
+                                   (300, 16, 64), (33, 30, 64), (20000, 640, 480)])
+def test_precomputed_weight_lo_parts_are_bitwise_neutral(M, N, K):
+    """dlrm_linear_fwd_wlo / dlrm_linear_bwd_data_wlo with W_lo from
+    dlrm_tf32_split_lo (B_lo loaded by TMA, not converted per tile) give
+    bitwise the results of the plain calls, on every kernel the shapes pick
+    (one-tile, persistent, split-K cluster, narrow BN that ignores W_lo)."""
+    P = _lib.ptr
+    X = torch.zeros((M, ceil4(K)), device="cuda")
+    X[:, :K] = rand((M, K), 21)
+    W = torch.zeros((N, ceil4(K)), device="cuda")
+    W[:, :K] = rand((N, K), 22, K ** -0.5)
+    Wl = torch.full_like(W, float("nan"))
+    _lib.call("dlrm_tf32_split_lo", P(W), P(Wl), W.numel(), _lib.stream_handle())
+    b = rand((N,), 23)
+    Y1 = linear_fwd(X, W, b, N, K, 1)
+    Y2 = torch.full((M, ceil4(N)), float("nan"), device="cuda")
+    _lib.call("dlrm_linear_fwd_wlo", P(X), X.stride(0), P(W), P(Wl), W.stride(0), P(b), P(Y2),
+              Y2.stride(0), M, N, K, Y2.shape[1], 1, _lib.stream_handle())
+    assert torch.equal(Y1, Y2)
+    gZ = torch.zeros((M, ceil4(N)), device="cuda")
+    gZ[:, :N] = rand((M, N), 24)
+    mask = torch.relu(rand((M, ceil4(K)), 25))
+    outs = []
+    for fn, extra in (("dlrm_linear_bwd_data", ()), ("dlrm_linear_bwd_data_wlo", (P(Wl),))):
+        dX = torch.full((M, ceil4(K)), float("nan"), device="cuda")
+        _lib.call(fn, P(gZ), gZ.stride(0), P(W), *extra, W.stride(0), P(mask), mask.stride(0),
+                  P(dX), dX.stride(0), M, N, K, _lib.stream_handle())
+        outs.append(dX[:, :K])
+    assert torch.equal(outs[0], outs[1])
+    # the low parts themselves: x - hi(x), rounded to TF32, zero where x is
+    hi = (W.view(torch.int32) & -8192).view(torch.float32)
+    assert torch.all((Wl == 0) | ((W - hi) != 0))
