@@ -291,7 +291,17 @@ class RankEngine:
             self.upd_mlp = self.upd_emb = update_rule("sgd", self.lr)
         else:
             raise ValueError(f"unknown optimizer: {optimizer!r}")
+        # weights' TF32 low parts for the tensor-core GEMMs, refreshed at the
+        # start of every step (as trainer.StepEngine)
+        self.use_wlo = not self.accurate and os.environ.get("DLRM_GEMM_WLO", "1") != "0"
+        self.params_lo = torch.zeros_like(self.params) if self.use_wlo else None
         self._build_descs()
+
+    def _wlo(self, l):
+        if not self.use_wlo:
+            return None
+        return C.c_void_p(self.params_lo.data_ptr() +
+                          (l.storage.data_ptr() - self.params.data_ptr()))
 
     def _build_descs(self):
         d, L = self.d, self.L
@@ -407,6 +417,8 @@ class RankEngine:
         s = _lib.stream_handle(stream)
         P, call, L = _lib.ptr, _lib.call, self.layers
         Bl, relu = self.Bl, _lib.ACT["relu"]
+        if self.use_wlo:  # ordered before the top MLP by the trainer's events
+            call("dlrm_tf32_split_lo", P(self.params), P(self.params_lo), self.params.numel(), s)
         a, lda = self.x, self.x.stride(0)
         for i in range(self.Lb):
             l, out = L[i], self.bact[i]
@@ -427,8 +439,8 @@ class RankEngine:
         a, lda = self.R, self.R.stride(0)
         for i in range(self.Lt - 1):
             l, out = L[self.Lb + i], self.tact[i]
-            call("dlrm_linear_fwd", P(a), lda, P(l.storage), l.ldw, P(l.bias),
-                 P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
+            call("dlrm_linear_fwd_wlo", P(a), lda, P(l.storage), self._wlo(l), l.ldw,
+                 P(l.bias), P(out), out.stride(0), Bl, l.n_out, l.n_in, out.shape[1], relu, s)
             a, lda = out, out.stride(0)
         head = L[-1]
         if self.head_fused:
@@ -508,8 +520,8 @@ class RankEngine:
             xin = self.R if i == 0 else self.tact[i - 1]
             dx = self.gR if i == 0 else self.gtop[i - 1]
             mask = None if i == 0 else self.tact[i - 1]
-            call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage), l.ldw,
-                 P(mask), mask.stride(0) if mask is not None else 0, P(dx),
+            call("dlrm_linear_bwd_data_wlo", P(gz), gz.stride(0), P(l.storage), self._wlo(l),
+                 l.ldw, P(mask), mask.stride(0) if mask is not None else 0, P(dx),
                  dx.stride(0), Bl, l.n_out, l.n_in, s)
             self._wgrad(stream, wgrad_stream, li, gz, gz.stride(0), xin)
 
@@ -530,9 +542,9 @@ class RankEngine:
             xin = self.x if i == 0 else self.bact[i - 1]
             if i > 0:
                 dx = self.gbot[i - 1]
-                call("dlrm_linear_bwd_data", P(gz), gz.stride(0), P(l.storage),
-                     l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0), P(dx),
-                     dx.stride(0), Bl, l.n_out, l.n_in, s)
+                call("dlrm_linear_bwd_data_wlo", P(gz), gz.stride(0), P(l.storage),
+                     self._wlo(l), l.ldw, P(self.bact[i - 1]), self.bact[i - 1].stride(0),
+                     P(dx), dx.stride(0), Bl, l.n_out, l.n_in, s)
             if i == 0 and wgrad_stream is not None:
                 # the first layer's weight gradient on the (then idle) calling
                 # stream, beside the weight-gradient stream (own workspace)
