@@ -716,8 +716,11 @@ class HybridTrainer:
         cur.wait_event(bot)
         e.phase_b_forward(bottom=False)
         # loss, correct count and this rank's index-error flag are known after
-        # the head; the reduced flag gates every update (on device)
-        e.publish_error()
+        # the head; the reduced flag gates every update (on device).  One
+        # rank: the flag is only reported, published off the critical path
+        # (side stream, after the apply) instead
+        if not single:
+            e.publish_error()
         if not single:
             comm.wait_event(mark(cur))
             with torch.cuda.stream(comm):
@@ -742,6 +745,9 @@ class HybridTrainer:
         side.wait_event(got)
         e.apply_sparse(side)
         e.resolve_errors(side)
+        if single:
+            with torch.cuda.stream(side):
+                e.publish_error()
         applied = mark(side)
         e.phase_b_bottom_backward(wgrad_stream=wg)
         if not single:
