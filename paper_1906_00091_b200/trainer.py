@@ -79,14 +79,37 @@ class PendingStepResult(StepResult):
     issued after it are not rolled back (each skipped only its own updates
     if its own batch was bad)."""
 
-    def __init__(self, engine: "StepEngine", slot: int, event, probs: torch.Tensor):
-        self._eng, self._slot, self._event, self.probs = engine, slot, event, probs
+    def __init__(self, engine: "StepEngine", slot: int, event):
+        self._eng, self._slot, self._event = engine, slot, event
         self._vals = None
+        self._err = None
+        self._probs = None
 
     def _materialise(self):
         if self._vals is None:
-            self._vals = self._eng._settle(self)
+            self._vals, self._err = self._eng._settle(self)
+        if self._err is not None:  # raised once, on the first read
+            err, self._err = self._err, None
+            raise err
         return self._vals
+
+    def _take_probs(self):
+        if self._probs is None:
+            # ordered after this step's copy into the ring (compute stream)
+            torch.cuda.current_stream().wait_event(self._event)
+            self._probs = self._eng._prob_ring[self._slot].clone()
+        return self._probs
+
+    def _release_slot(self):
+        """The ring slot is about to be reused: take this step's values and a
+        private copy of its probabilities first."""
+        self._take_probs()
+        if self._vals is None:  # an index error stays pending for the reader
+            self._vals, self._err = self._eng._settle(self)
+
+    @property
+    def probs(self) -> torch.Tensor:
+        return self._take_probs()
 
     @property
     def loss(self) -> float:
@@ -856,15 +879,22 @@ class StepEngine:
     RING = 8  # pinned result slots of sync=False steps
 
     def result_async(self) -> "PendingStepResult":
-        """The last step's result without a host synchronisation: loss /
-        correct sums, the error flag and the error payload are copied into a
-        pinned ring slot on the compute stream (PendingStepResult)."""
+        """The last step's result without a host synchronisation: the result
+        block (loss / correct sums, error flag and payload) is copied into a
+        pinned ring slot and the probabilities into a device ring slot, on
+        the compute stream (PendingStepResult).  (A snapshot kernel plus the
+        host copy on a separate read-back stream measured no better end to
+        end: e2e at c2 / c3 is bound by the host.)"""
         T = self.T
+        n = 4 + 4 * T
+        s = torch.cuda.current_stream()
         if getattr(self, "_ring", None) is None:
+            R = self.RING
             # per slot: [loss, correct, flag(int32), pad | err_pos[T] | err_val[T]]
-            self._ring = [torch.zeros(4 + 4 * T, dtype=torch.float32).pin_memory()
-                          for _ in range(self.RING)]
-            self._ring_owner = [None] * self.RING
+            self._ring = [torch.zeros(n, dtype=torch.float32).pin_memory() for _ in range(R)]
+            self._prob_ring = torch.zeros((R, self.B), dtype=torch.float32, device=self.dev)
+            self._ring_owner = [None] * R
+            self._ev = [torch.cuda.Event() for _ in range(R)]
             self._ring_next = 0
         k = self._ring_next
         self._ring_next = (k + 1) % self.RING
@@ -872,32 +902,29 @@ class StepEngine:
         if old is not None:
             old = old()
             if old is not None:  # an unread result still owns the slot
-                old._materialise()
-        h = self._ring[k]
-        s = torch.cuda.current_stream()
-        h.copy_(self.res_dev, non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(s)
-        res = PendingStepResult(self, k, ev, self.prob.clone())
+                old._release_slot()
+        self._ring[k].copy_(self.res_dev, non_blocking=True)
+        self._prob_ring[k].copy_(self.prob)
+        self._ev[k].record(s)
+        res = PendingStepResult(self, k, self._ev[k])
         self._ring_owner[k] = weakref.ref(res)
         return res
 
     def _settle(self, res: "PendingStepResult"):
+        """(loss, accuracy) of a pending step and its LookupIndexError (or
+        None), once its read-back landed."""
         res._event.synchronize()
         h, T = self._ring[res._slot], self.T
-        if self._ring_owner[res._slot] is not None and self._ring_owner[res._slot]() is res:
-            self._ring_owner[res._slot] = None
         vals = (float(h[0]) / self.B, float(h[1]) / self.B)
         if int(h[2:3].view(torch.int32)[0]):
-            res._vals = vals
             pos = h[4:4 + 2 * T].view(torch.int64).numpy()
             val = h[4 + 2 * T:4 + 4 * T].view(torch.int64).numpy()
             for t in range(T):
                 if pos[t] != INT64_MAX:
                     tab = self.model.tables[t]
-                    raise LookupIndexError(tab.table_id, int(pos[t]), int(val[t]),
-                                           tab.num_rows)
-        return vals
+                    return vals, LookupIndexError(tab.table_id, int(pos[t]), int(val[t]),
+                                                  tab.num_rows)
+        return vals, None
 
     def result(self) -> StepResult:
         """StepResult of the last step: the error flag and the loss / correct

@@ -217,3 +217,28 @@ def test_async_results_match_sync_and_report_their_own_error(golden):
     train_step(r, batches[2].dense, sb(batches[2]), batches[2].labels, Sgd(0.1))
     for a, b in zip(arrays(m.bottom, m.top, m.tables), arrays(r.bottom, r.top, r.tables)):
         assert np.array_equal(a, b)
+    # more pending steps than read-back ring slots, read only at the end: the
+    # reused slots hand their values, probabilities and a pending index error
+    # to the older results first
+    n = 3 * len(batches) + 13
+    ms, ma2 = build(c), build(c)
+    seq = [(batches[k % len(batches)], k == 5) for k in range(n)]
+    sync, pend = [], []
+    for hb, is_bad in seq:
+        idx = None
+        if is_bad:
+            idx = [i.copy() for i in hb.indices]
+            idx[1][0] = -3
+        try:
+            sync.append(train_step(ms, hb.dense, sb(hb, idx), hb.labels, Sgd(0.1)))
+        except LookupIndexError as err:
+            sync.append(err)
+        pend.append(train_step(ma2, hb.dense, sb(hb, idx), hb.labels, Sgd(0.1), sync=False))
+    for x, y in zip(sync, pend):
+        if isinstance(x, LookupIndexError):
+            with pytest.raises(LookupIndexError) as e:
+                _ = y.loss
+            assert (e.value.table_id, e.value.position, e.value.index) == \
+                (x.table_id, x.position, x.index)
+            continue
+        assert x.loss == y.loss and x.accuracy == y.accuracy and torch.equal(x.probs, y.probs)
