@@ -1246,7 +1246,10 @@ int launch_stream(const float* W, int64_t dim, const TableSet& ts, int64_t nb, f
     DLRM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  launch(kern, kNumSMs, 32 * WARPS, smem, s, W, dim, ts, nb, out, stride, ep, ef);
+  // DLRM_EMB_FWD_CTAS: measurement override of the persistent grid
+  static const int ctas = getenv("DLRM_EMB_FWD_CTAS") ? atoi(getenv("DLRM_EMB_FWD_CTAS")) : kNumSMs;
+  launch(kern, unsigned(ctas > 0 && ctas <= kNumSMs ? ctas : kNumSMs), 32 * WARPS, smem, s, W,
+         dim, ts, nb, out, stride, ep, ef);
   return check_launch("emb_fwd_stream_kernel");
 }
 
