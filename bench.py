@@ -572,7 +572,8 @@ def e2e_train_step(model, cfg, hbs, B, K, warmup, dist, dev):
     # c3 batch packs in 0.32 ms on 4 threads, scripts/pack_bench.py; two
     # batches in flight keep the input ahead of the 0.4 ms step)
     pf = Prefetcher(source(), B, T, cfg.dense_dim, capacities=caps, depth=4,
-                    threads=min(4, max(1, (os.cpu_count() or 2) // 4)), workers=2)
+                    threads=int(os.environ.get("DLRM_PF_THREADS", min(4, max(1, (os.cpu_count() or 2) // 4)))),
+                    workers=int(os.environ.get("DLRM_PF_WORKERS", 2)))
     it = iter(pf)
     opt = Sgd(0.1)
     for _ in range(warmup + 2):   # eager step, graph capture, warm-up
