@@ -118,9 +118,33 @@ __device__ unsigned long long g_ia_prof[24];
 // (j ^ (r & 7))).  TMEM: D buffers [0, 64) / [64, 128), A slots from 128.
 // Roles: warps 0-3 epilogue, 4-7 splitters (TMEM lane quarters), 8 MMA
 // issuer, 9 loader (TMA, or cp.async for non-uniform feature pointers).
+// Role profile at c4 (DLRM_IF_PROF, scripts/if_prof.py): splitters busy 94 %
+// and epilogue 86 % of the kernel; eight splitter warps (two per lane
+// quarter, half the columns each) cut the MMA's wait for them from 72k to
+// 12k cycles per CTA but left the epilogue at 95 % busy and the kernel no
+// faster (179 vs 172 us), so four stay.
 constexpr int IF_WARPS = 10;
 constexpr int IF_THREADS = 32 * IF_WARPS;
 
+#ifdef DLRM_IF_PROF
+__device__ unsigned long long g_if_prof[16];
+#define IF_WAIT(bar, par, k)                                  \
+  do {                                                        \
+    const long long t0_ = clock64();                          \
+    mbar_wait(bar, par);                                      \
+    ifp[k] += (unsigned long long)(clock64() - t0_);          \
+  } while (0)
+#define IF_FLUSH(k)                                                          \
+  do {                                                                       \
+    ifp[k] += (unsigned long long)(clock64() - ift0);                        \
+    if (lane == 0)                                                           \
+      for (int i_ = 0; i_ < 16; ++i_)                                        \
+        if (ifp[i_]) atomicAdd(&g_if_prof[i_], ifp[i_]);                     \
+  } while (0)
+#else
+#define IF_WAIT(bar, par, k) mbar_wait(bar, par)
+#define IF_FLUSH(k)
+#endif
 __global__ void __launch_bounds__(IF_THREADS, 1)
 interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, IaGeom g,
                        int64_t batch, float* __restrict__ out, int64_t ld_out, int64_t pad_to) {
@@ -170,6 +194,10 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();
+#ifdef DLRM_IF_PROF
+  unsigned long long ifp[16] = {0};
+  const long long ift0 = clock64();
+#endif
   auto piece = [&](uint8_t* base, int r, int p) {  // 16-byte piece p (4 floats) of row r
     return base + size_t(p >> 3) * Rp * 128 + r * 128 + (((p & 7) ^ (r & 7)) << 4);
   };
@@ -179,7 +207,7 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int st = it % g.nst;
-      if (it >= g.nst) mbar_wait(&empty[st], ((it / g.nst) - 1) & 1);
+      if (it >= g.nst) IF_WAIT(&empty[st], ((it / g.nst) - 1) & 1, 0);
       uint8_t* base = stages + size_t(st) * g.stage_bytes;
       const int64_t b0 = tile * S;
       if (g.tma) {
@@ -212,8 +240,8 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
       const int st = it % g.nst, ab = it & 1;
       const int64_t b0 = tile * S;
       const int ns = int(batch - b0 < S ? batch - b0 : S);
-      mbar_wait(&land[st], (it / g.nst) & 1);
-      if (it >= 2) mbar_wait(&aempty[ab], ((it - 2) >> 1) & 1);
+      IF_WAIT(&land[st], (it / g.nst) & 1, 2);
+      if (it >= 2) IF_WAIT(&aempty[ab], ((it - 2) >> 1) & 1, 3);
       tc_fence_after();
       uint8_t* base = stages + size_t(st) * g.stage_bytes;
       const uint32_t slot = tmem + lane_off + 128u + uint32_t(ab * d);
@@ -252,9 +280,9 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it % g.nst, ab = it & 1;
-        mbar_wait(&land[st], (it / g.nst) & 1);
-        mbar_wait(&afull[ab], (it >> 1) & 1);
-        if (it >= 2) mbar_wait(&tempty[ab], ((it - 2) >> 1) & 1);
+        IF_WAIT(&land[st], (it / g.nst) & 1, 5);
+        IF_WAIT(&afull[ab], (it >> 1) & 1, 6);
+        if (it >= 2) IF_WAIT(&tempty[ab], ((it - 2) >> 1) & 1, 7);
         tc_fence_after();
         const uint32_t dt = tmem + uint32_t(64 * ab);
         const uint32_t a = tmem + 128u + uint32_t(ab * d);
@@ -289,17 +317,25 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
       const int ab = it & 1;
       const int64_t b0 = tile * S;
       const int ns = int(batch - b0 < S ? batch - b0 : S);
-      mbar_wait(&tfull[ab], (it >> 1) & 1);
+      IF_WAIT(&tfull[ab], (it >> 1) & 1, 9);
       tc_fence_after();
       const bool valid = i >= 0 && i / nf < ns;
-      for (int c0 = lo_c & ~15; c0 < hi_c; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16_issue(tmem + lane_off + uint32_t(64 * ab + c0), v);
-        tmem_wait_ld();
+      // the window's column chunks (at most 4 of 16: Rp <= 64) loaded with
+      // one wait instead of a load-wait round trip per chunk
+      const int cb = lo_c & ~15;
+      const int nch = (hi_c - cb + 15) >> 4;
+      uint32_t v[4][16];
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        if (ch < nch) tmem_ld16_issue(tmem + lane_off + uint32_t(64 * ab + cb + 16 * ch), v[ch]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        if (ch >= nch) break;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const int j = c0 + k;
-          if (valid && j >= blk && j < blk + nf) dst[i * nf + (j - blk)] = __uint_as_float(v[k]);
+          const int j = cb + 16 * ch + k;
+          if (valid && j >= blk && j < blk + nf) dst[i * nf + (j - blk)] = __uint_as_float(v[ch][k]);
         }
       }
       tc_fence_before();
@@ -318,6 +354,12 @@ interact_tc_fwd_kernel(const __grid_constant__ CUtensorMap tmZ, FeatureSet fs, I
       named_bar(2, IA_EPI);
     }
   }
+#ifdef DLRM_IF_PROF
+  if (warp == 9) IF_FLUSH(1);
+  else if (warp == 4) IF_FLUSH(4);
+  else if (warp == 8) IF_FLUSH(8);
+  else if (warp == 0) { if (lane == 0) ifp[11] = 1; IF_FLUSH(10); }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 8) {
@@ -829,6 +871,15 @@ extern "C" int dlrm_ia_prof(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, dlrm::g_ia_prof, sizeof(unsigned long long) * 24);
   static const unsigned long long zero[24] = {0};
   cudaMemcpyToSymbol(dlrm::g_ia_prof, zero, sizeof(zero));
+  return 0;
+}
+#endif
+
+#ifdef DLRM_IF_PROF
+extern "C" int dlrm_if_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, dlrm::g_if_prof, sizeof(unsigned long long) * 16);
+  static const unsigned long long zero[16] = {0};
+  cudaMemcpyToSymbol(dlrm::g_if_prof, zero, sizeof(zero));
   return 0;
 }
 #endif
