@@ -122,7 +122,8 @@ __device__ unsigned long long g_ia_prof[24];
 // and epilogue 86 % of the kernel; eight splitter warps (two per lane
 // quarter, half the columns each) cut the MMA's wait for them from 72k to
 // 12k cycles per CTA but left the epilogue at 95 % busy and the kernel no
-// faster (179 vs 172 us), so four stay.
+// faster (179 vs 172 us); eight splitter AND eight epilogue warps: 197 us,
+// every role ~95 % busy — the SM's issue slots are the limit, so four each.
 constexpr int IF_WARPS = 10;
 constexpr int IF_THREADS = 32 * IF_WARPS;
 
