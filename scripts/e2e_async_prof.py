@@ -7,6 +7,8 @@ from paper_1906_00091_b200 import DlrmConfig, Prefetcher, Sgd, init_model, train
 from paper_1906_00091_b200.rng import RandomBatchSource
 
 from bench import CONFIGS
+if os.environ.get("SWITCH"):
+    sys.setswitchinterval(float(os.environ["SWITCH"]))
 threads = int(os.environ.get("THREADS", 4))
 c = CONFIGS[os.environ.get("CONFIG", "c3")]
 B = c["batch"]
