@@ -221,6 +221,13 @@ int dlrm_linear_bwd_data_wlo(const float* gZ, int64_t ldg, const float* W,
  * multiple of 4, 16-byte aligned buffers. */
 int dlrm_tf32_split_lo(const float* x, float* lo, int64_t n, dlrm_stream_t stream);
 
+/* Input staging: on `stream`, wait for wait_ev (if any), copy `bytes` from
+ * pinned host memory to the device, then record ev1 / ev2 (if any; CUDA
+ * event handles).  The Python packer calls it right after packing a batch,
+ * without the interpreter lock. */
+int dlrm_h2d_async(void* dst, const void* src, size_t bytes, void* wait_ev, void* ev1,
+                   void* ev2, dlrm_stream_t stream);
+
 size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N, int64_t K);
 
 /* dW = gZ^T X (N x K), db = column sums of gZ (ref mlp_backward,

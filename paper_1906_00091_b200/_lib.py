@@ -79,6 +79,7 @@ _SIGS = {
     "dlrm_linear_bwd_data_wlo": [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                                  _i64, _i64, _i64, _vp],
     "dlrm_tf32_split_lo": [_vp, _vp, _i64, _vp],
+    "dlrm_h2d_async": [_vp, _vp, C.c_size_t, _vp, _vp, _vp, _vp],
     "dlrm_linear_bwd_weight": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp,
                                _i64, _vp, _vp, _i64, _vp, _f32, _vp, _vp,
                                _sz, _vp],
@@ -159,6 +160,9 @@ def pylib():
             po = C.py_object
             f.argtypes = [po, po, po, po, po, _vp, _vp, _i64, _i64, _i64, _i32, _vp, _i32]
             f.restype = C.c_int
+            g = L.dlrm_pack_stage_py
+            g.argtypes = f.argtypes + [_vp, C.c_size_t, _vp, _vp, _vp, _vp, _vp]
+            g.restype = C.c_int
             _pylib = L
     return _pylib or None
 

@@ -74,6 +74,17 @@ static int update_dense(float* p, const float* g, int64_t n, const Upd& u,
   return check_launch("update_dense_kernel");
 }
 
+extern "C" int dlrm_h2d_async(void* dst, const void* src, size_t bytes, void* wait_ev,
+                              void* ev1, void* ev2, dlrm_stream_t stream) {
+  DLRM_REQUIRE(dst && src, "bad h2d arguments");
+  cudaStream_t s = as_stream(stream);
+  if (wait_ev) DLRM_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(wait_ev), 0));
+  DLRM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  if (ev1) DLRM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev1), s));
+  if (ev2) DLRM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev2), s));
+  return 0;
+}
+
 extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
                               const int32_t* err_flag, dlrm_stream_t stream) {
   return update_dense(p, g, n, sgd_rule(lr), err_flag, stream);

@@ -46,10 +46,38 @@ static int get_vec(PyObject* o, Py_buffer* v, char a, char b, Py_ssize_t n) {
   return 0;
 }
 
+/* The staging half (optional): after packing, still without the GIL, the
+ * block's H2D copy is issued on `stream` (after wait_ev) and ev1 / ev2
+ * recorded (dlrm_h2d_async); nnz_out (optional) receives the per-table index
+ * counts. */
+static int pack_impl(PyObject* dense, PyObject* labels, PyObject* offsets, PyObject* indices,
+                     PyObject* weights, uint8_t* dst, const int64_t* sec, int64_t batch,
+                     int64_t k0, int64_t ldx, int32_t nt, const int64_t* cap_base,
+                     int32_t nthreads, void* dev_dst, size_t bytes, void* wait_ev, void* ev1,
+                     void* ev2, void* stream, int64_t* nnz_out);
+
 int dlrm_pack_batch_py(PyObject* dense, PyObject* labels, PyObject* offsets, PyObject* indices,
                        PyObject* weights, uint8_t* dst, const int64_t* sec, int64_t batch,
                        int64_t k0, int64_t ldx, int32_t nt, const int64_t* cap_base,
                        int32_t nthreads) {
+  return pack_impl(dense, labels, offsets, indices, weights, dst, sec, batch, k0, ldx, nt,
+                   cap_base, nthreads, NULL, 0, NULL, NULL, NULL, NULL, NULL);
+}
+
+int dlrm_pack_stage_py(PyObject* dense, PyObject* labels, PyObject* offsets, PyObject* indices,
+                       PyObject* weights, uint8_t* dst, const int64_t* sec, int64_t batch,
+                       int64_t k0, int64_t ldx, int32_t nt, const int64_t* cap_base,
+                       int32_t nthreads, void* dev_dst, size_t bytes, void* wait_ev, void* ev1,
+                       void* ev2, void* stream, int64_t* nnz_out) {
+  return pack_impl(dense, labels, offsets, indices, weights, dst, sec, batch, k0, ldx, nt,
+                   cap_base, nthreads, dev_dst, bytes, wait_ev, ev1, ev2, stream, nnz_out);
+}
+
+static int pack_impl(PyObject* dense, PyObject* labels, PyObject* offsets, PyObject* indices,
+                     PyObject* weights, uint8_t* dst, const int64_t* sec, int64_t batch,
+                     int64_t k0, int64_t ldx, int32_t nt, const int64_t* cap_base,
+                     int32_t nthreads, void* dev_dst, size_t bytes, void* wait_ev, void* ev1,
+                     void* ev2, void* stream, int64_t* nnz_out) {
   if (nt < 1 || nt > MAXT) return 1;
   PyObject* fo = PySequence_Fast(offsets, "offsets");
   PyObject* fi = fo ? PySequence_Fast(indices, "indices") : NULL;
@@ -122,11 +150,18 @@ int dlrm_pack_batch_py(PyObject* dense, PyObject* labels, PyObject* offsets, PyO
     const double* dp = (const double*)bd.buf;
     const int64_t ldd = bd.strides[0] / 8;
     const double* lp = (const double*)bl.buf;
-    int r;
+    int r, h = 0;
     Py_BEGIN_ALLOW_THREADS
     r = dlrm_pack_batch(dst, sec, batch, k0, ldx, nt, cap_base, dp, ldd, lp, po, pi, nnz,
                         fw ? pw : NULL, nthreads);
+    if (r == 0 && dev_dst) h = dlrm_h2d_async(dev_dst, dst, bytes, wait_ev, ev1, ev2, stream);
     Py_END_ALLOW_THREADS
+    if (r == 0 && h != 0) {
+      PyErr_SetString(PyExc_RuntimeError, dlrm_last_error());
+      rc = -1;
+      goto out;
+    }
+    if (r == 0 && nnz_out) memcpy(nnz_out, nnz, sizeof(int64_t) * (size_t)nt);
     rc = r == 0 ? 0 : 1;
   }
 out:

@@ -22,6 +22,7 @@ Here:
 
 from __future__ import annotations
 
+import os
 import queue
 import threading
 from concurrent.futures import ThreadPoolExecutor
@@ -216,6 +217,9 @@ class InputLayout:
 # ----------------------------------------------------------------------------
 # staged-batch handles (what a Prefetcher yields in place of the arrays)
 
+_STAGE_NATIVE = os.environ.get("DLRM_PF_NATIVE", "1") != "0"
+
+
 class _Slot:
     def __init__(self, layout: InputLayout, device):
         self.host = layout.new_host_block()
@@ -224,6 +228,12 @@ class _Slot:
         self.ready = torch.cuda.Event()      # device block holds the batch
         self.consumed = torch.cuda.Event()   # the step copied it out
         self.consumed_set = False
+        # CUDA events exist once recorded (torch creates them lazily): the
+        # native stager records into their handles
+        s = torch.cuda.current_stream(device)
+        self.h2d_done.record(s)
+        self.ready.record(s)
+        self.nnz = np.zeros(layout.T, dtype=np.int64)
 
 
 class StagedDense:
@@ -319,9 +329,28 @@ class Prefetcher:
             self._done[seq] = item
             self._cv.notify_all()
 
+    def _stage_native(self, slot, stream, sh, dense, offs, idx, labels, weights) -> bool:
+        """Pack + H2D + event records in one native call without the
+        interpreter lock (libdlrmpy.so); False when unavailable or the arrays
+        are not the reference's dtypes (then the Python path stages)."""
+        PL = _lib.pylib() if _STAGE_NATIVE else None
+        L = self.layout
+        if PL is None or (weights is not None and any(w is not None for w in weights)
+                          and not L.weighted):
+            return False
+        rc = PL.dlrm_pack_stage_py(
+            dense, labels, offs, idx, weights, slot.host.data_ptr(), L._sec.ctypes.data, L.B,
+            L.k0, _ceil4(L.k0), L.T, L._cap_base_ptr, int(self._pool._max_workers),
+            slot.dev.data_ptr(), L.nbytes, slot.consumed if slot.consumed_set else None,
+            slot.h2d_done, slot.ready, sh, slot.nnz.ctypes.data)
+        if rc >= 2:
+            L.check(idx, weights)  # raises the OverflowError
+        return rc == 0
+
     def _run(self):
         torch.cuda.set_device(self.device)
         stream = torch.cuda.Stream(device=self.device)
+        sh = _lib.stream_handle(stream)
         while not self._stop:
             slot = self._free.get()
             if slot is None:
@@ -347,17 +376,18 @@ class Prefetcher:
                     self._publish(seq, None)
                     return
             try:
-                if slot.consumed_set:
-                    stream.wait_event(slot.consumed)   # the step copied it out
                 slot.h2d_done.synchronize()             # the host block is free
                 dense, offs, idx, labels, weights = hb
-                self.layout.pack(slot.host, dense, offs, idx, labels, weights, self._pool)
-                with torch.cuda.stream(stream):
-                    slot.dev.copy_(slot.host, non_blocking=True)
-                    slot.h2d_done.record(stream)
-                    slot.ready.record(stream)
-                nnz = [int(np.asarray(i).shape[0]) for i in idx]
-                self._publish(seq, (slot, nnz, weights is not None))
+                if not self._stage_native(slot, stream, sh, dense, offs, idx, labels, weights):
+                    if slot.consumed_set:
+                        stream.wait_event(slot.consumed)   # the step copied it out
+                    self.layout.pack(slot.host, dense, offs, idx, labels, weights, self._pool)
+                    with torch.cuda.stream(stream):
+                        slot.dev.copy_(slot.host, non_blocking=True)
+                        slot.h2d_done.record(stream)
+                        slot.ready.record(stream)
+                    slot.nnz[:] = [int(np.asarray(i).shape[0]) for i in idx]
+                self._publish(seq, (slot, slot.nnz.tolist(), weights is not None))
             except BaseException as e:
                 self._free.put(slot)
                 self._publish(seq, e)

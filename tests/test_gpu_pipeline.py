@@ -59,3 +59,33 @@ def test_prefetcher_overflow_raises():
     with pytest.raises(OverflowError):
         for d, b, l in pf:
             train_step(init_model(cfg), d, b, l, Sgd(0.1))
+
+
+def test_native_and_python_staging_give_the_same_blocks():
+    """The native stager (pack + H2D + event records in one call without
+    the interpreter lock) and the Python staging path put identical input
+    blocks on the device, in source order."""
+    from paper_1906_00091_b200 import pipeline
+    cfg = _cfg()
+    src = RandomBatchSource(cfg.embedding_sizes, 13, 128, 5, False, seed=9)
+    batches = [src.next_batch() for _ in range(6)]
+    caps = [max(len(hb.indices[t]) for hb in batches) for t in range(4)]
+    blocks = {}
+    for native in (True, False):
+        saved, pipeline._STAGE_NATIVE = pipeline._STAGE_NATIVE, native
+        try:
+            pf = Prefetcher(iter(batches), 128, 4, 13, capacities=caps, depth=3, threads=2)
+            got = []
+            for d, b, l in pf:
+                out = torch.empty_like(d._slot.dev)
+                d.consume(out)
+                torch.cuda.synchronize()
+                got.append((out.cpu(), [sb.nnz for sb in b]))
+            pf.close()
+        finally:
+            pipeline._STAGE_NATIVE = saved
+        blocks[native] = got
+    assert len(blocks[True]) == len(blocks[False]) == 6
+    for (a, na), (b, nb) in zip(blocks[True], blocks[False]):
+        assert torch.equal(a, b) and na == nb
+    assert [n for _, n in blocks[True]] == [[len(i) for i in hb.indices] for hb in batches]
