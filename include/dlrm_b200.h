@@ -228,6 +228,19 @@ int dlrm_tf32_split_lo(const float* x, float* lo, int64_t n, dlrm_stream_t strea
 int dlrm_h2d_async(void* dst, const void* src, size_t bytes, void* wait_ev, void* ev1,
                    void* ev2, dlrm_stream_t stream);
 
+/* Device-to-device copy on `stream` after wait_ev, then ev recorded (the
+ * staged input block handed to the step engine in one call). */
+int dlrm_d2d_async(void* dst, const void* src, size_t bytes, void* wait_ev, void* ev,
+                   dlrm_stream_t stream);
+
+/* A step's result read-back on `stream` in one call: the result block to
+ * pinned host memory, the probabilities device to device, then `ev`
+ * recorded (the engine's asynchronous results; one call instead of three
+ * runtime calls from the training thread). */
+int dlrm_step_result_copy(void* host_dst, const void* res, size_t res_bytes, void* prob_dst,
+                          const void* prob, size_t prob_bytes, void* ev,
+                          dlrm_stream_t stream);
+
 size_t dlrm_linear_bwd_weight_workspace_size(int64_t M, int64_t N, int64_t K);
 
 /* dW = gZ^T X (N x K), db = column sums of gZ (ref mlp_backward,

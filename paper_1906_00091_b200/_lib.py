@@ -80,6 +80,8 @@ _SIGS = {
                                  _i64, _i64, _i64, _vp],
     "dlrm_tf32_split_lo": [_vp, _vp, _i64, _vp],
     "dlrm_h2d_async": [_vp, _vp, C.c_size_t, _vp, _vp, _vp, _vp],
+    "dlrm_step_result_copy": [_vp, _vp, C.c_size_t, _vp, _vp, C.c_size_t, _vp, _vp],
+    "dlrm_d2d_async": [_vp, _vp, C.c_size_t, _vp, _vp, _vp],
     "dlrm_linear_bwd_weight": [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp,
                                _i64, _vp, _vp, _i64, _vp, _f32, _vp, _vp,
                                _sz, _vp],

@@ -85,6 +85,28 @@ extern "C" int dlrm_h2d_async(void* dst, const void* src, size_t bytes, void* wa
   return 0;
 }
 
+extern "C" int dlrm_d2d_async(void* dst, const void* src, size_t bytes, void* wait_ev, void* ev,
+                              dlrm_stream_t stream) {
+  DLRM_REQUIRE(dst && src, "bad d2d arguments");
+  cudaStream_t s = as_stream(stream);
+  if (wait_ev) DLRM_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(wait_ev), 0));
+  DLRM_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+  if (ev) DLRM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), s));
+  return 0;
+}
+
+extern "C" int dlrm_step_result_copy(void* host_dst, const void* res, size_t res_bytes,
+                                     void* prob_dst, const void* prob, size_t prob_bytes,
+                                     void* ev, dlrm_stream_t stream) {
+  DLRM_REQUIRE(host_dst && res, "bad result copy arguments");
+  cudaStream_t s = as_stream(stream);
+  DLRM_CUDA(cudaMemcpyAsync(host_dst, res, res_bytes, cudaMemcpyDeviceToHost, s));
+  if (prob_dst && prob_bytes)
+    DLRM_CUDA(cudaMemcpyAsync(prob_dst, prob, prob_bytes, cudaMemcpyDeviceToDevice, s));
+  if (ev) DLRM_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), s));
+  return 0;
+}
+
 extern "C" int dlrm_sgd_dense(float* p, const float* g, int64_t n, float lr,
                               const int32_t* err_flag, dlrm_stream_t stream) {
   return update_dense(p, g, n, sgd_rule(lr), err_flag, stream);

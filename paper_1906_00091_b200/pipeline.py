@@ -233,6 +233,7 @@ class _Slot:
         s = torch.cuda.current_stream(device)
         self.h2d_done.record(s)
         self.ready.record(s)
+        self.consumed.record(s)
         self.nnz = np.zeros(layout.T, dtype=np.int64)
 
 
@@ -246,15 +247,11 @@ class StagedDense:
     def consume(self, engine_block: torch.Tensor, stream=None):
         """Copy the landed block into the engine's input block on ``stream``
         (after the H2D copy) and release the ring slot."""
-        cur = torch.cuda.current_stream()
-        s = stream or cur
-        s.wait_event(self._slot.ready)
-        if s == cur:
-            engine_block.copy_(self._slot.dev, non_blocking=True)
-        else:
-            with torch.cuda.stream(s):
-                engine_block.copy_(self._slot.dev, non_blocking=True)
-        self._slot.consumed.record(s)
+        s = stream or torch.cuda.current_stream()
+        # wait for the H2D, copy, record `consumed`: one native call
+        _lib.call("dlrm_d2d_async", _lib.ptr(engine_block), _lib.ptr(self._slot.dev),
+                  self._layout.nbytes, self._slot.ready, self._slot.consumed,
+                  _lib.stream_handle(s))
         self._slot.consumed_set = True
         self._pf._release(self._slot)
 

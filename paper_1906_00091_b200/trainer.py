@@ -895,6 +895,8 @@ class StepEngine:
             self._prob_ring = torch.zeros((R, self.B), dtype=torch.float32, device=self.dev)
             self._ring_owner = [None] * R
             self._ev = [torch.cuda.Event() for _ in range(R)]
+            for ev in self._ev:
+                ev.record(s)  # creates the CUDA events (recorded natively below)
             self._ring_next = 0
         k = self._ring_next
         self._ring_next = (k + 1) % self.RING
@@ -903,9 +905,9 @@ class StepEngine:
             old = old()
             if old is not None:  # an unread result still owns the slot
                 old._release_slot()
-        self._ring[k].copy_(self.res_dev, non_blocking=True)
-        self._prob_ring[k].copy_(self.prob)
-        self._ev[k].record(s)
+        _lib.call("dlrm_step_result_copy", C.c_void_p(self._ring[k].data_ptr()),
+                  _lib.ptr(self.res_dev), 4 * n, _lib.ptr(self._prob_ring[k]),
+                  _lib.ptr(self.prob), 4 * self.B, self._ev[k], _lib.stream_handle(s))
         res = PendingStepResult(self, k, self._ev[k])
         self._ring_owner[k] = weakref.ref(res)
         return res
