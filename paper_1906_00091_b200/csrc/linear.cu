@@ -140,6 +140,14 @@ skinny_wgrad_final_kernel(const float* __restrict__ part, int S, int64_t N, int 
 // phases are added in phase order in shared memory, the slab partials by
 // skinny_wgrad_final4_kernel (a warp per output, fixed-order tree).
 constexpr int kSkVCols = 512, kSkVPhases = 4;
+#ifndef DLRM_SKV_U
+#define DLRM_SKV_U 8
+#endif
+#ifndef DLRM_SKV_ROWS
+#define DLRM_SKV_ROWS 128
+#endif
+constexpr int kSkVU = DLRM_SKV_U;        // gZ rows in flight per thread
+constexpr int kSkVRows = DLRM_SKV_ROWS;  // X rows staged per chunk
 
 int skinny_v_slabs(int64_t M, int64_t N) {
   const int64_t cb = ceil_div(N, kSkVCols);
@@ -156,8 +164,8 @@ skinny_wgrad_partial4_kernel(const float* __restrict__ gZ, int64_t ldg,
                              int K, int64_t rows_per_slab, float* __restrict__ part) {
   pdl_entry();
   extern __shared__ float sk_smem[];
-  float* xs = sk_smem;                               // [kSkinnyRows][KM + 1]
-  float* red = sk_smem + kSkinnyRows * (KM + 1);     // [128][4 (KM + 1)]
+  float* xs = sk_smem;                               // [kSkVRows][KM + 1]
+  float* red = sk_smem + kSkVRows * (KM + 1);        // [128][4 (KM + 1)]
   const int ph = threadIdx.x >> 7, ct = threadIdx.x & 127;
   const int64_t n = int64_t(blockIdx.x) * kSkVCols + 4 * ct;
   const int64_t m0 = int64_t(blockIdx.y) * rows_per_slab;
@@ -168,8 +176,8 @@ skinny_wgrad_partial4_kernel(const float* __restrict__ gZ, int64_t ldg,
   for (int j = 0; j < 4; ++j)
 #pragma unroll
     for (int k = 0; k <= KM; ++k) acc[j][k] = 0.f;
-  for (int64_t mb = m0; mb < m1; mb += kSkinnyRows) {
-    const int cnt = int(m1 - mb < kSkinnyRows ? m1 - mb : kSkinnyRows);
+  for (int64_t mb = m0; mb < m1; mb += kSkVRows) {
+    const int cnt = int(m1 - mb < kSkVRows ? m1 - mb : kSkVRows);
     __syncthreads();
     for (int e = threadIdx.x; e < cnt * KM; e += 128 * kSkVPhases) {
       const int r = e / KM, k = e - r * KM;
@@ -178,10 +186,10 @@ skinny_wgrad_partial4_kernel(const float* __restrict__ gZ, int64_t ldg,
     __syncthreads();
     if (n < N) {
       // rows ph, ph + 4, ... of the chunk; four loads issued before use
-      for (int r0 = ph; r0 < cnt; r0 += 4 * kSkVPhases) {
-        float4 g[4];
+      for (int r0 = ph; r0 < cnt; r0 += kSkVU * kSkVPhases) {
+        float4 g[kSkVU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kSkVU; ++u) {
           const int r = r0 + u * kSkVPhases;
           const float* src = gZ + (mb + (r < cnt ? r : 0)) * ldg + n;
           if (r >= cnt) {
@@ -196,7 +204,7 @@ skinny_wgrad_partial4_kernel(const float* __restrict__ gZ, int64_t ldg,
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kSkVU; ++u) {
           const int r = r0 + u * kSkVPhases;
           if (r >= cnt) break;
           const float* xr = xs + r * (KM + 1);
@@ -282,7 +290,7 @@ int skinny_wgrad4(const float* gZ, int64_t ldg, const float* X, int64_t ldx, int
   const int S = skinny_v_slabs(M, N);
   const int64_t rows = ceil_div(M, S);
   auto kp = skinny_wgrad_partial4_kernel<KM>;
-  const size_t smem = size_t(kSkinnyRows * (KM + 1) + 128 * 4 * (KM + 1)) * 4;
+  const size_t smem = size_t(kSkVRows * (KM + 1) + 128 * 4 * (KM + 1)) * 4;
   static bool attr = false;
   if (!attr) {
     DLRM_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
